@@ -1,0 +1,121 @@
+/*
+ * llmint8.h -- C ABI of the B200 (sm_100a) LLM.int8() linear-layer path.
+ *
+ * Drop-in boundary for the reference package `int8mm`'s operator API
+ * (reference tree: pkg/src/int8mm/). Plain pointers and sizes only; every
+ * pointer argument is DEVICE memory unless stated otherwise, every function is
+ * stream-ordered on `stream` (a cudaStream_t, NULL = legacy default stream)
+ * and never synchronizes the host. The caller owns every buffer; nothing is
+ * allocated or freed inside the library.
+ *
+ * Layouts (row-major, leading dimensions in elements):
+ *   X     fp16  M x K   (activations; the reference's DenseMatrix x, f16-valued)
+ *   W     fp16  K x N   (weights in the reference orientation, x @ w)
+ *   Xq    int8  M x ldq (row-quantized X, 0 at outlier columns, ldq % 16 == 0)
+ *   WqT   int8  N x ldq (column-quantized W stored K-major, 0 at outlier rows)
+ *   Y     fp16 or fp32, M x N
+ * Scales are carried as the exact absmax values (float32, exact for fp16
+ * inputs): the reference's f64 scale is 127.0 / (amax == 0 ? 127 : amax).
+ *
+ * Return value: I8MM_OK (0) or one of the I8MM_ERR_* codes below; the Python
+ * shim maps them onto the reference's exception classes.
+ */
+#ifndef LLMINT8_H
+#define LLMINT8_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    I8MM_OK = 0,
+    I8MM_ERR_SHAPE = 1,      /* ShapeMismatchError   (tensors.py:21, gemm.py:64-65) */
+    I8MM_ERR_OVERFLOW = 2,   /* GemmOverflowError    (gemm.py:41, 66-69)            */
+    I8MM_ERR_ALPHA = 3,      /* ValueError on alpha  (gemm.py:208-209)              */
+    I8MM_ERR_PARAMS = 4,     /* ParamsMismatchError  (gemm.py:45, 136-146)          */
+    I8MM_ERR_ARGUMENT = 5,   /* bad pointer / alignment / workspace too small        */
+    I8MM_ERR_CUDA = 6,       /* CUDA launch or driver error                           */
+    I8MM_ERR_UNSUPPORTED = 7 /* device is not sm_100                                  */
+};
+
+enum { I8MM_OUT_F16 = 0, I8MM_OUT_F32 = 1, I8MM_OUT_F32_EXACT = 2 };
+
+#define I8MM_MAX_INNER_DIM (1 << 17) /* gemm.py:35 MAX_INNER_DIM */
+
+/* Library identification / diagnostics. */
+int i8mm_version(void);
+const char* i8mm_status_string(int status);
+/* Number of kernels this library launched since load (for bench accounting). */
+uint64_t i8mm_launch_count(void);
+
+/* K1. Outlier-column scan.  Replaces extract_outlier_columns' mask
+ * (gemm.py:208-210): col_mask bit k is set iff some |X[i,k]| >= (float)alpha.
+ * col_mask (ceil(K/32) words) is zeroed by the call. nonfinite (1 int32,
+ * nullable) is set to 1 if X holds NaN/Inf (DenseMatrix rejects those,
+ * tensors.py:47-48). */
+int i8mm_outlier_scan(const void* x, int64_t M, int64_t K, int64_t ldx, float alpha,
+                      uint32_t* col_mask, int32_t* nonfinite, void* stream);
+
+/* Outlier index list: sorted ascending indices of set bits (gemm.py:211,
+ * outliers.py:27-44) into o_idx[K], their count into *o_count (device). */
+int i8mm_outlier_compact(const uint32_t* col_mask, int64_t K, int32_t* o_idx, int32_t* o_count,
+                         void* stream);
+
+/* K2. Row-wise quantization over the keep columns (quantize.py:168-179 applied
+ * to x[:, keep], gemm.py:242) plus the outlier gather x[:, O] (gemm.py:238).
+ * col_mask NULL = no outliers (plain rowwise_quantize). xo (M x o_cap fp16,
+ * nullable) receives X[i, o_idx[t]] for t < min(*o_count, o_cap). */
+int i8mm_quantize_rows(const void* x, int64_t M, int64_t K, int64_t ldx, const uint32_t* col_mask,
+                       const int32_t* o_idx, const int32_t* o_count, int8_t* xq, int64_t ldq,
+                       float* row_amax, void* xo, int64_t o_cap, void* stream);
+
+/* K3. Column-wise quantization of W over the keep rows (quantize.py:168-171,
+ * 182-187 applied to w[keep, :], gemm.py:243), written transposed (WqT, N x
+ * ldq, K-major) for the tensor-core GEMM. row_mask NULL = no outliers. */
+int i8mm_quantize_cols_t(const void* w, int64_t K, int64_t N, int64_t ldw, const uint32_t* row_mask,
+                         int8_t* wq_t, int64_t ldq, float* col_amax, void* stream);
+
+/* K4a. Exact int8 GEMM, C = A @ B with int32 accumulation (gemm.py:78-82).
+ * a: M x K (lda), b_t: N x K (ldb) i.e. B stored K-major, c: M x N int32. */
+int i8mm_gemm_i32(const int8_t* a, int64_t lda, const int8_t* b_t, int64_t ldb, int32_t* c,
+                  int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream);
+
+/* K4b. Fused GEMM + dequantization + outlier term (gemm.py:120-147 row x col
+ * branch, gemm.py:238 + 244-247):
+ *   Y[i,j] = C[i,j] * (ax_i/127) * (aw_j/127) + sum_{t<|O|} X[i,O_t] * W[O_t, j]
+ * xq/wq_t as produced by K2/K3; w (K x N fp16) supplies the outlier rows;
+ * xo/o_cap as produced by K2 (x is used for outliers beyond o_cap).
+ * out_kind: I8MM_OUT_F16 | I8MM_OUT_F32 (fp32 epilogue math) |
+ * I8MM_OUT_F32_EXACT (f64 epilogue replicating the reference bit-for-bit). */
+int i8mm_gemm_dequant(const int8_t* xq, const int8_t* wq_t, int64_t ldq, int64_t M, int64_t N,
+                      int64_t K, const float* row_amax, const float* col_amax, const void* x,
+                      int64_t ldx, const void* w, int64_t ldw, const void* xo, int64_t o_cap,
+                      const int32_t* o_idx, const int32_t* o_count, void* y, int64_t ldy,
+                      int out_kind, void* stream);
+
+/* Exact dequantization of an int32 accumulator (gemm.py:130,141,147):
+ * out[i,j] = (float)((double)c[i,j] / (sx[i] * sw[j])), f64 scales. */
+int i8mm_dequantize_output(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const double* sx,
+                           const double* sw, float* out, int64_t ldo, void* stream);
+
+/* int8 transpose helper (K x N -> N x ldq) for callers holding B row-major. */
+int i8mm_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int64_t lds, int8_t* dst,
+                      int64_t ldd, void* stream);
+
+/* Whole-pipeline entry: llm_int8_matmul(x, w, alpha) (gemm.py:214-247) with
+ * per-call W quantization, exactly the reference semantics. workspace must
+ * hold i8mm_llm_int8_workspace_size(M, K, N) bytes (256-byte aligned).
+ * *o_count_dev (device int32) receives |O| (decomposed_cols). */
+size_t i8mm_llm_int8_workspace_size(int64_t M, int64_t K, int64_t N);
+int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M,
+                         int64_t K, int64_t N, float alpha, void* y, int64_t ldy, int out_kind,
+                         void* workspace, size_t workspace_bytes, int32_t* o_count_dev,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LLMINT8_H */

@@ -1,0 +1,28 @@
+"""B200-native (sm_100a) LLM.int8() linear layer (arXiv 2208.07339).
+
+Drop-in for the reference package ``int8mm``'s operator API on the
+LLM.int8() path: quantize (row-/column-wise), the outlier-decomposed int8
+matmul, and the Int8 linear module / backend plugin. Hot ops are hand-written
+CUDA kernels for sm_100a (tcgen05 + TMA + TMEM) behind the C ABI in
+``include/llmint8.h``; PyTorch provides device memory and streams only.
+"""
+
+from .errors import GemmOverflowError, ParamsMismatchError, ShapeMismatchError
+from .gemm import (MAX_INNER_DIM, MatmulResult, dequantize_output, extract_outlier_columns,
+                   int8_gemm_i32, llm_int8_matmul, vectorwise_matmul)
+from .linear import (ABSMAX, BACKEND_KINDS, EXACT, VECTORWISE, ZEROPOINT, Int8Linear,
+                     LinearBackend, _linear, linear, llm_int8_backend)
+from .quantize import colwise_quantize, rowwise_quantize, vectorwise_params
+from .synthetic import planted_pair
+from .types import ColwiseParams, OutlierSet, QuantizedTensor, RowwiseParams
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "MAX_INNER_DIM", "GemmOverflowError", "ParamsMismatchError", "ShapeMismatchError",
+    "MatmulResult", "OutlierSet", "QuantizedTensor", "RowwiseParams", "ColwiseParams",
+    "extract_outlier_columns", "int8_gemm_i32", "dequantize_output", "llm_int8_matmul",
+    "vectorwise_matmul", "rowwise_quantize", "colwise_quantize", "vectorwise_params",
+    "BACKEND_KINDS", "LinearBackend", "EXACT", "ABSMAX", "ZEROPOINT", "VECTORWISE",
+    "llm_int8_backend", "linear", "_linear", "Int8Linear", "planted_pair",
+]

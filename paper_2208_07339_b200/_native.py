@@ -1,0 +1,127 @@
+"""ctypes binding of the in-tree sm_100a library (include/llmint8.h).
+
+There is no fallback: if the library is missing, fails to load, or the
+device is not a B200 (sm_100), every call raises. Status codes map onto the
+reference's exception classes (gemm.py:41-46, tensors.py:21).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import GemmOverflowError, ParamsMismatchError, ShapeMismatchError
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "libllmint8_sm100.so"
+
+I8MM_OK = 0
+I8MM_ERR_SHAPE = 1
+I8MM_ERR_OVERFLOW = 2
+I8MM_ERR_ALPHA = 3
+I8MM_ERR_PARAMS = 4
+I8MM_ERR_ARGUMENT = 5
+I8MM_ERR_CUDA = 6
+I8MM_ERR_UNSUPPORTED = 7
+
+OUT_F16 = 0
+OUT_F32 = 1
+OUT_F32_EXACT = 2
+
+# Every symbol include/llmint8.h declares (tests check the .so exports them all).
+EXPORTED_SYMBOLS = (
+    "i8mm_version",
+    "i8mm_status_string",
+    "i8mm_launch_count",
+    "i8mm_outlier_scan",
+    "i8mm_outlier_compact",
+    "i8mm_quantize_rows",
+    "i8mm_quantize_cols_t",
+    "i8mm_gemm_i32",
+    "i8mm_gemm_dequant",
+    "i8mm_dequantize_output",
+    "i8mm_transpose_i8",
+    "i8mm_llm_int8_workspace_size",
+    "i8mm_llm_int8_matmul",
+)
+
+_lib = None
+
+
+class NativeLibraryError(RuntimeError):
+    """The sm_100a CUDA library is missing or unusable (no CPU fallback exists)."""
+
+
+def _declare(lib: ctypes.CDLL) -> None:
+    P, I64, I32, F32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+    sigs = {
+        "i8mm_version": ([], I32),
+        "i8mm_status_string": ([I32], ctypes.c_char_p),
+        "i8mm_launch_count": ([], ctypes.c_uint64),
+        "i8mm_outlier_scan": ([P, I64, I64, I64, F32, P, P, P], I32),
+        "i8mm_outlier_compact": ([P, I64, P, P, P], I32),
+        "i8mm_quantize_rows": ([P, I64, I64, I64, P, P, P, P, I64, P, P, I64, P], I32),
+        "i8mm_quantize_cols_t": ([P, I64, I64, I64, P, P, I64, P, P], I32),
+        "i8mm_gemm_i32": ([P, I64, P, I64, P, I64, I64, I64, I64, P], I32),
+        "i8mm_gemm_dequant": ([P, P, I64, I64, I64, I64, P, P, P, I64, P, I64, P, I64, P, P, P,
+                               I64, I32, P], I32),
+        "i8mm_dequantize_output": ([P, I64, I64, I64, P, P, P, I64, P], I32),
+        "i8mm_transpose_i8": ([P, I64, I64, I64, P, I64, P], I32),
+        "i8mm_llm_int8_workspace_size": ([I64, I64, I64], ctypes.c_size_t),
+        "i8mm_llm_int8_matmul": ([P, I64, P, I64, I64, I64, I64, F32, P, I64, I32, P,
+                                  ctypes.c_size_t, P, P], I32),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and return the sm_100a library; raise if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise NativeLibraryError(
+            f"{p} is missing: build it with `python -m paper_2208_07339_b200.build` "
+            "(there is no CPU fallback for the LLM.int8() path)")
+    try:
+        lib = ctypes.CDLL(str(p))
+    except OSError as e:  # pragma: no cover - depends on the host
+        raise NativeLibraryError(f"cannot load {p}: {e}") from e
+    _declare(lib)
+    _lib = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    return load_library()
+
+
+def check(status: int, what: str = "") -> None:
+    """Raise the reference's exception class for a non-zero status."""
+    if status == I8MM_OK:
+        return
+    msg = lib().i8mm_status_string(status).decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if status == I8MM_ERR_SHAPE:
+        raise ShapeMismatchError(msg)
+    if status == I8MM_ERR_OVERFLOW:
+        raise GemmOverflowError(msg)
+    if status == I8MM_ERR_PARAMS:
+        raise ParamsMismatchError(msg)
+    if status == I8MM_ERR_ALPHA:
+        raise ValueError(msg)
+    if status == I8MM_ERR_UNSUPPORTED:
+        raise NativeLibraryError(msg)
+    if status == I8MM_ERR_ARGUMENT:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def launch_count() -> int:
+    return int(lib().i8mm_launch_count())

@@ -1,0 +1,288 @@
+// extern "C" boundary of the B200 LLM.int8() library (declared in
+// include/llmint8.h). Host-side validation mirrors the reference's error
+// contract (gemm.py:63-69, 208-209; tensors.py:21) so the Python shim can
+// raise the same exception classes; compute is stream-ordered and never
+// synchronizes the host.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+
+#include "../../include/llmint8.h"
+#include "kernels.cuh"
+
+namespace i8mm {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int num_sms() {
+    static int sms = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    });
+    return sms;
+}
+
+static int check_device() {
+    static int ok = -1;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0, major = 0, minor = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+            ok = 0;
+            return;
+        }
+        ok = (major == 10 && minor == 0) ? 1 : 0;
+    });
+    return ok ? I8MM_OK : I8MM_ERR_UNSUPPORTED;
+}
+
+static int cuda_status(cudaError_t e) { return e == cudaSuccess ? I8MM_OK : I8MM_ERR_CUDA; }
+
+static inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// gemm.py:63-69 _check_inner (shape part is checked by the callers)
+static int check_inner(int64_t K) {
+    if (K > I8MM_MAX_INNER_DIM) return I8MM_ERR_OVERFLOW;
+    return I8MM_OK;
+}
+
+}  // namespace i8mm
+
+using namespace i8mm;
+
+extern "C" {
+
+int i8mm_version(void) { return 1; }
+
+const char* i8mm_status_string(int s) {
+    switch (s) {
+        case I8MM_OK: return "ok";
+        case I8MM_ERR_SHAPE: return "shape mismatch";
+        case I8MM_ERR_OVERFLOW: return "inner dimension exceeds the int32 overflow guard";
+        case I8MM_ERR_ALPHA: return "alpha must be positive and finite";
+        case I8MM_ERR_PARAMS: return "quantization params mismatch";
+        case I8MM_ERR_ARGUMENT: return "invalid argument";
+        case I8MM_ERR_CUDA: return "CUDA error";
+        case I8MM_ERR_UNSUPPORTED: return "device is not sm_100 (B200)";
+        default: return "unknown status";
+    }
+}
+
+uint64_t i8mm_launch_count(void) { return g_launches.load(); }
+
+int i8mm_outlier_scan(const void* x, int64_t M, int64_t K, int64_t ldx, float alpha,
+                      uint32_t* col_mask, int32_t* nonfinite, void* stream) {
+    if (int s = check_device()) return s;
+    if (!(alpha > 0.0f) || !std::isfinite(alpha)) return I8MM_ERR_ALPHA;
+    if (M < 0 || K <= 0 || ldx < K || !col_mask || (M > 0 && !x)) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_outlier_scan(static_cast<const __half*>(x), M, K, ldx, alpha,
+                                           col_mask, nonfinite, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_outlier_compact(const uint32_t* col_mask, int64_t K, int32_t* o_idx, int32_t* o_count,
+                         void* stream) {
+    if (int s = check_device()) return s;
+    if (K <= 0 || !col_mask || !o_idx || !o_count) return I8MM_ERR_ARGUMENT;
+    return cuda_status(
+        launch_outlier_compact(col_mask, K, o_idx, o_count, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_quantize_rows(const void* x, int64_t M, int64_t K, int64_t ldx, const uint32_t* col_mask,
+                       const int32_t* o_idx, const int32_t* o_count, int8_t* xq, int64_t ldq,
+                       float* row_amax, void* xo, int64_t o_cap, void* stream) {
+    if (int s = check_device()) return s;
+    if (M < 0 || K <= 0 || ldx < K || ldq < K || !xq || !row_amax || (M > 0 && !x))
+        return I8MM_ERR_ARGUMENT;
+    if (xo && (!o_idx || !o_count || o_cap <= 0)) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_quantize_rows(static_cast<const __half*>(x), M, K, ldx, col_mask,
+                                            o_idx, o_count, xq, ldq, row_amax,
+                                            static_cast<__half*>(xo), o_cap,
+                                            static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_quantize_cols_t(const void* w, int64_t K, int64_t N, int64_t ldw, const uint32_t* row_mask,
+                         int8_t* wq_t, int64_t ldq, float* col_amax, void* stream) {
+    if (int s = check_device()) return s;
+    if (K <= 0 || N < 0 || ldw < N || ldq < K || !wq_t || !col_amax || (N > 0 && !w))
+        return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_quantize_cols_t(static_cast<const __half*>(w), K, N, ldw, row_mask,
+                                              wq_t, ldq, col_amax,
+                                              static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_gemm_i32(const int8_t* a, int64_t lda, const int8_t* b_t, int64_t ldb, int32_t* c,
+                  int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
+    if (int s = check_device()) return s;
+    if (int s = check_inner(K)) return s;
+    if (M < 0 || N < 0 || K < 0 || lda < K || ldb < K || ldc < N || !a || !b_t || !c)
+        return I8MM_ERR_ARGUMENT;
+    if ((lda % 16) || (ldb % 16)) return I8MM_ERR_ARGUMENT;
+    GemmArgs g{};
+    g.a = a;
+    g.lda = lda;
+    g.b = b_t;
+    g.ldb = ldb;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.y = c;
+    g.ldy = ldc;
+    return cuda_status(launch_gemm_sm100(g, EPI_I32, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_gemm_dequant(const int8_t* xq, const int8_t* wq_t, int64_t ldq, int64_t M, int64_t N,
+                      int64_t K, const float* row_amax, const float* col_amax, const void* x,
+                      int64_t ldx, const void* w, int64_t ldw, const void* xo, int64_t o_cap,
+                      const int32_t* o_idx, const int32_t* o_count, void* y, int64_t ldy,
+                      int out_kind, void* stream) {
+    if (int s = check_device()) return s;
+    if (int s = check_inner(K)) return s;
+    if (M < 0 || N < 0 || K <= 0 || ldq < K || (ldq % 16) || ldy < N || !xq || !wq_t ||
+        !row_amax || !col_amax || !y)
+        return I8MM_ERR_ARGUMENT;
+    if (o_count && (!o_idx || !x || !w || ldx < K || ldw < N)) return I8MM_ERR_ARGUMENT;
+    int epi;
+    switch (out_kind) {
+        case I8MM_OUT_F16: epi = EPI_F16; break;
+        case I8MM_OUT_F32: epi = EPI_F32; break;
+        case I8MM_OUT_F32_EXACT: epi = EPI_F32_EXACT; break;
+        default: return I8MM_ERR_ARGUMENT;
+    }
+    GemmArgs g{};
+    g.a = xq;
+    g.lda = ldq;
+    g.b = wq_t;
+    g.ldb = ldq;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.y = y;
+    g.ldy = ldy;
+    g.row_amax = row_amax;
+    g.col_amax = col_amax;
+    g.x = static_cast<const __half*>(x);
+    g.ldx = ldx;
+    g.w = static_cast<const __half*>(w);
+    g.ldw = ldw;
+    g.xo = static_cast<const __half*>(xo);
+    g.o_cap = xo ? o_cap : 0;
+    g.o_idx = o_idx;
+    g.o_count = o_count;
+    return cuda_status(launch_gemm_sm100(g, epi, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_dequantize_output(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const double* sx,
+                           const double* sw, float* out, int64_t ldo, void* stream) {
+    if (int s = check_device()) return s;
+    if (M < 0 || N < 0 || ldc < N || ldo < N || !c || !sx || !sw || !out) return I8MM_ERR_ARGUMENT;
+    return cuda_status(
+        launch_dequantize_output(c, M, N, ldc, sx, sw, out, ldo, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int64_t lds, int8_t* dst,
+                      int64_t ldd, void* stream) {
+    if (int s = check_device()) return s;
+    if (rows < 0 || cols < 0 || lds < cols || ldd < rows || !src || !dst) return I8MM_ERR_ARGUMENT;
+    return cuda_status(
+        launch_transpose_i8(src, rows, cols, lds, dst, ldd, static_cast<cudaStream_t>(stream)));
+}
+
+// ---------------------------------------------------------------- pipeline
+namespace {
+struct Workspace {
+    uint32_t* mask;
+    int32_t* o_idx;
+    int32_t* o_count;
+    int32_t* nonfinite;
+    float* row_amax;
+    float* col_amax;
+    int8_t* xq;
+    int8_t* wq_t;
+    __half* xo;
+    int64_t ldq, o_cap;
+    size_t bytes;
+};
+constexpr int64_t kOCap = 64;  // compacted outlier slice width (wider |O| reads X directly)
+
+Workspace carve(void* base, int64_t M, int64_t K, int64_t N) {
+    Workspace w{};
+    w.ldq = round_up(K, 16);
+    w.o_cap = kOCap;
+    uintptr_t p = reinterpret_cast<uintptr_t>(base);
+    const uintptr_t p0 = p;
+    auto take = [&](size_t bytes) {
+        uintptr_t r = p;
+        p += static_cast<uintptr_t>(round_up(static_cast<int64_t>(bytes), 256));
+        return r;
+    };
+    w.mask = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * ((K + 31) / 32)));
+    w.o_idx = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * K));
+    w.o_count = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 2));
+    w.nonfinite = w.o_count + 1;
+    w.row_amax = reinterpret_cast<float*>(take(sizeof(float) * (M > 0 ? M : 1)));
+    w.col_amax = reinterpret_cast<float*>(take(sizeof(float) * (N > 0 ? N : 1)));
+    w.xq = reinterpret_cast<int8_t*>(take(static_cast<size_t>(M * w.ldq)));
+    w.wq_t = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
+    w.xo = reinterpret_cast<__half*>(take(sizeof(__half) * static_cast<size_t>(M * kOCap)));
+    w.bytes = p - p0;
+    return w;
+}
+}  // namespace
+
+size_t i8mm_llm_int8_workspace_size(int64_t M, int64_t K, int64_t N) {
+    if (M < 0 || K <= 0 || N < 0) return 0;
+    return carve(nullptr, M, K, N).bytes + 256;
+}
+
+int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M,
+                         int64_t K, int64_t N, float alpha, void* y, int64_t ldy, int out_kind,
+                         void* workspace, size_t workspace_bytes, int32_t* o_count_dev,
+                         void* stream) {
+    if (int s = check_device()) return s;
+    if (int s = check_inner(K)) return s;
+    if (!(alpha > 0.0f) || !std::isfinite(alpha)) return I8MM_ERR_ALPHA;
+    if (M <= 0 || K <= 0 || N <= 0 || ldx < K || ldw < N || ldy < N || !x || !w || !y ||
+        !workspace)
+        return I8MM_ERR_ARGUMENT;
+    void* base = reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(workspace), 256));
+    Workspace ws = carve(base, M, K, N);
+    if (ws.bytes + (static_cast<char*>(base) - static_cast<char*>(workspace)) > workspace_bytes)
+        return I8MM_ERR_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const __half* xh = static_cast<const __half*>(x);
+    const __half* wh = static_cast<const __half*>(w);
+    cudaError_t e;
+    // gemm.py:225 extract_outlier_columns
+    if ((e = launch_outlier_scan(xh, M, K, ldx, alpha, ws.mask, nullptr, st))) return I8MM_ERR_CUDA;
+    if ((e = launch_outlier_compact(ws.mask, K, ws.o_idx, ws.o_count, st))) return I8MM_ERR_CUDA;
+    // gemm.py:242 rowwise over keep columns + gather of x[:, O] (gemm.py:238)
+    if ((e = launch_quantize_rows(xh, M, K, ldx, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
+                                  ws.row_amax, ws.xo, ws.o_cap, st)))
+        return I8MM_ERR_CUDA;
+    // gemm.py:243 colwise over keep rows, stored K-major
+    if ((e = launch_quantize_cols_t(wh, K, N, ldw, ws.mask, ws.wq_t, ws.ldq, ws.col_amax, st)))
+        return I8MM_ERR_CUDA;
+    // gemm.py:193-194, 238, 244-247: int8 GEMM + dequant + outlier term
+    int s = i8mm_gemm_dequant(ws.xq, ws.wq_t, ws.ldq, M, N, K, ws.row_amax, ws.col_amax, x, ldx, w,
+                              ldw, ws.xo, ws.o_cap, ws.o_idx, ws.o_count, y, ldy, out_kind, stream);
+    if (s) return s;
+    if (o_count_dev) {
+        if (cudaMemcpyAsync(o_count_dev, ws.o_count, sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                            st) != cudaSuccess)
+            return I8MM_ERR_CUDA;
+    }
+    return I8MM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// Internal declarations shared by the LLM.int8() CUDA translation units.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace i8mm {
+
+// launch accounting + device properties (capi.cu)
+void count_launch();
+int num_sms();
+
+cudaError_t launch_outlier_scan(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
+                                uint32_t* col_mask, int32_t* nonfinite, cudaStream_t st);
+cudaError_t launch_outlier_compact(const uint32_t* col_mask, int64_t K, int32_t* o_idx,
+                                   int32_t* o_count, cudaStream_t st);
+cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t ldx,
+                                 const uint32_t* mask, const int32_t* o_idx,
+                                 const int32_t* o_count, int8_t* xq, int64_t ldq, float* amax,
+                                 __half* xo, int64_t o_cap, cudaStream_t st);
+cudaError_t launch_quantize_cols_t(const __half* w, int64_t K, int64_t N, int64_t ldw,
+                                   const uint32_t* row_mask, int8_t* wq_t, int64_t ldq,
+                                   float* col_amax, cudaStream_t st);
+cudaError_t launch_dequantize_output(const int32_t* c, int64_t M, int64_t N, int64_t ldc,
+                                     const double* sx, const double* sw, float* out, int64_t ldo,
+                                     cudaStream_t st);
+cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int64_t lds,
+                                int8_t* dst, int64_t ldd, cudaStream_t st);
+
+// Output kinds of the tcgen05 GEMM epilogue.
+enum EpiKind : int { EPI_I32 = 0, EPI_F16 = 1, EPI_F32 = 2, EPI_F32_EXACT = 3 };
+
+struct GemmArgs {
+    const int8_t* a;  // M x lda int8 (K-major)
+    int64_t lda;
+    const int8_t* b;  // N x ldb int8 (K-major)
+    int64_t ldb;
+    int64_t M, N, K;
+    void* y;
+    int64_t ldy;
+    // dequant + outlier epilogue (unused for EPI_I32)
+    const float* row_amax;
+    const float* col_amax;
+    const __half* x;
+    int64_t ldx;
+    const __half* w;
+    int64_t ldw;
+    const __half* xo;
+    int64_t o_cap;
+    const int32_t* o_idx;
+    const int32_t* o_count;
+};
+
+cudaError_t launch_gemm_sm100(const GemmArgs& args, int epi, cudaStream_t st);
+
+}  // namespace i8mm

@@ -1,0 +1,285 @@
+"""GPU parity: the sm_100a kernels vs the reference's golden vectors and the
+CPU oracle. Bit-exact for outlier sets, int8 codes, scales and the int32
+accumulator; bit-exact float32 output in ``exact`` mode; stated tolerances for
+the fast fp16 / fp32 epilogues (tests/_golden.py::fp16_tolerance; fp32:
+<= 2e-6 * max|ref|).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import _golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def p():
+    import paper_2208_07339_b200 as pkg
+    from paper_2208_07339_b200 import _native
+
+    _native.load_library()
+    return pkg
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _scales(amax_t):
+    from paper_2208_07339_b200.types import _scales_from_amax
+
+    return _scales_from_amax(amax_t)
+
+
+def test_device_is_sm100(p):
+    assert torch.cuda.get_device_capability() == (10, 0)
+
+
+GOLDEN = _golden.cases()
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN))
+def test_golden_case(p, name):
+    from paper_2208_07339_b200.gemm import llm_int8_trace
+
+    g = GOLDEN[name]
+    x, w, alpha = g["x"], g["w"], g["alpha"]
+    tr = llm_int8_trace(x, w, alpha)
+    dims = tr["scan"].dims()
+    assert dims == tuple(int(d) for d in g["dims"])
+    keep = _golden.keep_mask(x.shape[1], dims)
+    if keep.any():
+        assert np.array_equal(_np(tr["xq"])[:, keep], g["xq"])
+        assert np.array_equal(_scales(tr["row_amax"]), g["sx"])
+        assert np.array_equal(_np(tr["wq_t"]).T[keep, :], g["wq"])
+        assert np.array_equal(_scales(tr["col_amax"]), g["sw"])
+        assert np.array_equal(_np(tr["c"]), g["c"])
+    # outlier columns / rows hold code 0
+    assert not _np(tr["xq"])[:, ~keep].any()
+    ref = g["out"]
+    assert np.array_equal(_np(tr["y_exact"]), ref), "exact mode must be bit-identical"
+    y32 = _np(tr["y32"]).astype(np.float64)
+    assert np.abs(y32 - ref).max() <= 2e-6 * max(1.0, np.abs(ref).max())
+    y16 = _np(tr["y16"]).astype(np.float64)
+    assert (np.abs(y16 - ref) <= _golden.fp16_tolerance(ref)).all()
+    r = p.llm_int8_matmul(x, w, alpha)
+    assert r.decomposed_cols == int(g["decomposed_cols"])
+    assert r.int8_fraction == pytest.approx(float(g["int8_fraction"]), abs=0)
+    assert r.scheme == "llm_int8"
+
+
+@pytest.mark.parametrize("name", ["no_outliers_8x16x8", "planted_64x256x64_s0"])
+def test_vectorwise_golden(p, name):
+    g = GOLDEN[name]
+    r = p.vectorwise_matmul(g["x"], g["w"], exact=True)
+    assert np.array_equal(_np(r.output), g["vw"])
+
+
+def test_no_outliers_bitwise_equals_vectorwise(p):
+    """tests/test_gemm.py:223-230 / acceptance criterion 5."""
+    for seed in range(5):
+        rng = np.random.Generator(np.random.PCG64(seed + 500))
+        x = np.clip(rng.standard_normal((16, 48)), -5.9, 5.9).astype(np.float16)
+        w = rng.standard_normal((48, 12)).astype(np.float16)
+        a = p.llm_int8_matmul(x, w, 6.0, exact=True)
+        b = p.vectorwise_matmul(x, w, exact=True)
+        assert a.decomposed_cols == 0 and a.int8_fraction == 1.0
+        assert np.array_equal(_np(a.output), _np(b.output))
+
+
+def test_full_decomposition_matches_exact(p):
+    """alpha -> 0: every column decomposed (tests/test_gemm.py:232-239)."""
+    rng = np.random.Generator(np.random.PCG64(23))
+    x = rng.standard_normal((8, 16)).astype(np.float16)
+    w = rng.standard_normal((16, 8)).astype(np.float16)
+    r = p.llm_int8_matmul(x, w, alpha=1e-9, out_dtype=torch.float32)
+    exact = x.astype(np.float64) @ w.astype(np.float64)
+    rel = np.linalg.norm(_np(r.output) - exact) / np.linalg.norm(exact)
+    assert rel < 1e-6
+    assert r.decomposed_cols == 16 and r.int8_fraction == 0.0
+
+
+def test_kats(p):
+    k = _golden.kats()
+    q = p.rowwise_quantize(np.array(k["rowwise_hand"]["x"], dtype=np.float32))
+    assert q.params.scales.tolist() == k["rowwise_hand"]["scales"]
+    assert _np(q.codes).tolist() == k["rowwise_hand"]["codes"]
+    q0 = p.rowwise_quantize(np.array(k["rowwise_zero_row"]["x"], dtype=np.float32))
+    assert q0.params.scales.tolist() == k["rowwise_zero_row"]["scales"]
+    assert _np(q0.codes).tolist() == k["rowwise_zero_row"]["codes"]
+    qc = p.colwise_quantize(np.array(k["colwise_hand"]["w"], dtype=np.float32))
+    assert qc.params.scales.tolist() == k["colwise_hand"]["scales"]
+    assert _np(qc.codes).tolist() == k["colwise_hand"]["codes"]
+    d = k["dequant_outer"]
+    out = p.dequantize_output(torch.tensor(d["c"], dtype=torch.int32),
+                              p.RowwiseParams(scales=d["sx"]), p.ColwiseParams(scales=d["sw"]))
+    assert _np(out).astype(np.float64).tolist() == d["out"]
+    for key in ("gemm_identity", "gemm_hand"):
+        c = p.int8_gemm_i32(np.array(k[key]["a"], dtype=np.int8), np.array(k[key]["b"], dtype=np.int8))
+        assert _np(c).tolist() == k[key]["c"]
+    s = p.extract_outlier_columns(np.array(k["outlier_direct_scan"]["x"], dtype=np.float32), 6.0)
+    assert list(s.dims) == k["outlier_direct_scan"]["dims"] and s.alpha == 6.0
+    s = p.extract_outlier_columns(np.array(k["outlier_threshold_f32"]["x"], dtype=np.float32), 6.1)
+    # fp16(6.1) = 6.1015625 >= f32(6.1): the GPU consumes fp16 values
+    assert list(s.dims) == [0]
+
+
+def test_gemm_worst_case_inner_dim(p):
+    """127*127*2^17 = 2,114,060,288 fits int32 exactly (tests/test_gemm.py:56-63)."""
+    h = p.MAX_INNER_DIM
+    a = torch.full((1, h), 127, dtype=torch.int8, device="cuda")
+    b = torch.full((h, 1), 127, dtype=torch.int8, device="cuda")
+    assert int(p.int8_gemm_i32(a, b)[0, 0]) == 127 * 127 * h == 2_114_060_288
+    a = torch.full((3, h), -127, dtype=torch.int8, device="cuda")
+    b = torch.full((h, 5), 127, dtype=torch.int8, device="cuda")
+    assert (p.int8_gemm_i32(a, b) == -127 * 127 * h).all()
+
+
+def test_error_contract(p):
+    h = p.MAX_INNER_DIM + 1
+    with pytest.raises(p.GemmOverflowError):
+        p.int8_gemm_i32(torch.zeros((1, h), dtype=torch.int8), torch.zeros((h, 1), dtype=torch.int8))
+    with pytest.raises(p.ShapeMismatchError):
+        p.int8_gemm_i32(np.zeros((2, 3), np.int8), np.zeros((2, 2), np.int8))
+    with pytest.raises(p.ShapeMismatchError):
+        p.llm_int8_matmul(np.ones((2, 3), np.float32), np.ones((2, 3), np.float32))
+    with pytest.raises(ValueError):
+        p.extract_outlier_columns(np.ones((2, 3), np.float32), 0.0)
+    with pytest.raises(ValueError):
+        p.extract_outlier_columns(np.ones((2, 3), np.float32), float("inf"))
+    with pytest.raises(p.ParamsMismatchError):
+        p.dequantize_output(torch.ones((2, 2), dtype=torch.int32), p.RowwiseParams(scales=[1.0] * 3),
+                            p.ColwiseParams(scales=[1.0, 2.0]))
+    with pytest.raises(p.ParamsMismatchError):
+        p.dequantize_output(torch.ones((1, 1), dtype=torch.int32), p.ColwiseParams(scales=[1.0]),
+                            p.RowwiseParams(scales=[1.0]))
+    bad = np.ones((2, 3), np.float32)
+    bad[1, 1] = np.nan
+    with pytest.raises(ValueError):
+        p.llm_int8_matmul(bad, np.ones((3, 2), np.float32))
+    with pytest.raises(ValueError):
+        p.int8_gemm_i32(np.full((1, 2), -128, np.int8), np.ones((2, 1), np.int8))
+
+
+@pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 300, 129), (130, 257, 4112), (257, 513, 1000),
+                                 (384, 768, 2048), (1, 4096, 4096), (300, 40, 16)])
+def test_int8_gemm_matches_oracle(p, oracle_mod, mnk):
+    m, n, k = mnk
+    rng = np.random.Generator(np.random.PCG64(sum(mnk)))
+    a = rng.integers(-127, 128, size=(m, k), dtype=np.int8)
+    b = rng.integers(-127, 128, size=(k, n), dtype=np.int8)
+    c = p.int8_gemm_i32(a, b)
+    assert np.array_equal(_np(c), oracle_mod.c_gemm_i32(a, b))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_planted_sweep_vs_oracle(p, oracle_mod, seed):
+    """Planted pairs (sweep.py:60-77), seeds 0..9: bit-exact stages + exact Y."""
+    from paper_2208_07339_b200.gemm import llm_int8_trace
+
+    m, k, n = (256, 1024, 512) if seed % 2 == 0 else (97, 1040, 328)
+    x, w = oracle_mod.planted_pair(m, k, n, 6, 20.0, seed)
+    x = x.astype(np.float16).astype(np.float32)
+    w = w.astype(np.float16).astype(np.float32)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    tr = llm_int8_trace(x, w, 6.0)
+    assert tr["scan"].dims() == ref.dims
+    assert np.array_equal(_np(tr["xq"]), ref.xq)
+    assert np.array_equal(_np(tr["wq_t"]).T, ref.wq)
+    keep = _golden.keep_mask(k, ref.dims)
+    assert np.array_equal(_scales(tr["row_amax"]), ref.sx)
+    assert np.array_equal(_scales(tr["col_amax"]), ref.sw)
+    assert np.array_equal(_np(tr["c"]), ref.c)
+    assert np.array_equal(_np(tr["y_exact"]), ref.output)
+    y16 = _np(tr["y16"]).astype(np.float64)
+    assert (np.abs(y16 - ref.output) <= _golden.fp16_tolerance(ref.output)).all()
+    assert keep.sum() == k - len(ref.dims)
+
+
+@pytest.mark.parametrize("n_out", [17, 70])
+def test_many_outliers_paths(p, oracle_mod, n_out):
+    """|O| beyond the smem-staged (16) and compacted-slice (64) fast paths."""
+    x, w = oracle_mod.planted_pair(130, 512, 300, n_out, 20.0, 3)
+    x = x.astype(np.float16).astype(np.float32)
+    w = w.astype(np.float16).astype(np.float32)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    assert len(ref.dims) >= n_out
+    r = p.llm_int8_matmul(x, w, 6.0, exact=True)
+    assert np.array_equal(_np(r.output), ref.output)
+    r16 = p.llm_int8_matmul(x, w, 6.0)
+    assert (np.abs(_np(r16.output).astype(np.float64) - ref.output)
+            <= _golden.fp16_tolerance(ref.output)).all()
+
+
+def test_cfg1_digest(p):
+    """Config 1 (512x4096->4096, 6 planted x20, seed 0) against the reference's
+    own digests (tests/golden/cfg1_digest.json, generated by make_golden.py)."""
+    from paper_2208_07339_b200.gemm import llm_int8_trace
+    from paper_2208_07339_b200.synthetic import planted_pair
+
+    dig, sample = _golden.cfg1()
+    m, k, n = dig["shape"]
+    x, w = planted_pair(m, k, n, *dig["planted"])
+    x = x.astype(np.float16).astype(np.float32)
+    w = w.astype(np.float16).astype(np.float32)
+    tr = llm_int8_trace(x, w, dig["alpha"])
+    dims = tr["scan"].dims()
+    assert list(dims) == dig["dims"]
+    keep = _golden.keep_mask(k, dims)
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    assert sha(_np(tr["xq"])[:, keep]) == dig["sha256"]["xq"]
+    assert sha(_scales(tr["row_amax"])) == dig["sha256"]["sx"]
+    assert sha(np.ascontiguousarray(_np(tr["wq_t"]).T[keep, :])) == dig["sha256"]["wq"]
+    assert sha(_scales(tr["col_amax"])) == dig["sha256"]["sw"]
+    assert sha(_np(tr["c"])) == dig["sha256"]["c"]
+    yex = _np(tr["y_exact"])
+    assert sha(yex) == dig["sha256"]["out"]
+    assert np.array_equal(yex[dig["sample_rows"]], sample)
+
+
+def test_int8_linear_module(p, oracle_mod):
+    x, w = oracle_mod.planted_pair(64, 512, 256, 4, 20.0, 1)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda(), alpha=6.0)
+    y = lin(x16.reshape(4, 16, 512))
+    assert y.shape == (4, 16, 256) and y.dtype == torch.float16
+    ref = oracle_mod.c_llm_int8_matmul(x.astype(np.float16).astype(np.float32),
+                                       w.astype(np.float16).astype(np.float32), 6.0)
+    err = np.abs(_np(y.reshape(64, 256)).astype(np.float64) - ref.output)
+    assert (err <= _golden.fp16_tolerance(ref.output)).all()
+    # the backend plugin point (transformer.py:257-267)
+    y2 = p.linear(x, w, p.llm_int8_backend(6.0))
+    assert y2.dtype == torch.float32
+    with pytest.raises(NotImplementedError):
+        p.linear(x, w, p.ABSMAX)
+
+
+def test_capi_pipeline_entry(p, oracle_mod):
+    """The single-call C entry i8mm_llm_int8_matmul (what an FFI binding calls)."""
+    from paper_2208_07339_b200 import _native as nat
+
+    x, w = oracle_mod.planted_pair(200, 768, 320, 6, 20.0, 4)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    w16 = torch.from_numpy(w.astype(np.float16)).cuda()
+    L = nat.lib()
+    ws_bytes = L.i8mm_llm_int8_workspace_size(200, 768, 320)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    y = torch.empty((200, 320), dtype=torch.float32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    nat.check(L.i8mm_llm_int8_matmul(x16.data_ptr(), 768, w16.data_ptr(), 320, 200, 768, 320,
+                                     6.0, y.data_ptr(), 320, nat.OUT_F32_EXACT, ws.data_ptr(),
+                                     ws_bytes, cnt.data_ptr(), st))
+    ref = oracle_mod.c_llm_int8_matmul(x.astype(np.float16).astype(np.float32),
+                                       w.astype(np.float16).astype(np.float32), 6.0)
+    assert int(cnt.item()) == len(ref.dims)
+    assert np.array_equal(_np(y), ref.output)
+    assert L.i8mm_llm_int8_matmul(x16.data_ptr(), 768, w16.data_ptr(), 320, 200, 768, 320, -1.0,
+                                  y.data_ptr(), 320, 0, ws.data_ptr(), ws_bytes, None, st) == 3

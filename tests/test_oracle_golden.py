@@ -1,0 +1,107 @@
+"""Pin the CPU oracle (numpy + C restatements) to the reference's golden vectors.
+
+The oracle is only trusted as the GPU checker because every case below is
+bit-exact against outputs produced by the reference package itself
+(tests/golden/make_golden.py).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import _golden
+
+GOLDEN = _golden.cases()
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN))
+def test_numpy_oracle_matches_reference(oracle_mod, name):
+    g = GOLDEN[name]
+    tr = oracle_mod.llm_int8_matmul(g["x"], g["w"], g["alpha"])
+    assert tr.dims == tuple(int(d) for d in g["dims"])
+    keep = _golden.keep_mask(g["x"].shape[1], tr.dims)
+    if keep.any():
+        assert np.array_equal(tr.xq[:, keep], g["xq"])
+        assert np.array_equal(tr.sx, g["sx"])
+        assert np.array_equal(tr.wq[keep], g["wq"])
+        assert np.array_equal(tr.sw, g["sw"])
+        assert np.array_equal(tr.c, g["c"])
+    assert np.array_equal(tr.output, g["out"])
+    assert tr.decomposed_cols == int(g["decomposed_cols"])
+    assert tr.int8_fraction == float(g["int8_fraction"])
+    assert np.array_equal(oracle_mod.vectorwise_matmul(g["x"], g["w"]), g["vw"])
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN))
+def test_c_oracle_matches_reference(oracle_mod, name):
+    g = GOLDEN[name]
+    tr = oracle_mod.c_llm_int8_matmul(g["x"], g["w"], g["alpha"])
+    assert tr.dims == tuple(int(d) for d in g["dims"])
+    keep = _golden.keep_mask(g["x"].shape[1], tr.dims)
+    if keep.any():
+        assert np.array_equal(tr.xq[:, keep], g["xq"])
+        assert np.array_equal(tr.sx, g["sx"])
+        assert np.array_equal(tr.wq[keep], g["wq"])
+        assert np.array_equal(tr.sw, g["sw"])
+        assert np.array_equal(tr.c, g["c"])
+    assert np.array_equal(tr.output, g["out"])
+
+
+def test_kats(oracle_mod):
+    k = _golden.kats()
+    r = k["round_half_away"]
+    assert oracle_mod.round_half_away(np.array(r["in"])).tolist() == r["out"]
+    codes, sc = oracle_mod.rowwise_quantize(np.array(k["rowwise_hand"]["x"], np.float32))
+    assert sc.tolist() == k["rowwise_hand"]["scales"] and codes.tolist() == k["rowwise_hand"]["codes"]
+    codes, sc = oracle_mod.rowwise_quantize(np.array(k["rowwise_zero_row"]["x"], np.float32))
+    assert sc.tolist() == k["rowwise_zero_row"]["scales"]
+    codes, sc = oracle_mod.colwise_quantize(np.array(k["colwise_hand"]["w"], np.float32))
+    assert sc.tolist() == k["colwise_hand"]["scales"] and codes.tolist() == k["colwise_hand"]["codes"]
+    d = k["dequant_outer"]
+    out = oracle_mod.dequantize_output(np.array(d["c"], np.int32), np.array(d["sx"]), np.array(d["sw"]))
+    assert out.astype(np.float64).tolist() == d["out"]
+    for key in ("gemm_identity", "gemm_hand"):
+        a, b = np.array(k[key]["a"], np.int8), np.array(k[key]["b"], np.int8)
+        assert oracle_mod.int8_gemm_i32(a, b).tolist() == k[key]["c"]
+        assert oracle_mod.c_gemm_i32(a, b).tolist() == k[key]["c"]
+    h = k["gemm_worst_case"]["k"]
+    c = oracle_mod.c_gemm_i32(np.full((1, h), 127, np.int8), np.full((h, 1), 127, np.int8))
+    assert int(c[0, 0]) == k["gemm_worst_case"]["c"]
+    x = np.array(k["outlier_threshold_f32"]["x"], np.float32)
+    assert list(oracle_mod.outlier_dims(x, 6.1)) == k["outlier_threshold_f32"]["dims"]
+    assert list(oracle_mod.c_outlier_mask(x, 6.1).nonzero()[0]) == [0]
+
+
+def test_bigint_equivalence_c_oracle(oracle_mod):
+    """Acceptance criterion 1 (test_acceptance.py:50-59) on the C oracle, 200 seeds."""
+    for seed in range(200):
+        rng = np.random.Generator(np.random.PCG64(seed))
+        s, h, o = (int(d) for d in rng.integers(1, 65, size=3))
+        a = rng.integers(-127, 128, size=(s, h)).astype(np.int8)
+        b = rng.integers(-127, 128, size=(h, o)).astype(np.int8)
+        ref = a.astype(np.int64) @ b.astype(np.int64)
+        assert np.array_equal(oracle_mod.c_gemm_i32(a, b), ref)
+        assert np.array_equal(oracle_mod.int8_gemm_i32(a, b), ref)
+
+
+def test_cfg1_digest_c_oracle(oracle_mod):
+    """The C oracle reproduces the reference's config-1 digests (one run ~1 s)."""
+    dig, sample = _golden.cfg1()
+    m, k, n = dig["shape"]
+    x, w = oracle_mod.planted_pair(m, k, n, *dig["planted"])
+    x = x.astype(np.float16).astype(np.float32)
+    w = w.astype(np.float16).astype(np.float32)
+    tr = oracle_mod.c_llm_int8_matmul(x, w, dig["alpha"])
+    assert list(tr.dims) == dig["dims"]
+    keep = _golden.keep_mask(k, tr.dims)
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    assert sha(tr.xq[:, keep]) == dig["sha256"]["xq"]
+    assert sha(tr.sx) == dig["sha256"]["sx"]
+    assert sha(np.ascontiguousarray(tr.wq[keep])) == dig["sha256"]["wq"]
+    assert sha(tr.sw) == dig["sha256"]["sw"]
+    assert sha(tr.c) == dig["sha256"]["c"]
+    assert sha(tr.output) == dig["sha256"]["out"]
+    assert np.array_equal(tr.output[dig["sample_rows"]], sample)
