@@ -93,8 +93,15 @@ int i8mm_gemm_i32(const int8_t* a, int64_t lda, const int8_t* b_t, int64_t ldb, 
 int i8mm_gemm_dequant(const int8_t* xq, const int8_t* wq_t, int64_t ldq, int64_t M, int64_t N,
                       int64_t K, const float* row_amax, const float* col_amax, const void* x,
                       int64_t ldx, const void* w, int64_t ldw, const void* xo, int64_t o_cap,
-                      const int32_t* o_idx, const int32_t* o_count, void* y, int64_t ldy,
-                      int out_kind, void* stream);
+                      const void* wo, int64_t ldwo, const int32_t* o_idx, const int32_t* o_count,
+                      void* y, int64_t ldy, int out_kind, void* stream);
+
+/* Compact copy of the outlier rows W[O, :] (gemm.py:238 w.data[idx_out, :]):
+ * wo[t * ldwo + j] = W[o_idx[t], j] for t < min(*o_count, cap). Feeds the
+ * epilogue's outlier term with contiguous 16-byte loads (wo/ldwo above). */
+int i8mm_gather_outlier_rows(const void* w, int64_t ldw, int64_t N, const int32_t* o_idx,
+                             const int32_t* o_count, int64_t cap, void* wo, int64_t ldwo,
+                             void* stream);
 
 /* Exact dequantization of an int32 accumulator (gemm.py:130,141,147):
  * out[i,j] = (float)((double)c[i,j] / (sx[i] * sw[j])), f64 scales. */
@@ -114,6 +121,42 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
                          int64_t K, int64_t N, float alpha, void* y, int64_t ldy, int out_kind,
                          void* workspace, size_t workspace_bytes, int32_t* o_count_dev,
                          void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Int8 linear module (weight-stationary). Replaces the reference's module
+ * boundary LinearBackend("llm_int8") + _linear (transformer.py:45-66,
+ * 257-267), which re-quantizes W on every call (transformer.py:260, 267).
+ * prepare() caches WqT with full-column scales plus each column's top-4 |w|
+ * candidates; forward() reproduces the per-call column scales over the keep
+ * rows EXACTLY (quantize.py:182-187 on w[keep, :], gemm.py:243) by patching
+ * only the columns whose cached maximisers are all outlier rows. Outputs are
+ * identical to i8mm_llm_int8_matmul. W (fp16, K x N) must stay resident: the
+ * outlier rows are multiplied in fp16 (gemm.py:238).
+ */
+size_t i8mm_linear_weight_bytes(int64_t K, int64_t N);
+size_t i8mm_linear_prepare_scratch_bytes(int64_t K, int64_t N);
+int i8mm_linear_prepare(const void* w, int64_t ldw, int64_t K, int64_t N, void* wbuf,
+                        size_t wbuf_bytes, void* scratch, size_t scratch_bytes, void* stream);
+size_t i8mm_linear_workspace_size(int64_t M, int64_t K, int64_t N);
+/* scan + compact + quantize rows + gather outlier rows + column fixup */
+int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                         const void* wbuf, int64_t K, int64_t N, float alpha, void* workspace,
+                         size_t workspace_bytes, void* stream);
+/* main tcgen05 GEMM over the cached codes + col-mapped GEMM over the patches */
+int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                     const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
+                     void* workspace, size_t workspace_bytes, void* stream);
+/* prologue + gemm; *o_count_dev (nullable) receives |O| */
+int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                        const void* wbuf, int64_t K, int64_t N, float alpha, void* y, int64_t ldy,
+                        int out_kind, void* workspace, size_t workspace_bytes,
+                        int32_t* o_count_dev, void* stream);
+/* introspection (tests): device pointers into the workspace / weight buffer.
+ * workspace views: [o_count, o_idx, xq, row_amax, p_count, p_idx, p_amax, wq_p]
+ * weight views:    [wq_t, col_amax, cand_v, cand_r] */
+int i8mm_linear_workspace_views(void* workspace, int64_t M, int64_t K, int64_t N, void** views,
+                                int n_views);
+int i8mm_linear_weight_views(void* wbuf, int64_t K, int64_t N, void** views, int n_views);
 
 #ifdef __cplusplus
 }

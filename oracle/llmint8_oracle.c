@@ -112,21 +112,34 @@ void oracle_colwise_quantize(const float* w, int64_t K, int64_t N, const uint8_t
 }
 
 /* gemm.py:78-82 exact int8 x int8 -> int32 (|sum| <= 127^2 * 2^17 < 2^31).
- * a: MxK row-major, b: KxN row-major, c: MxN. i-k-j order, OpenMP over rows. */
+ * a: MxK row-major, b: KxN row-major, c: MxN. Cache-blocked i-k-j order:
+ * a block of RB rows of C (CB columns wide) stays in L1/L2 while each B row
+ * segment is reused RB times; OpenMP over (row block, column block) tiles.
+ * Integer addition is associative, so the blocking is exact. */
+#define ORACLE_RB 16
+#define ORACLE_CB 2048
 __attribute__((target_clones("arch=x86-64-v4", "arch=x86-64-v3", "default")))
 void oracle_gemm_i32(const int8_t* a, const int8_t* b, int32_t* c, int64_t M, int64_t N,
                      int64_t K, int threads) {
     set_threads(threads);
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t i = 0; i < M; ++i) {
-        int32_t* crow = c + i * N;
-        memset(crow, 0, (size_t)N * sizeof(int32_t));
-        const int8_t* arow = a + i * K;
-        for (int64_t k = 0; k < K; ++k) {
-            const int32_t av = arow[k];
-            if (!av) continue;
-            const int8_t* brow = b + k * N;
-            for (int64_t j = 0; j < N; ++j) crow[j] += av * (int32_t)brow[j];
+    const int64_t nrb = (M + ORACLE_RB - 1) / ORACLE_RB;
+    const int64_t ncb = (N + ORACLE_CB - 1) / ORACLE_CB;
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+    for (int64_t rb = 0; rb < nrb; ++rb) {
+        for (int64_t cb = 0; cb < ncb; ++cb) {
+            const int64_t i0 = rb * ORACLE_RB, i1 = i0 + ORACLE_RB < M ? i0 + ORACLE_RB : M;
+            const int64_t j0 = cb * ORACLE_CB, j1 = j0 + ORACLE_CB < N ? j0 + ORACLE_CB : N;
+            const int64_t w = j1 - j0;
+            for (int64_t i = i0; i < i1; ++i) memset(c + i * N + j0, 0, (size_t)w * sizeof(int32_t));
+            for (int64_t k = 0; k < K; ++k) {
+                const int8_t* brow = b + k * N + j0;
+                for (int64_t i = i0; i < i1; ++i) {
+                    const int32_t av = a[i * K + k];
+                    if (!av) continue;
+                    int32_t* crow = c + i * N + j0;
+                    for (int64_t j = 0; j < w; ++j) crow[j] += av * (int32_t)brow[j];
+                }
+            }
         }
     }
 }

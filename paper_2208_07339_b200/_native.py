@@ -44,6 +44,16 @@ EXPORTED_SYMBOLS = (
     "i8mm_transpose_i8",
     "i8mm_llm_int8_workspace_size",
     "i8mm_llm_int8_matmul",
+    "i8mm_gather_outlier_rows",
+    "i8mm_linear_weight_bytes",
+    "i8mm_linear_prepare_scratch_bytes",
+    "i8mm_linear_prepare",
+    "i8mm_linear_workspace_size",
+    "i8mm_linear_prologue",
+    "i8mm_linear_gemm",
+    "i8mm_linear_forward",
+    "i8mm_linear_workspace_views",
+    "i8mm_linear_weight_views",
 )
 
 _lib = None
@@ -64,8 +74,21 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_quantize_rows": ([P, I64, I64, I64, P, P, P, P, I64, P, P, I64, P], I32),
         "i8mm_quantize_cols_t": ([P, I64, I64, I64, P, P, I64, P, P], I32),
         "i8mm_gemm_i32": ([P, I64, P, I64, P, I64, I64, I64, I64, P], I32),
-        "i8mm_gemm_dequant": ([P, P, I64, I64, I64, I64, P, P, P, I64, P, I64, P, I64, P, P, P,
-                               I64, I32, P], I32),
+        "i8mm_gemm_dequant": ([P, P, I64, I64, I64, I64, P, P, P, I64, P, I64, P, I64, P, I64, P,
+                               P, P, I64, I32, P], I32),
+        "i8mm_gather_outlier_rows": ([P, I64, I64, P, P, I64, P, I64, P], I32),
+        "i8mm_linear_weight_bytes": ([I64, I64], ctypes.c_size_t),
+        "i8mm_linear_prepare_scratch_bytes": ([I64, I64], ctypes.c_size_t),
+        "i8mm_linear_prepare": ([P, I64, I64, I64, P, ctypes.c_size_t, P, ctypes.c_size_t, P], I32),
+        "i8mm_linear_workspace_size": ([I64, I64, I64], ctypes.c_size_t),
+        "i8mm_linear_prologue": ([P, I64, I64, P, I64, P, I64, I64, F32, P, ctypes.c_size_t, P],
+                                 I32),
+        "i8mm_linear_gemm": ([P, I64, I64, P, I64, P, I64, I64, P, I64, I32, P, ctypes.c_size_t,
+                              P], I32),
+        "i8mm_linear_forward": ([P, I64, I64, P, I64, P, I64, I64, F32, P, I64, I32, P,
+                                 ctypes.c_size_t, P, P], I32),
+        "i8mm_linear_workspace_views": ([P, I64, I64, I64, P, I32], I32),
+        "i8mm_linear_weight_views": ([P, I64, I64, P, I32], I32),
         "i8mm_dequantize_output": ([P, I64, I64, I64, P, P, P, I64, P], I32),
         "i8mm_transpose_i8": ([P, I64, I64, I64, P, I64, P], I32),
         "i8mm_llm_int8_workspace_size": ([I64, I64, I64], ctypes.c_size_t),

@@ -144,8 +144,8 @@ int i8mm_gemm_i32(const int8_t* a, int64_t lda, const int8_t* b_t, int64_t ldb, 
 int i8mm_gemm_dequant(const int8_t* xq, const int8_t* wq_t, int64_t ldq, int64_t M, int64_t N,
                       int64_t K, const float* row_amax, const float* col_amax, const void* x,
                       int64_t ldx, const void* w, int64_t ldw, const void* xo, int64_t o_cap,
-                      const int32_t* o_idx, const int32_t* o_count, void* y, int64_t ldy,
-                      int out_kind, void* stream) {
+                      const void* wo, int64_t ldwo, const int32_t* o_idx, const int32_t* o_count,
+                      void* y, int64_t ldy, int out_kind, void* stream) {
     if (int s = check_device()) return s;
     if (int s = check_inner(K)) return s;
     if (M < 0 || N < 0 || K <= 0 || ldq < K || (ldq % 16) || ldy < N || !xq || !wq_t ||
@@ -179,7 +179,21 @@ int i8mm_gemm_dequant(const int8_t* xq, const int8_t* wq_t, int64_t ldq, int64_t
     g.o_cap = xo ? o_cap : 0;
     g.o_idx = o_idx;
     g.o_count = o_count;
+    g.wo = static_cast<const __half*>(wo);
+    g.ldwo = ldwo;
+    g.wo_cap = wo ? o_cap : 0;
     return cuda_status(launch_gemm_sm100(g, epi, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_gather_outlier_rows(const void* w, int64_t ldw, int64_t N, const int32_t* o_idx,
+                             const int32_t* o_count, int64_t cap, void* wo, int64_t ldwo,
+                             void* stream) {
+    if (int s = check_device()) return s;
+    if (N <= 0 || ldw < N || ldwo < N || cap < 0 || !w || !o_idx || !o_count || !wo)
+        return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_gather_rows(static_cast<const __half*>(w), ldw, N, o_idx, o_count, cap,
+                                          static_cast<__half*>(wo), ldwo,
+                                          static_cast<cudaStream_t>(stream)));
 }
 
 int i8mm_dequantize_output(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const double* sx,
@@ -210,12 +224,19 @@ struct Workspace {
     int8_t* xq;
     int8_t* wq_t;
     __half* xo;
+    __half* wo;
+    int32_t* p_count;
+    int32_t* p_idx;
+    float* p_amax;
+    int8_t* wq_p;
     int64_t ldq, o_cap;
     size_t bytes;
 };
 constexpr int64_t kOCap = 64;  // compacted outlier slice width (wider |O| reads X directly)
 
-Workspace carve(void* base, int64_t M, int64_t K, int64_t N) {
+// Per-call workspace. `linear` = weight-stationary layout: no WqT (it lives in
+// the prepared weight buffer) but room for the patched columns (worst case N).
+Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false) {
     Workspace w{};
     w.ldq = round_up(K, 16);
     w.o_cap = kOCap;
@@ -233,10 +254,45 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N) {
     w.row_amax = reinterpret_cast<float*>(take(sizeof(float) * (M > 0 ? M : 1)));
     w.col_amax = reinterpret_cast<float*>(take(sizeof(float) * (N > 0 ? N : 1)));
     w.xq = reinterpret_cast<int8_t*>(take(static_cast<size_t>(M * w.ldq)));
-    w.wq_t = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
+    w.wq_t = linear ? nullptr : reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
     w.xo = reinterpret_cast<__half*>(take(sizeof(__half) * static_cast<size_t>(M * kOCap)));
+    w.wo = reinterpret_cast<__half*>(take(sizeof(__half) * static_cast<size_t>(kOCap * round_up(N, 8))));
+    if (linear) {
+        w.p_count = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 4));
+        w.p_idx = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
+        w.p_amax = reinterpret_cast<float*>(take(sizeof(float) * N));
+        w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
+    }
     w.bytes = p - p0;
     return w;
+}
+
+// Prepared weight buffer of the weight-stationary linear layer.
+struct WeightBuf {
+    int8_t* wq_t;     // N x ldq codes with the full-column scale
+    float* col_amax;  // N, amax over all K rows
+    uint16_t* cand_v; // kTopT x N, |w| fp16 bits, descending
+    int32_t* cand_r;  // kTopT x N, rows
+    int64_t ldq;
+    size_t bytes;
+};
+
+WeightBuf carve_weight(void* base, int64_t K, int64_t N) {
+    WeightBuf b{};
+    b.ldq = round_up(K, 16);
+    uintptr_t p = reinterpret_cast<uintptr_t>(base);
+    const uintptr_t p0 = p;
+    auto take = [&](size_t bytes) {
+        uintptr_t r = p;
+        p += static_cast<uintptr_t>(round_up(static_cast<int64_t>(bytes), 256));
+        return r;
+    };
+    b.wq_t = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * b.ldq)));
+    b.col_amax = reinterpret_cast<float*>(take(sizeof(float) * N));
+    b.cand_v = reinterpret_cast<uint16_t*>(take(sizeof(uint16_t) * kTopT * N));
+    b.cand_r = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * kTopT * N));
+    b.bytes = p - p0;
+    return b;
 }
 }  // namespace
 
@@ -273,15 +329,190 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
     // gemm.py:243 colwise over keep rows, stored K-major
     if ((e = launch_quantize_cols_t(wh, K, N, ldw, ws.mask, ws.wq_t, ws.ldq, ws.col_amax, st)))
         return I8MM_ERR_CUDA;
+    // compact copy of the outlier rows W[O, :] for the epilogue (gemm.py:238)
+    if ((e = launch_gather_rows(wh, ldw, N, ws.o_idx, ws.o_count, ws.o_cap, ws.wo, round_up(N, 8), st)))
+        return I8MM_ERR_CUDA;
     // gemm.py:193-194, 238, 244-247: int8 GEMM + dequant + outlier term
     int s = i8mm_gemm_dequant(ws.xq, ws.wq_t, ws.ldq, M, N, K, ws.row_amax, ws.col_amax, x, ldx, w,
-                              ldw, ws.xo, ws.o_cap, ws.o_idx, ws.o_count, y, ldy, out_kind, stream);
+                              ldw, ws.xo, ws.o_cap, ws.wo, round_up(N, 8), ws.o_idx, ws.o_count, y,
+                              ldy, out_kind, stream);
     if (s) return s;
     if (o_count_dev) {
         if (cudaMemcpyAsync(o_count_dev, ws.o_count, sizeof(int32_t), cudaMemcpyDeviceToDevice,
                             st) != cudaSuccess)
             return I8MM_ERR_CUDA;
     }
+    return I8MM_OK;
+}
+
+// ---------------------------------------------------------------- linear layer
+size_t i8mm_linear_weight_bytes(int64_t K, int64_t N) {
+    if (K <= 0 || N <= 0) return 0;
+    return carve_weight(nullptr, K, N).bytes + 256;
+}
+
+size_t i8mm_linear_prepare_scratch_bytes(int64_t K, int64_t N) {
+    if (K <= 0 || N <= 0) return 0;
+    const int64_t rpb = topt_chunk_rows(K);
+    const int64_t chunks = (K + rpb - 1) / rpb;
+    return static_cast<size_t>(2 * chunks * kTopT * N) * sizeof(uint32_t) + 512;
+}
+
+int i8mm_linear_prepare(const void* w, int64_t ldw, int64_t K, int64_t N, void* wbuf,
+                        size_t wbuf_bytes, void* scratch, size_t scratch_bytes, void* stream) {
+    if (int s = check_device()) return s;
+    if (int s = check_inner(K)) return s;
+    if (K <= 0 || N <= 0 || ldw < N || !w || !wbuf || !scratch) return I8MM_ERR_ARGUMENT;
+    void* base = reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256));
+    WeightBuf b = carve_weight(base, K, N);
+    if (b.bytes + (static_cast<char*>(base) - static_cast<char*>(wbuf)) > wbuf_bytes)
+        return I8MM_ERR_ARGUMENT;
+    if (scratch_bytes < i8mm_linear_prepare_scratch_bytes(K, N)) return I8MM_ERR_ARGUMENT;
+    const int64_t rpb = topt_chunk_rows(K);
+    const int64_t chunks = (K + rpb - 1) / rpb;
+    uint32_t* sv = reinterpret_cast<uint32_t*>(round_up(reinterpret_cast<intptr_t>(scratch), 256));
+    int32_t* sr = reinterpret_cast<int32_t*>(sv + chunks * kTopT * N);
+    return cuda_status(launch_weight_prepare(static_cast<const __half*>(w), K, N, ldw, b.wq_t, b.ldq,
+                                             b.col_amax, b.cand_v, b.cand_r, sv, sr,
+                                             static_cast<cudaStream_t>(stream)));
+}
+
+size_t i8mm_linear_workspace_size(int64_t M, int64_t K, int64_t N) {
+    if (M < 0 || K <= 0 || N <= 0) return 0;
+    return carve(nullptr, M, K, N, true).bytes + 256;
+}
+
+static int linear_ws(void* workspace, size_t bytes, int64_t M, int64_t K, int64_t N, Workspace* ws) {
+    void* base = reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(workspace), 256));
+    *ws = carve(base, M, K, N, true);
+    if (ws->bytes + (static_cast<char*>(base) - static_cast<char*>(workspace)) > bytes)
+        return I8MM_ERR_ARGUMENT;
+    return I8MM_OK;
+}
+
+int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                         const void* wbuf, int64_t K, int64_t N, float alpha, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+    if (int s = check_device()) return s;
+    if (int s = check_inner(K)) return s;
+    if (!(alpha > 0.0f) || !std::isfinite(alpha)) return I8MM_ERR_ALPHA;
+    if (M <= 0 || K <= 0 || N <= 0 || ldx < K || ldw < N || !x || !w || !wbuf || !workspace)
+        return I8MM_ERR_ARGUMENT;
+    Workspace ws;
+    if (int s = linear_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
+    const WeightBuf b = carve_weight(
+        reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)), K, N);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const __half* xh = static_cast<const __half*>(x);
+    const __half* wh = static_cast<const __half*>(w);
+    if (launch_outlier_scan(xh, M, K, ldx, alpha, ws.mask, nullptr, st)) return I8MM_ERR_CUDA;
+    if (launch_outlier_compact(ws.mask, K, ws.o_idx, ws.o_count, st)) return I8MM_ERR_CUDA;
+    if (launch_quantize_rows(xh, M, K, ldx, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
+                             ws.row_amax, ws.xo, ws.o_cap, st))
+        return I8MM_ERR_CUDA;
+    if (launch_gather_rows(wh, ldw, N, ws.o_idx, ws.o_count, ws.o_cap, ws.wo, round_up(N, 8), st))
+        return I8MM_ERR_CUDA;
+    if (launch_weight_fixup(wh, K, N, ldw, ws.mask, b.col_amax, b.cand_v, b.cand_r, ws.p_count,
+                            ws.p_idx, ws.p_amax, ws.wq_p, ws.ldq, st))
+        return I8MM_ERR_CUDA;
+    return I8MM_OK;
+}
+
+int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                     const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    if (int s = check_device()) return s;
+    if (M <= 0 || K <= 0 || N <= 0 || ldy < N || !y || !wbuf || !workspace) return I8MM_ERR_ARGUMENT;
+    Workspace ws;
+    if (int s = linear_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
+    const WeightBuf b = carve_weight(
+        reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)), K, N);
+    int epi;
+    switch (out_kind) {
+        case I8MM_OUT_F16: epi = EPI_F16; break;
+        case I8MM_OUT_F32: epi = EPI_F32; break;
+        case I8MM_OUT_F32_EXACT: epi = EPI_F32_EXACT; break;
+        default: return I8MM_ERR_ARGUMENT;
+    }
+    GemmArgs g{};
+    g.a = ws.xq;
+    g.lda = ws.ldq;
+    g.b = b.wq_t;
+    g.ldb = b.ldq;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.y = y;
+    g.ldy = ldy;
+    g.row_amax = ws.row_amax;
+    g.col_amax = b.col_amax;
+    g.x = static_cast<const __half*>(x);
+    g.ldx = ldx;
+    g.w = static_cast<const __half*>(w);
+    g.ldw = ldw;
+    g.xo = ws.xo;
+    g.o_cap = ws.o_cap;
+    g.o_idx = ws.o_idx;
+    g.o_count = ws.o_count;
+    g.wo = ws.wo;
+    g.ldwo = round_up(N, 8);
+    g.wo_cap = ws.o_cap;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (launch_gemm_sm100(g, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
+    // patched columns: their amax over keep rows differs from the cached one
+    g.b = ws.wq_p;
+    g.col_amax = ws.p_amax;
+    g.col_map = ws.p_idx;
+    g.n_count = ws.p_count;
+    if (launch_gemm_sm100(g, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
+    return I8MM_OK;
+}
+
+int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                        const void* wbuf, int64_t K, int64_t N, float alpha, void* y, int64_t ldy,
+                        int out_kind, void* workspace, size_t workspace_bytes,
+                        int32_t* o_count_dev, void* stream) {
+    int s = i8mm_linear_prologue(x, ldx, M, w, ldw, wbuf, K, N, alpha, workspace, workspace_bytes,
+                                 stream);
+    if (s) return s;
+    s = i8mm_linear_gemm(x, ldx, M, w, ldw, wbuf, K, N, y, ldy, out_kind, workspace,
+                         workspace_bytes, stream);
+    if (s) return s;
+    if (o_count_dev) {
+        Workspace ws;
+        linear_ws(workspace, workspace_bytes, M, K, N, &ws);
+        if (cudaMemcpyAsync(o_count_dev, ws.o_count, sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                            static_cast<cudaStream_t>(stream)) != cudaSuccess)
+            return I8MM_ERR_CUDA;
+    }
+    return I8MM_OK;
+}
+
+// Device pointers into a linear-layer workspace (for tests / introspection).
+int i8mm_linear_workspace_views(void* workspace, int64_t M, int64_t K, int64_t N, void** views,
+                                int n_views) {
+    if (!workspace || !views || n_views < 8) return I8MM_ERR_ARGUMENT;
+    void* base = reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(workspace), 256));
+    Workspace ws = carve(base, M, K, N, true);
+    views[0] = ws.o_count;  // int32 |O|
+    views[1] = ws.o_idx;    // int32 [K]
+    views[2] = ws.xq;       // int8 [M x ldq]
+    views[3] = ws.row_amax; // float [M]
+    views[4] = ws.p_count;  // int32 patched-column count
+    views[5] = ws.p_idx;    // int32 [N]
+    views[6] = ws.p_amax;   // float [N]
+    views[7] = ws.wq_p;     // int8 [N x ldq]
+    return I8MM_OK;
+}
+
+int i8mm_linear_weight_views(void* wbuf, int64_t K, int64_t N, void** views, int n_views) {
+    if (!wbuf || !views || n_views < 4) return I8MM_ERR_ARGUMENT;
+    WeightBuf b = carve_weight(reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)),
+                               K, N);
+    views[0] = b.wq_t;
+    views[1] = b.col_amax;
+    views[2] = b.cand_v;
+    views[3] = b.cand_r;
     return I8MM_OK;
 }
 

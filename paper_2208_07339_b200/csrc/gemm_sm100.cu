@@ -4,13 +4,20 @@
 // the high-precision outlier term sum_{o in O} X[:,o] W[o,:] (gemm.py:238,
 // 244-247), written straight to the output tile.
 //
-// Structure (one CTA per SM, persistent, warp-specialised, 256 threads):
-//   warp 0      TMA producer   : A (Xq, 128x128 B) + B (WqT, 256x128 B) per
-//                                stage into a 4-deep SWIZZLE_128B smem ring
-//   warp 1      MMA issuer     : tcgen05.mma.cta_group::1.kind::i8, M=128,
-//                                N=256, K=32, accumulating in TMEM
+// Structure (persistent, warp-specialised, 384 threads per CTA). CG=2 (the
+// default for M > 128) runs CTA pairs (cluster 2x1) on cta_group::2 MMAs:
+// a 256x256 output tile per pair, each CTA loading 128 rows of Xq and 128 rows
+// of WqT per stage, which halves the per-SM shared-memory operand traffic of
+// the 1-CTA (CG=1) 128x256 tile.
+//   warp 0      TMA producer   : Xq / WqT K-blocks of 128 B into a SWIZZLE_128B
+//                                smem ring (4 stages CG=1, 6 stages CG=2); in a
+//                                pair both CTAs load, the leader's mbarrier
+//                                counts both CTAs' bytes
+//   warp 1      MMA issuer     : one elected lane of the leader CTA issues
+//                                tcgen05.mma.cta_group::{1,2}.kind::i8
+//                                (M = 128 CG, N = 256, K = 32) into TMEM
 //   warp 2      TMEM allocator : 512 columns = two 128x256 int32 accumulators
-//   warps 4..7  epilogue       : tcgen05.ld -> dequant + outlier FMAs ->
+//   warps 4..11 epilogue       : tcgen05.ld -> dequant + outlier FMAs ->
 //                                global stores, overlapping the next tile's
 //                                mainloop (double-buffered TMEM)
 #include <cuda.h>
@@ -18,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -26,38 +34,49 @@
 namespace i8mm {
 
 namespace gemm {
-constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BM = 128;  // rows of the output tile per CTA
+constexpr int BN = 256;  // columns of the output tile (per CTA pair when CG=2)
 constexpr int BK = 128;  // bytes == int8 elements: one SWIZZLE_128B atom row
 constexpr int UMMA_K = 32;
-constexpr int STAGES = 4;
+constexpr int MAX_STAGES = 6;
 constexpr int A_BYTES = BM * BK;
-constexpr int B_BYTES = BN * BK;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+
+template <int CG>
+struct Cfg {
+    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int B_ROWS = BN / CG;  // WqT rows loaded by each CTA
+    static constexpr int B_BYTES = B_ROWS * BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr size_t SMEM_OPERANDS = static_cast<size_t>(STAGES) * STAGE_BYTES;
+    static constexpr int GROUP_M = CG == 1 ? 16 : 8;
+};
 constexpr int WO_CAP = 16;  // outlier rows of W staged in smem per tile
-constexpr int THREADS = 256;
 constexpr int EPI_WARP0 = 4;
+constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half of BN
+constexpr int EPI_THREADS = EPI_WARPS * 32;
+constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
+constexpr int COLS_PER_EPI_WARP = BN / (EPI_WARPS / 4);
 constexpr uint32_t TMEM_COLS = 2 * BN;
-constexpr int GROUP_M = 16;
 
 struct __align__(8) Barriers {
-    uint64_t full[STAGES];
-    uint64_t empty[STAGES];
+    uint64_t full[MAX_STAGES];
+    uint64_t empty[MAX_STAGES];
     uint64_t tmem_full[2];
     uint64_t tmem_empty[2];
     uint32_t tmem_slot;
 };
 
-constexpr size_t SMEM_OPERANDS = static_cast<size_t>(STAGES) * STAGE_BYTES;
 constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(float);
 constexpr size_t SMEM_COLS = static_cast<size_t>(BN) * sizeof(double);
-constexpr size_t SMEM_TOTAL = 1024 /*align slack*/ + SMEM_OPERANDS + SMEM_WO + SMEM_COLS +
-                              sizeof(Barriers) + 64;
+template <int CG>
+constexpr size_t smem_total() {
+    return 1024 /*align slack*/ + Cfg<CG>::SMEM_OPERANDS + SMEM_WO + SMEM_COLS + sizeof(Barriers) + 64;
+}
 
 struct Params {
     int64_t M, N, K;
     int num_kb;
-    int m_tiles, n_tiles, total_tiles;
+    int m_tiles;
     void* y;
     int64_t ldy;
     const float* row_amax;
@@ -70,12 +89,36 @@ struct Params {
     int64_t o_cap;
     const int32_t* o_idx;
     const int32_t* o_count;
-    int vec_store;  // 1: y rows 16-byte aligned and N % (16/elt) == 0
+    const __half* wo;
+    int64_t ldwo;
+    int64_t wo_cap;
+    const int32_t* col_map;
+    const int32_t* n_count;
+    int vec_store;  // 1: y rows 16-byte aligned and row pitch a multiple of 16 B
 };
 
-__device__ __forceinline__ void tile_coords(const Params& p, int t, int& m_blk, int& n_blk) {
+struct TileSpace {
+    int n_live, n_tiles, total;
+};
+
+__device__ __forceinline__ TileSpace tile_space(const Params& p) {
+    TileSpace ts;
+    int64_t n = p.N;
+    if (p.n_count != nullptr) {
+        const int64_t c = *p.n_count;
+        n = c < n ? c : n;
+    }
+    ts.n_live = static_cast<int>(n);
+    ts.n_tiles = static_cast<int>((n + BN - 1) / BN);
+    ts.total = p.m_tiles * ts.n_tiles;
+    return ts;
+}
+
+template <int GROUP_M>
+__device__ __forceinline__ void tile_coords(const Params& p, const TileSpace& ts, int t,
+                                            int& m_blk, int& n_blk) {
     // grouped raster: GROUP_M m-tiles share each B panel while it is hot in L2
-    const int per_group = GROUP_M * p.n_tiles;
+    const int per_group = GROUP_M * ts.n_tiles;
     const int g = t / per_group;
     const int first_m = g * GROUP_M;
     const int gm = min(GROUP_M, p.m_tiles - first_m);
@@ -86,10 +129,14 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& m_blk, 
 
 __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0f : a; }
 
-template <int EPI>
+template <int EPI, int CG>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+    using C = Cfg<CG>;
+    constexpr int STAGES = C::STAGES;
+    constexpr int B_BYTES = C::B_BYTES;
+    constexpr size_t SMEM_OPERANDS = C::SMEM_OPERANDS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -101,6 +148,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const TileSpace ts = tile_space(p);
+    const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;  // rank within the CTA pair
+    const bool leader = crank == 0;
+    const int cluster_id = static_cast<int>(blockIdx.x) / CG;
+    const int n_clusters = static_cast<int>(gridDim.x) / CG;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_a);
@@ -111,13 +163,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->tmem_full[a], 1);
-            mbar_init(&bars->tmem_empty[a], 4);  // one arrive per epilogue warp
+            // one arrive per epilogue warp of every CTA of the pair
+            mbar_init(&bars->tmem_empty[a], CG * EPI_WARPS);
         }
         fence_mbarrier_init();
     }
-    if (warp == 2) tmem_alloc<TMEM_COLS>(&bars->tmem_slot);
+    if (warp == 2) {
+        if constexpr (CG == 2) tmem_alloc_pair<TMEM_COLS>(&bars->tmem_slot);
+        else tmem_alloc<TMEM_COLS>(&bars->tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised + TMEM allocated
     tc_fence_after();
     const uint32_t tmem_base = bars->tmem_slot;
 
@@ -127,16 +184,27 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t pol = l2_policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+            for (int t = cluster_id; t < ts.total; t += n_clusters) {
                 int m_blk, n_blk;
-                tile_coords(p, t, m_blk, n_blk);
+                tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
+                const int a_row = m_blk * (BM * CG) + static_cast<int>(crank) * BM;
+                const int b_row = n_blk * BN + static_cast<int>(crank) * C::B_ROWS;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1u);
-                    mbar_arrive_expect_tx(&bars->full[stage], STAGE_BYTES);
-                    tma_load_2d(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES, kb * BK,
-                                m_blk * BM, pol);
-                    tma_load_2d(&tmap_b, &bars->full[stage], smem_b + stage * B_BYTES, kb * BK,
-                                n_blk * BN, pol);
+                    if constexpr (CG == 2) {
+                        // the leader's full barrier counts both CTAs' bytes
+                        if (leader) mbar_arrive_expect_tx(&bars->full[stage], CG * C::STAGE_BYTES);
+                        tma_load_2d_pair(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES,
+                                         kb * BK, a_row, pol);
+                        tma_load_2d_pair(&tmap_b, &bars->full[stage], smem_b + stage * B_BYTES,
+                                         kb * BK, b_row, pol);
+                    } else {
+                        mbar_arrive_expect_tx(&bars->full[stage], C::STAGE_BYTES);
+                        tma_load_2d(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES, kb * BK,
+                                    a_row, pol);
+                        tma_load_2d(&tmap_b, &bars->full[stage], smem_b + stage * B_BYTES, kb * BK,
+                                    b_row, pol);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -144,13 +212,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        constexpr uint32_t idesc = idesc_i8(BM, BN);
+    } else if (warp == 1 && leader) {
+        // ===================== MMA issuer (leader CTA) =====================
+        constexpr uint32_t idesc = idesc_i8(BM * CG, BN);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+        for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1u);
@@ -166,9 +234,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int k = 0; k < BK / UMMA_K; ++k) {
                         const uint64_t ad = smem_desc_k_sw128(a0 + k * UMMA_K);
                         const uint64_t bd = smem_desc_k_sw128(b0 + k * UMMA_K);
-                        mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        if constexpr (CG == 2) mma_i8_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        else mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
-                    mma_commit(&bars->empty[stage]);  // frees the smem slot when MMAs finish
+                    // frees the smem slot (in both CTAs of a pair) when the MMAs finish
+                    if constexpr (CG == 2) mma_commit_pair(&bars->empty[stage], 0x3);
+                    else mma_commit(&bars->empty[stage]);
                 }
                 __syncwarp();
                 if (++stage == STAGES) {
@@ -176,81 +247,116 @@ __global__ void __launch_bounds__(THREADS, 1)
                     phase ^= 1u;
                 }
             }
-            if (lane == 0) mma_commit(&bars->tmem_full[acc]);  // accumulator ready
+            if (lane == 0) {  // accumulator ready (both CTAs' epilogues)
+                if constexpr (CG == 2) mma_commit_pair(&bars->tmem_full[acc], 0x3);
+                else mma_commit(&bars->tmem_full[acc]);
+            }
             __syncwarp();
         }
     } else if (warp >= EPI_WARP0) {
         // ===================== epilogue =====================
-        const int ew = warp - EPI_WARP0;  // == warp % 4: TMEM lanes 32*ew .. 32*ew+31
-        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..127
+        const int quad = warp & 3;                       // TMEM lanes 32*quad .. +31
+        const int half = (warp - EPI_WARP0) >> 2;        // which half of the BN columns
+        const int et = threadIdx.x - EPI_WARP0 * 32;     // 0 .. EPI_THREADS-1
         int n_out = 0;
         if constexpr (EPI != EPI_I32) n_out = p.o_count ? *p.o_count : 0;
-        const bool fast_o = n_out <= WO_CAP && n_out <= p.o_cap && p.xo != nullptr;
+        const bool wo_fast = n_out <= WO_CAP && p.wo != nullptr && n_out <= p.wo_cap;
+        const bool xo_fast = n_out <= WO_CAP && p.xo != nullptr && n_out <= p.o_cap;
+        const bool stage_wo = n_out > 0 && n_out <= WO_CAP;
         int it = 0;
-        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+        for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
             int m_blk, n_blk;
-            tile_coords(p, t, m_blk, n_blk);
+            tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            const int64_t row = static_cast<int64_t>(m_blk) * BM + ew * 32 + lane;
+            const int64_t row = static_cast<int64_t>(m_blk) * (BM * CG) + crank * BM + quad * 32 + lane;
             const int64_t col0 = static_cast<int64_t>(n_blk) * BN;
             const bool row_ok = row < p.M;
+            const bool mapped = p.col_map != nullptr;
 
             float xo_r[WO_CAP];
             float rowf = 0.0f;
             double sx = 1.0;
             if constexpr (EPI != EPI_I32) {
-                // stage per-tile column factors and outlier W rows in smem
-                named_bar_sync(1, 128);  // previous tile's readers are done
-                for (int j = et; j < BN; j += 128) {
+                // ---- stage per-tile column factors and outlier W rows in smem
+                named_bar_sync(1, EPI_THREADS);  // previous tile's readers are done
+                for (int j = et; j < BN; j += EPI_THREADS) {
                     const int64_t c = col0 + j;
-                    const float aw = c < p.N ? amax_or_127(p.col_amax[c]) : 127.0f;
+                    const float aw = c < ts.n_live ? amax_or_127(p.col_amax[c]) : 127.0f;
                     if constexpr (EPI == EPI_F32_EXACT)
                         smem_col[j] = 127.0 / static_cast<double>(aw);
                     else
                         reinterpret_cast<float*>(smem_col)[j] = aw * (1.0f / 16129.0f);
                 }
-                if (fast_o) {
-                    for (int i = et; i < n_out * BN; i += 128) {
-                        const int o = i / BN, j = i - (i / BN) * BN;
-                        const int64_t c = col0 + j;
-                        smem_wo[i] =
-                            c < p.N ? __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + c])
-                                    : 0.0f;
+                if (stage_wo) {
+                    if (wo_fast && !mapped && col0 + BN <= ts.n_live && (p.ldwo % 8) == 0) {
+                        // 16-byte vector loads of the compact outlier rows
+                        for (int i = et; i < n_out * (BN / 8); i += EPI_THREADS) {
+                            const int o = i / (BN / 8), v = i % (BN / 8);
+                            const uint4 q = *reinterpret_cast<const uint4*>(
+                                p.wo + static_cast<int64_t>(o) * p.ldwo + col0 + v * 8);
+                            const __half2* h2 = reinterpret_cast<const __half2*>(&q);
+                            float4* dst = reinterpret_cast<float4*>(smem_wo + o * BN + v * 8);
+                            const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]);
+                            const float2 f2 = __half22float2(h2[2]), f3 = __half22float2(h2[3]);
+                            dst[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
+                            dst[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
+                        }
+                    } else {
+                        for (int i = et; i < n_out * BN; i += EPI_THREADS) {
+                            const int o = i / BN, j = i % BN;
+                            const int64_t c = col0 + j;
+                            float v = 0.0f;
+                            if (c < ts.n_live) {
+                                const int64_t gc = mapped ? p.col_map[c] : c;
+                                v = wo_fast ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + gc])
+                                            : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + gc]);
+                            }
+                            smem_wo[o * BN + j] = v;
+                        }
                     }
                 }
-                named_bar_sync(1, 128);
+                named_bar_sync(1, EPI_THREADS);
                 const float ax = row_ok ? amax_or_127(p.row_amax[row]) : 127.0f;
                 rowf = ax;
                 sx = 127.0 / static_cast<double>(ax);
-                if (fast_o) {
+                if (stage_wo) {
 #pragma unroll
-                    for (int o = 0; o < WO_CAP; ++o)
-                        xo_r[o] = (o < n_out && row_ok) ? __half2float(p.xo[row * p.o_cap + o]) : 0.0f;
+                    for (int o = 0; o < WO_CAP; ++o) {
+                        float v = 0.0f;
+                        if (o < n_out && row_ok)
+                            v = xo_fast ? __half2float(p.xo[row * p.o_cap + o])
+                                        : __half2float(p.x[row * p.ldx + p.o_idx[o]]);
+                        xo_r[o] = v;
+                    }
                 }
             }
 
             mbar_wait(&bars->tmem_full[acc], acc_phase);
             tc_fence_after();
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 32; ++ch) {
+            for (int cc = 0; cc < COLS_PER_EPI_WARP / 32; ++cc) {
+                const int ch = half * (COLS_PER_EPI_WARP / 32) + cc;
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(t_row + ch * 32, r);
                 tmem_ld_wait();
                 const int64_t cbase = col0 + ch * 32;
-                if (!row_ok) continue;
+                if (!row_ok || cbase >= ts.n_live) continue;
+                const bool full_chunk = !mapped && p.vec_store && cbase + 32 <= ts.n_live;
                 if constexpr (EPI == EPI_I32) {
                     int32_t* yr = reinterpret_cast<int32_t*>(p.y) + row * p.ldy;
-                    if (p.vec_store && cbase + 32 <= p.N) {
+                    if (full_chunk) {
 #pragma unroll
                         for (int u = 0; u < 8; ++u)
                             *reinterpret_cast<uint4*>(yr + cbase + 4 * u) =
                                 make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]);
                     } else {
-                        for (int j = 0; j < 32; ++j)
-                            if (cbase + j < p.N) yr[cbase + j] = static_cast<int32_t>(r[j]);
+                        for (int j = 0; j < 32; ++j) {
+                            const int64_t c = cbase + j;
+                            if (c < ts.n_live) yr[mapped ? p.col_map[c] : c] = static_cast<int32_t>(r[j]);
+                        }
                     }
                 } else {
                     float v[32];
@@ -266,31 +372,45 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (n_out > 0) {
                             for (int j = 0; j < 32; ++j) {
                                 const int64_t c = cbase + j;
-                                if (c >= p.N) break;
+                                if (c >= ts.n_live) break;
+                                const int64_t gc = mapped ? p.col_map[c] : c;
                                 double hacc = 0.0;
                                 for (int o = 0; o < n_out; ++o) {
                                     const int64_t k = p.o_idx[o];
                                     const double xv = __half2float(p.x[row * p.ldx + k]);
-                                    const double wv = __half2float(p.w[k * p.ldw + c]);
+                                    const double wv = __half2float(p.w[k * p.ldw + gc]);
                                     hacc = __dadd_rn(hacc, __dmul_rn(xv, wv));
                                 }
                                 v[j] = __double2float_rn(__dadd_rn(static_cast<double>(v[j]), hacc));
                             }
                         }
                     } else {
-                        const float* cf = reinterpret_cast<const float*>(smem_col) + ch * 32;
+                        const float4* cf4 = reinterpret_cast<const float4*>(
+                            reinterpret_cast<const float*>(smem_col) + ch * 32);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            v[j] = static_cast<float>(static_cast<int32_t>(r[j])) * rowf * cf[j];
+                        for (int u = 0; u < 8; ++u) {
+                            const float4 f = cf4[u];
+                            v[4 * u + 0] = static_cast<float>(static_cast<int32_t>(r[4 * u + 0])) * rowf * f.x;
+                            v[4 * u + 1] = static_cast<float>(static_cast<int32_t>(r[4 * u + 1])) * rowf * f.y;
+                            v[4 * u + 2] = static_cast<float>(static_cast<int32_t>(r[4 * u + 2])) * rowf * f.z;
+                            v[4 * u + 3] = static_cast<float>(static_cast<int32_t>(r[4 * u + 3])) * rowf * f.w;
+                        }
                         if (n_out > 0) {
-                            if (fast_o) {
+                            if (stage_wo) {
 #pragma unroll
                                 for (int o = 0; o < WO_CAP; ++o) {
                                     if (o < n_out) {
                                         const float xv = xo_r[o];
-                                        const float* wr = smem_wo + o * BN + ch * 32;
+                                        const float4* wr = reinterpret_cast<const float4*>(
+                                            smem_wo + o * BN + ch * 32);
 #pragma unroll
-                                        for (int j = 0; j < 32; ++j) v[j] = fmaf(xv, wr[j], v[j]);
+                                        for (int u = 0; u < 8; ++u) {
+                                            const float4 f = wr[u];
+                                            v[4 * u + 0] = fmaf(xv, f.x, v[4 * u + 0]);
+                                            v[4 * u + 1] = fmaf(xv, f.y, v[4 * u + 1]);
+                                            v[4 * u + 2] = fmaf(xv, f.z, v[4 * u + 2]);
+                                            v[4 * u + 3] = fmaf(xv, f.w, v[4 * u + 3]);
+                                        }
                                     }
                                 }
                             } else {
@@ -299,7 +419,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                                     const float xv = __half2float(p.x[row * p.ldx + k]);
                                     for (int j = 0; j < 32; ++j) {
                                         const int64_t c = cbase + j;
-                                        const float wv = c < p.N ? __half2float(p.w[k * p.ldw + c]) : 0.0f;
+                                        float wv = 0.0f;
+                                        if (c < ts.n_live)
+                                            wv = __half2float(p.w[k * p.ldw + (mapped ? p.col_map[c] : c)]);
                                         v[j] = fmaf(xv, wv, v[j]);
                                     }
                                 }
@@ -308,7 +430,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                     if constexpr (EPI == EPI_F16) {
                         __half* yr = reinterpret_cast<__half*>(p.y) + row * p.ldy;
-                        if (p.vec_store && cbase + 32 <= p.N) {
+                        if (full_chunk) {
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 uint32_t pk[4];
@@ -321,19 +443,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                                     make_uint4(pk[0], pk[1], pk[2], pk[3]);
                             }
                         } else {
-                            for (int j = 0; j < 32; ++j)
-                                if (cbase + j < p.N) yr[cbase + j] = __float2half_rn(v[j]);
+                            for (int j = 0; j < 32; ++j) {
+                                const int64_t c = cbase + j;
+                                if (c < ts.n_live) yr[mapped ? p.col_map[c] : c] = __float2half_rn(v[j]);
+                            }
                         }
                     } else {
                         float* yr = reinterpret_cast<float*>(p.y) + row * p.ldy;
-                        if (p.vec_store && cbase + 32 <= p.N) {
+                        if (full_chunk) {
 #pragma unroll
                             for (int u = 0; u < 8; ++u)
                                 *reinterpret_cast<float4*>(yr + cbase + 4 * u) =
                                     make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
                         } else {
-                            for (int j = 0; j < 32; ++j)
-                                if (cbase + j < p.N) yr[cbase + j] = v[j];
+                            for (int j = 0; j < 32; ++j) {
+                                const int64_t c = cbase + j;
+                                if (c < ts.n_live) yr[mapped ? p.col_map[c] : c] = v[j];
+                            }
                         }
                     }
                 }
@@ -341,14 +467,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             // accumulator drained: hand TMEM back to the MMA warp
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_remote(&bars->tmem_empty[acc], 0);
+                else mbar_arrive(&bars->tmem_empty[acc]);
+            }
         }
     }
 
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // both CTAs done with TMEM and barriers
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem_base);
+        if constexpr (CG == 2) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+        else tmem_dealloc<TMEM_COLS>(tmem_base);
     }
 }
 
@@ -388,23 +519,53 @@ static bool make_tmap_i8(CUtensorMap* map, const int8_t* base, int64_t rows, int
     return r == CUDA_SUCCESS;
 }
 
-template <int EPI>
+template <int EPI, int CG>
 static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
                               int grid, cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
+    constexpr size_t smem = smem_total<CG>();
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(gemm_i8_kernel<EPI>,
+        attr_err = cudaFuncSetAttribute(gemm_i8_kernel<EPI, CG>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(SMEM_TOTAL));
+                                        static_cast<int>(smem));
     });
     if (attr_err != cudaSuccess) return attr_err;
-    gemm_i8_kernel<EPI><<<grid, THREADS, SMEM_TOTAL, st>>>(ta, tb, p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG>, ta, tb, p);
     count_launch();
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
+template <int EPI>
+static cudaError_t launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
+                             int grid, int cg, cudaStream_t st) {
+    return cg == 2 ? launch_epi<EPI, 2>(ta, tb, p, grid, st) : launch_epi<EPI, 1>(ta, tb, p, grid, st);
+}
+
 }  // namespace gemm
+
+// I8MM_FORCE_CG1=1 pins the 1-CTA kernel (tests cover both variants)
+static bool force_cg1() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("I8MM_FORCE_CG1");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
 
 cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     using namespace gemm;
@@ -412,19 +573,20 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     if ((a.lda % 16) || (a.ldb % 16) || (reinterpret_cast<uintptr_t>(a.a) & 15) ||
         (reinterpret_cast<uintptr_t>(a.b) & 15))
         return cudaErrorInvalidValue;
+    // CTA pairs (cta_group::2, 256-row tiles) unless M fits one 128-row tile
+    const int cg = (a.M > BM && !force_cg1()) ? 2 : 1;
     CUtensorMap ta, tb;
     const int64_t kdim = a.K > 0 ? a.K : 16;
     if (!make_tmap_i8(&ta, a.a, a.M, kdim, a.lda, BM)) return cudaErrorInvalidValue;
-    if (!make_tmap_i8(&tb, a.b, a.N, kdim, a.ldb, BN)) return cudaErrorInvalidValue;
+    if (!make_tmap_i8(&tb, a.b, a.N, kdim, a.ldb, BN / cg)) return cudaErrorInvalidValue;
     Params p{};
     p.M = a.M;
     p.N = a.N;
     p.K = a.K;
     p.num_kb = static_cast<int>((a.K + BK - 1) / BK);
     if (p.num_kb == 0) p.num_kb = 1;  // K == 0: one zero-filled block -> C = 0
-    p.m_tiles = static_cast<int>((a.M + BM - 1) / BM);
-    p.n_tiles = static_cast<int>((a.N + BN - 1) / BN);
-    p.total_tiles = p.m_tiles * p.n_tiles;
+    p.m_tiles = static_cast<int>((a.M + BM * cg - 1) / (BM * cg));
+    const int64_t max_tiles = static_cast<int64_t>(p.m_tiles) * ((a.N + BN - 1) / BN);
     p.y = a.y;
     p.ldy = a.ldy;
     p.row_amax = a.row_amax;
@@ -437,14 +599,20 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     p.o_cap = a.o_cap;
     p.o_idx = a.o_idx;
     p.o_count = a.o_count;
+    p.wo = a.wo;
+    p.ldwo = a.ldwo;
+    p.wo_cap = a.wo ? a.wo_cap : 0;
+    p.col_map = a.col_map;
+    p.n_count = a.n_count;
     const int elt = (epi == EPI_F16) ? 2 : 4;
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
-    const int grid = static_cast<int>(p.total_tiles < num_sms() ? p.total_tiles : num_sms());
+    const int64_t clusters = num_sms() / cg;
+    const int grid = cg * static_cast<int>(max_tiles < clusters ? max_tiles : clusters);
     switch (epi) {
-        case EPI_I32: return launch_epi<EPI_I32>(ta, tb, p, grid, st);
-        case EPI_F16: return launch_epi<EPI_F16>(ta, tb, p, grid, st);
-        case EPI_F32: return launch_epi<EPI_F32>(ta, tb, p, grid, st);
-        case EPI_F32_EXACT: return launch_epi<EPI_F32_EXACT>(ta, tb, p, grid, st);
+        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, p, grid, cg, st);
+        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, p, grid, cg, st);
+        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, p, grid, cg, st);
+        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, p, grid, cg, st);
         default: return cudaErrorInvalidValue;
     }
 }

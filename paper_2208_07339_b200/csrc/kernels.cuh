@@ -24,6 +24,21 @@ cudaError_t launch_quantize_cols_t(const __half* w, int64_t K, int64_t N, int64_
 cudaError_t launch_dequantize_output(const int32_t* c, int64_t M, int64_t N, int64_t ldc,
                                      const double* sx, const double* sw, float* out, int64_t ldo,
                                      cudaStream_t st);
+cudaError_t launch_gather_rows(const __half* w, int64_t ldw, int64_t N, const int32_t* idx,
+                               const int32_t* count, int64_t cap, __half* out, int64_t ldo,
+                               cudaStream_t st);
+cudaError_t launch_col_amax(const __half* w, int64_t K, int64_t N, int64_t ldw,
+                            const uint32_t* row_mask, float* col_amax, cudaStream_t st);
+int64_t topt_chunk_rows(int64_t K);
+constexpr int kTopT = 4;  // cached |w| candidates per column (weight-stationary fixup)
+cudaError_t launch_weight_prepare(const __half* w, int64_t K, int64_t N, int64_t ldw, int8_t* wq_t,
+                                  int64_t ldq, float* col_amax, uint16_t* cand_v, int32_t* cand_r,
+                                  uint32_t* scratch_v, int32_t* scratch_r, cudaStream_t st);
+cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
+                                const uint32_t* mask, const float* amax_full,
+                                const uint16_t* cand_v, const int32_t* cand_r, int32_t* p_count,
+                                int32_t* p_idx, float* p_amax, int8_t* wq_p, int64_t ldq,
+                                cudaStream_t st);
 cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int64_t lds,
                                 int8_t* dst, int64_t ldd, cudaStream_t st);
 
@@ -49,6 +64,15 @@ struct GemmArgs {
     int64_t o_cap;
     const int32_t* o_idx;
     const int32_t* o_count;
+    // compact outlier rows of W: wo[t * ldwo + j] = W[o_idx[t], j] (nullable)
+    const __half* wo;
+    int64_t ldwo;
+    int64_t wo_cap;
+    // column remap for the weight-stationary patch GEMM (nullable): output
+    // column c of this GEMM is Y column col_map[c]; the live column count is
+    // *n_count (<= N) read on the device.
+    const int32_t* col_map;
+    const int32_t* n_count;
 };
 
 cudaError_t launch_gemm_sm100(const GemmArgs& args, int epi, cudaStream_t st);

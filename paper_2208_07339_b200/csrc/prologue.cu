@@ -15,77 +15,66 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "quant_common.cuh"
 
 namespace i8mm {
 
-__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
-
-__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-
-__device__ __forceinline__ bool h_is_nonfinite(__half h) {
-    return (__half_as_ushort(h) & 0x7C00u) == 0x7C00u;
-}
-
-// quantize.py:26-29 + 115-117: clip(copysign(floor(fl64(|p|+0.5)), p), +-127)
-__device__ __forceinline__ int8_t code_of(float x, double s) {
-    double p = __dmul_rn(static_cast<double>(x), s);
-    double t = __dadd_rn(fabs(p), 0.5);
-    double r = copysign(floor(t), p);
-    r = fmin(fmax(r, -127.0), 127.0);
-    return static_cast<int8_t>(static_cast<int>(r));
-}
-
-// quantize.py:168-171: scale = 127 / amax, all-zero slice -> scale 1.
-__device__ __forceinline__ double scale_of(float amax) {
-    return 127.0 / (amax == 0.0f ? 127.0 : static_cast<double>(amax));
-}
-
 // ------------------------------------------------------------------ K1 scan
 // Vector path: each thread owns 8 consecutive columns (one 16-byte load per
-// row) for a chunk of rows; 4 adjacent lanes form one 32-bit mask word.
+// row) for a chunk of rows; 4 adjacent lanes form one 32-bit mask word. The
+// threshold test runs on the fp16 bit patterns, two halves per 32-bit SIMD
+// compare: for finite fp16 x, |x| >= a  <=>  (bits(x) & 0x7FFF) >= bits(a_h),
+// where a_h is the smallest fp16 >= (float)alpha (computed on the host), so
+// the test is exactly the reference's float32 comparison (gemm.py:210).
+__device__ __forceinline__ uint32_t half_bits_to_mask8(const uint32_t (&hit)[4]) {
+    uint32_t b = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b |= ((hit[i] & 1u) << (2 * i)) | (((hit[i] >> 16) & 1u) << (2 * i + 1));
+    return b;
+}
+
 __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M, int64_t K,
-                                        int64_t ldx, float alpha, int64_t rows_per_block,
+                                        int64_t ldx, uint32_t thr_bits, int64_t rows_per_block,
                                         uint32_t* __restrict__ col_mask,
                                         int32_t* __restrict__ nonfinite) {
     const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // vector col
     const int64_t nvec = K >> 3;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
     const int64_t r1 = min(M, r0 + rows_per_block);
-    uint32_t bits = 0, bad = 0;
+    const uint32_t thr2 = thr_bits * 0x10001u;
+    uint32_t hit[4] = {0, 0, 0, 0};
+    uint32_t bad = 0;
     if (v < nvec) {
         const __half* p = x + r0 * ldx + (v << 3);
         int64_t r = r0;
-        for (; r + 4 <= r1; r += 4) {
-            uint4 q[4];
+        for (; r + 8 <= r1; r += 8) {
+            uint4 q[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) q[u] = ld_stream_u4(p + u * ldx);
-            p += 4 * ldx;
+            for (int u = 0; u < 8; ++u) q[u] = ld_stream_u4(p + u * ldx);
+            p += 8 * ldx;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const __half* h = reinterpret_cast<const __half*>(&q[u]);
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t w4[4] = {q[u].x & 0x7FFF7FFFu, q[u].y & 0x7FFF7FFFu,
+                                        q[u].z & 0x7FFF7FFFu, q[u].w & 0x7FFF7FFFu};
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    bits |= (fabsf(__half2float(h[e])) >= alpha ? 1u : 0u) << e;
-                    bad |= h_is_nonfinite(h[e]) ? 1u : 0u;
+                for (int i = 0; i < 4; ++i) {
+                    hit[i] |= __vcmpgeu2(w4[i], thr2);
+                    bad |= __vcmpgeu2(w4[i], 0x7C007C00u);
                 }
             }
         }
         for (; r < r1; ++r, p += ldx) {
-            uint4 q = ld_stream_u4(p);
-            const __half* h = reinterpret_cast<const __half*>(&q);
+            const uint4 q = ld_stream_u4(p);
+            const uint32_t w4[4] = {q.x & 0x7FFF7FFFu, q.y & 0x7FFF7FFFu, q.z & 0x7FFF7FFFu,
+                                    q.w & 0x7FFF7FFFu};
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                bits |= (fabsf(__half2float(h[e])) >= alpha ? 1u : 0u) << e;
-                bad |= h_is_nonfinite(h[e]) ? 1u : 0u;
+            for (int i = 0; i < 4; ++i) {
+                hit[i] |= __vcmpgeu2(w4[i], thr2);
+                bad |= __vcmpgeu2(w4[i], 0x7C007C00u);
             }
         }
     }
+    const uint32_t bits = half_bits_to_mask8(hit);
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t word = bits << (8u * (lane & 3u));
     word |= __shfl_xor_sync(0xffffffffu, word, 1);
@@ -186,36 +175,64 @@ __device__ __forceinline__ uint32_t mask_byte(const uint32_t* mask, int64_t v) {
     return (mask[v >> 2] >> (8u * (v & 3))) & 0xFFu;
 }
 
+__device__ __forceinline__ uint32_t keep_word(uint32_t mbyte, int i) {
+    // 16-bit lane keep-masks for elements 2i, 2i+1 of a vector (mask bit = outlier)
+    return (((mbyte >> (2 * i)) & 1u) ? 0u : 0x0000FFFFu) |
+           (((mbyte >> (2 * i + 1)) & 1u) ? 0u : 0xFFFF0000u);
+}
+
+__device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t* red) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, d));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    v = lane < nw ? red[lane] : 0u;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, d));
+    return v;
+}
+
 // One block per row; the row stays in registers (VPT 16-byte vectors/thread).
+// amax over keep columns runs on fp16 bit patterns (monotone for |x|) with
+// 2-way SIMD max; codes use the fp32 fast path with exact f64 fallback.
 template <int VPT>
-__global__ void __launch_bounds__(512) quantize_rows_vec_kernel(const __half* __restrict__ x, int64_t K, int64_t ldx,
-                                         const uint32_t* __restrict__ col_mask,
-                                         const int32_t* __restrict__ o_idx,
-                                         const int32_t* __restrict__ o_count,
-                                         int8_t* __restrict__ xq, int64_t ldq,
-                                         float* __restrict__ row_amax, __half* __restrict__ xo,
-                                         int64_t o_cap) {
-    __shared__ float red[32];
+__global__ void __launch_bounds__(512) quantize_rows_vec_kernel(
+    const __half* __restrict__ x, int64_t K, int64_t ldx, const uint32_t* __restrict__ col_mask,
+    const int32_t* __restrict__ o_idx, const int32_t* __restrict__ o_count,
+    int8_t* __restrict__ xq, int64_t ldq, float* __restrict__ row_amax, __half* __restrict__ xo,
+    int64_t o_cap) {
+    __shared__ uint32_t red[32];
     const int64_t row = blockIdx.x;
     const int64_t nvec = K >> 3;
     const __half* xr = x + row * ldx;
     uint4 q[VPT];
     uint32_t mb[VPT];
-    float amax = 0.0f;
+    uint32_t am2 = 0;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int64_t v = threadIdx.x + static_cast<int64_t>(j) * blockDim.x;
+        mb[j] = 0xFFu;
+        if (v < nvec) {
+            q[j] = ld_stream_u4(xr + (v << 3));
+            mb[j] = col_mask ? mask_byte(col_mask, v) : 0u;
+        }
+    }
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
         const int64_t v = threadIdx.x + static_cast<int64_t>(j) * blockDim.x;
         if (v < nvec) {
-            q[j] = ld_stream_u4(xr + (v << 3));
-            mb[j] = col_mask ? mask_byte(col_mask, v) : 0u;
-            const __half* h = reinterpret_cast<const __half*>(&q[j]);
+            const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (!((mb[j] >> e) & 1u)) amax = fmaxf(amax, fabsf(__half2float(h[e])));
+            for (int i = 0; i < 4; ++i)
+                am2 = __vmaxu2(am2, (w4[i] & 0x7FFF7FFFu) & keep_word(mb[j], i));
         }
     }
-    amax = block_max(amax, red);
+    const uint32_t am_bits = block_max_u32(max(am2 & 0xFFFFu, am2 >> 16), red);
+    const float amax = __half2float(__ushort_as_half(static_cast<unsigned short>(am_bits)));
     const double s = scale_of(amax);
+    const float s32 = static_cast<float>(s);
     int8_t* qr = xq + row * ldq;
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
@@ -225,8 +242,8 @@ __global__ void __launch_bounds__(512) quantize_rows_vec_kernel(const __half* __
             uint32_t lo = 0, hi = 0;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const int8_t c = ((mb[j] >> e) & 1u) ? int8_t(0) : code_of(__half2float(h[e]), s);
-                const uint32_t b = static_cast<uint32_t>(static_cast<uint8_t>(c));
+                const int c = ((mb[j] >> e) & 1u) ? 0 : code_fast(__half2float(h[e]), s32, s);
+                const uint32_t b = static_cast<uint32_t>(c) & 0xFFu;
                 if (e < 4) lo |= b << (8 * e);
                 else hi |= b << (8 * (e - 4));
             }
@@ -276,82 +293,6 @@ __global__ void quantize_rows_scalar_kernel(const __half* __restrict__ x, int64_
     }
 }
 
-// ------------------------------------------------------------------ K3 cols
-// Column absmax over keep rows. Threads own 2 adjacent columns (half2), the
-// grid splits K into chunks; partial maxima merge with an integer atomicMax
-// on the float bit pattern (valid: amax >= 0). col_amax must be zeroed.
-__global__ void col_amax_kernel(const __half* __restrict__ w, int64_t K, int64_t N, int64_t ldw,
-                                const uint32_t* __restrict__ row_mask, int64_t rows_per_block,
-                                float* __restrict__ col_amax) {
-    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
-    const int64_t k0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
-    const int64_t k1 = min(K, k0 + rows_per_block);
-    if (j >= N) return;
-    float m0 = 0.0f, m1 = 0.0f;
-    const bool pair = (j + 1 < N) && ((ldw & 1) == 0);
-    for (int64_t k = k0; k < k1; ++k) {
-        if (row_mask && ((row_mask[k >> 5] >> (k & 31)) & 1u)) continue;  // block-uniform
-        if (pair) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(w + k * ldw + j));
-            m0 = fmaxf(m0, fabsf(f.x));
-            m1 = fmaxf(m1, fabsf(f.y));
-        } else {
-            m0 = fmaxf(m0, fabsf(__half2float(w[k * ldw + j])));
-            if (j + 1 < N) m1 = fmaxf(m1, fabsf(__half2float(w[k * ldw + j + 1])));
-        }
-    }
-    atomicMax(reinterpret_cast<int*>(col_amax + j), __float_as_int(m0));
-    if (j + 1 < N) atomicMax(reinterpret_cast<int*>(col_amax + j + 1), __float_as_int(m1));
-}
-
-// Quantize a 64(k) x 64(n) tile of W and store it transposed (WqT[n][k]).
-__global__ void quantize_cols_t_kernel(const __half* __restrict__ w, int64_t K, int64_t N,
-                                       int64_t ldw, const uint32_t* __restrict__ row_mask,
-                                       const float* __restrict__ col_amax,
-                                       int8_t* __restrict__ wq_t, int64_t ldq) {
-    __shared__ double sc[64];
-    __shared__ int8_t tile[64][64 + 4];  // [n][k]
-    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 64;
-    const int64_t k0 = static_cast<int64_t>(blockIdx.y) * 64;
-    const int tid = threadIdx.x;  // 256 threads
-    if (tid < 64) sc[tid] = (n0 + tid < N) ? scale_of(col_amax[n0 + tid]) : 1.0;
-    __syncthreads();
-    // each thread: one k row (tid / 4), 16 columns ((tid % 4) * 16 ..)
-    const int kr = tid >> 2;
-    const int nc = (tid & 3) * 16;
-    const int64_t k = k0 + kr;
-    const bool kvalid = k < K;
-    const bool out = kvalid && row_mask && ((row_mask[k >> 5] >> (k & 31)) & 1u);
-#pragma unroll 4
-    for (int e = 0; e < 16; ++e) {
-        const int64_t n = n0 + nc + e;
-        int8_t c = 0;
-        if (kvalid && !out && n < N) c = code_of(__half2float(w[k * ldw + n]), sc[nc + e]);
-        tile[nc + e][kr] = c;
-    }
-    __syncthreads();
-    // store: each thread writes 16 bytes (one n row, 16 k) -> 64 rows x 4 chunks
-    const int nr = tid >> 2;
-    const int kc = (tid & 3) * 16;
-    const int64_t n = n0 + nr;
-    if (n < N) {
-        int8_t* dst = wq_t + n * ldq + k0 + kc;
-        const int64_t lim = imin64(16, ldq - (k0 + kc));
-        if (lim == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
-            uint32_t wv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                wv[u] = static_cast<uint32_t>(static_cast<uint8_t>(tile[nr][kc + 4 * u])) |
-                        static_cast<uint32_t>(static_cast<uint8_t>(tile[nr][kc + 4 * u + 1])) << 8 |
-                        static_cast<uint32_t>(static_cast<uint8_t>(tile[nr][kc + 4 * u + 2])) << 16 |
-                        static_cast<uint32_t>(static_cast<uint8_t>(tile[nr][kc + 4 * u + 3])) << 24;
-            *reinterpret_cast<uint4*>(dst) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-        } else {
-            for (int64_t u = 0; u < lim; ++u) dst[u] = tile[nr][kc + u];
-        }
-    }
-}
-
 // ------------------------------------------------------------------ dequant
 __global__ void dequantize_output_kernel(const int32_t* __restrict__ c, int64_t M, int64_t N,
                                          int64_t ldc, const double* __restrict__ sx,
@@ -382,15 +323,13 @@ __global__ void transpose_i8_kernel(const int8_t* __restrict__ src, int64_t rows
 }
 
 // ------------------------------------------------------------------ launchers
-static inline int grid_rows_chunk(int64_t M, int64_t col_blocks, int64_t target_blocks,
-                                  int64_t* rows_per_block) {
-    int64_t chunks = (target_blocks + col_blocks - 1) / col_blocks;
-    if (chunks < 1) chunks = 1;
-    if (chunks > M) chunks = M;
-    int64_t rpb = (M + chunks - 1) / chunks;
-    if (rpb < 1) rpb = 1;
-    *rows_per_block = rpb;
-    return static_cast<int>((M + rpb - 1) / rpb);
+// smallest fp16 bit pattern h (as |x| bits) with float(h) >= alpha (alpha > 0)
+static uint32_t alpha_threshold_bits(float alpha) {
+    if (!(alpha <= 65504.0f)) return 0x7C00u;  // only +-inf would qualify
+    __half h = __float2half_rn(alpha);
+    uint32_t b = __half_as_ushort(h) & 0x7FFFu;
+    if (__half2float(h) < alpha) b += 1u;
+    return b;
 }
 
 cudaError_t launch_outlier_scan(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
@@ -408,7 +347,7 @@ cudaError_t launch_outlier_scan(const __half* x, int64_t M, int64_t K, int64_t l
         const int64_t cb = (nvec + 255) / 256;
         const int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
         outlier_scan_vec_kernel<<<dim3(static_cast<unsigned>(cb), rb), 256, 0, st>>>(
-            x, M, K, ldx, alpha, rpb, col_mask, nonfinite);
+            x, M, K, ldx, alpha_threshold_bits(alpha), rpb, col_mask, nonfinite);
     } else {
         const int64_t cb = (K + 255) / 256;
         const int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
@@ -450,13 +389,15 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
         count_launch();
         return cudaGetLastError();
     }
+    // ~8 vectors (64 halves) per thread keeps 8 16-byte loads in flight; the
+    // block grows with K up to 512 threads, then VPT grows (<= 16).
     const int64_t nvec = K >> 3;
-    int vpt = 1;
-    while (vpt < 16 && (nvec + vpt - 1) / vpt > 512) vpt <<= 1;
-    int64_t threads = (nvec + vpt - 1) / vpt;
-    threads = ((threads + 31) / 32) * 32;
+    int64_t threads = ((nvec + 8 * 32 - 1) / (8 * 32)) * 32;
     if (threads < 64) threads = 64;
-    if (threads > 1024) return cudaErrorInvalidValue;
+    if (threads > 512) threads = 512;
+    int vpt = 1;
+    while (vpt < 16 && static_cast<int64_t>(vpt) * threads < nvec) vpt <<= 1;
+    if (static_cast<int64_t>(vpt) * threads < nvec) return cudaErrorInvalidValue;
     const int t = static_cast<int>(threads);
     switch (vpt) {
         case 1: launch_qrows<1>(t, x, M, K, ldx, mask, o_idx, o_count, xq, ldq, amax, xo, o_cap, st); break;
@@ -465,26 +406,6 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
         case 8: launch_qrows<8>(t, x, M, K, ldx, mask, o_idx, o_count, xq, ldq, amax, xo, o_cap, st); break;
         default: launch_qrows<16>(t, x, M, K, ldx, mask, o_idx, o_count, xq, ldq, amax, xo, o_cap, st); break;
     }
-    count_launch();
-    return cudaGetLastError();
-}
-
-cudaError_t launch_quantize_cols_t(const __half* w, int64_t K, int64_t N, int64_t ldw,
-                                   const uint32_t* row_mask, int8_t* wq_t, int64_t ldq,
-                                   float* col_amax, cudaStream_t st) {
-    if (N == 0) return cudaSuccess;
-    zero_u32_kernel<<<static_cast<unsigned>(imin64((N + 255) / 256, 1024)), 256, 0, st>>>(
-        reinterpret_cast<uint32_t*>(col_amax), N);
-    count_launch();
-    const int64_t cb = ((N + 1) / 2 + 255) / 256;
-    int64_t rpb;
-    const int rb = grid_rows_chunk(K, cb, static_cast<int64_t>(num_sms()) * 8, &rpb);
-    col_amax_kernel<<<dim3(static_cast<unsigned>(cb), rb), 256, 0, st>>>(w, K, N, ldw, row_mask,
-                                                                           rpb, col_amax);
-    count_launch();
-    const int64_t kt = (ldq + 63) / 64;  // cover the padding columns too (written as 0)
-    quantize_cols_t_kernel<<<dim3(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>(kt)),
-                             256, 0, st>>>(w, K, N, ldw, row_mask, col_amax, wq_t, ldq);
     count_launch();
     return cudaGetLastError();
 }

@@ -178,19 +178,34 @@ def dequantize_output(c, params_x, params_w) -> torch.Tensor:
     return out
 
 
-def _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, out_dtype, exact):
-    dev = xq.device
+def _gather_outlier_rows(w16: torch.Tensor, scan: OutlierScan, cap: int = O_CAP):
+    """Compact W[O, :] (fp16, cap x ceil8(N)) for the GEMM epilogue (gemm.py:238)."""
+    k, n = w16.shape
+    ldwo = round_up(n, 8)
+    wo = torch.empty((cap, ldwo), dtype=torch.float16, device=w16.device)
+    nat.check(nat.lib().i8mm_gather_outlier_rows(
+        w16.data_ptr(), w16.stride(0), n, scan.idx.data_ptr(), scan.count.data_ptr(), cap,
+        wo.data_ptr(), ldwo, stream_handle()), "gather_outlier_rows")
+    return wo
+
+
+def _out_kind(out_dtype, exact):
     if exact:
-        kind, dt = nat.OUT_F32_EXACT, torch.float32
-    else:
-        if out_dtype not in OUT_KINDS:
-            raise ValueError(f"out_dtype must be float16 or float32, got {out_dtype}")
-        kind, dt = OUT_KINDS[out_dtype], out_dtype
+        return nat.OUT_F32_EXACT, torch.float32
+    if out_dtype not in OUT_KINDS:
+        raise ValueError(f"out_dtype must be float16 or float32, got {out_dtype}")
+    return OUT_KINDS[out_dtype], out_dtype
+
+
+def _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, out_dtype, exact, wo=None):
+    dev = xq.device
+    kind, dt = _out_kind(out_dtype, exact)
     y = torch.empty((m, n), dtype=dt, device=dev)
     nat.check(nat.lib().i8mm_gemm_dequant(
         xq.data_ptr(), wq_t.data_ptr(), ldq, m, n, k, ax.data_ptr(), aw.data_ptr(),
         x16.data_ptr(), x16.stride(0), w16.data_ptr(), w16.stride(0),
         xo.data_ptr() if xo is not None else None, xo.shape[1] if xo is not None else 0,
+        wo.data_ptr() if wo is not None else None, wo.shape[1] if wo is not None else 0,
         scan.idx.data_ptr() if scan is not None else None,
         scan.count.data_ptr() if scan is not None else None,
         y.data_ptr(), n, kind, stream_handle()), "gemm_dequant")
@@ -220,7 +235,7 @@ def vectorwise_matmul(x, w, out_dtype: torch.dtype = torch.float16, exact: bool 
 
 
 def llm_int8_matmul(x, w, alpha: float = 6.0, out_dtype: torch.dtype = torch.float16,
-                    exact: bool = False, validate: bool = True) -> MatmulResult:
+                    exact: bool = False, validate: bool = True, _timer=None) -> MatmulResult:
     """Mixed-precision X @ W: outlier feature columns in high precision, the rest
     through the vector-wise int8 path with constants recomputed on the
     sub-matrices; the two partial products summed (gemm.py:214-247).
@@ -243,7 +258,12 @@ def llm_int8_matmul(x, w, alpha: float = 6.0, out_dtype: torch.dtype = torch.flo
         _check_finite(w16, "w")
     xq, ldq, ax, xo = _quantize_rows(x16, scan)  # gemm.py:242 (+ gather, gemm.py:238)
     wq_t, _, aw = _quantize_cols_t(w16, scan)  # gemm.py:243
-    y = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, out_dtype, exact)
+    wo = _gather_outlier_rows(w16, scan)  # gemm.py:238
+    if _timer is not None:
+        _timer.mark("gemm_begin")
+    y = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, out_dtype, exact, wo)
+    if _timer is not None:
+        _timer.mark("gemm_end")
     return MatmulResult(y, "llm_int8", scan.count, k)
 
 
@@ -262,8 +282,11 @@ def llm_int8_trace(x, w, alpha: float = 6.0) -> dict:
     L = nat.lib()
     nat.check(L.i8mm_gemm_i32(xq.data_ptr(), ldq, wq_t.data_ptr(), ldq, c.data_ptr(), n, m, n, k,
                               stream_handle()), "gemm_i32")
-    y16 = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, torch.float16, False)
-    y32 = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, torch.float32, False)
-    yex = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, None, True)
+    wo = _gather_outlier_rows(w16, scan)
+    y16 = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, torch.float16, False,
+                        wo)
+    y32 = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, torch.float32, False,
+                        wo)
+    yex = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, None, True, wo)
     return {"scan": scan, "xq": xq[:, :k], "row_amax": ax, "wq_t": wq_t[:, :k], "col_amax": aw,
             "c": c, "y16": y16, "y32": y32, "y_exact": yex, "xo": xo}

@@ -13,8 +13,10 @@ from dataclasses import dataclass
 
 import torch
 
-from ._tensors import as_f16_matrix
-from .gemm import llm_int8_matmul, vectorwise_matmul
+from . import _native as nat
+from ._tensors import as_f16_matrix, stream_handle
+from .errors import ShapeMismatchError
+from .gemm import _out_kind, llm_int8_matmul, vectorwise_matmul
 
 BACKEND_KINDS = ("exact", "absmax", "zeropoint", "vectorwise", "llm_int8")
 
@@ -72,19 +74,92 @@ class Int8Linear(torch.nn.Module):
     ``weight`` is K x N (the reference orientation, transformer.py:291-346);
     use ``Int8Linear.from_linear`` for an ``nn.Linear`` (N x K weight). The
     per-call semantics are exactly ``llm_int8_matmul`` (gemm.py:214-247).
+
+    Weight-stationary (default): the int8 codes of W with full-column scales
+    and each column's top-4 |w| candidates are prepared once
+    (``i8mm_linear_prepare``); every call reproduces the reference's per-call
+    column scales over the keep rows exactly by patching only the columns
+    whose cached maximisers are all outlier rows (``i8mm_linear_forward``).
+    ``weight_stationary=False`` re-quantizes W on every call like the reference.
     """
 
     def __init__(self, weight, alpha: float = 6.0, bias=None,
-                 out_dtype: torch.dtype = torch.float16) -> None:
+                 out_dtype: torch.dtype = torch.float16, weight_stationary: bool = True) -> None:
         super().__init__()
+        if not (float(alpha) > 0):
+            raise ValueError(f"alpha must be positive, got {alpha}")
         self.alpha = float(alpha)
         self.out_dtype = out_dtype
+        self.weight_stationary = bool(weight_stationary)
         self.register_buffer("weight", as_f16_matrix(weight, "weight"))
         if bias is not None:
             b = torch.as_tensor(bias).to(device=self.weight.device, dtype=out_dtype)
             self.register_buffer("bias", b)
         else:
             self.bias = None
+        self.wbuf = None
+        self._last_ws = None
+        if self.weight_stationary:
+            self._prepare()
+
+    def _prepare(self) -> None:
+        L = nat.lib()
+        k, n = self.weight.shape
+        dev = self.weight.device
+        self.wbuf = torch.empty(L.i8mm_linear_weight_bytes(k, n), dtype=torch.uint8, device=dev)
+        scratch = torch.empty(L.i8mm_linear_prepare_scratch_bytes(k, n), dtype=torch.uint8,
+                              device=dev)
+        nat.check(L.i8mm_linear_prepare(self.weight.data_ptr(), self.weight.stride(0), k, n,
+                                        self.wbuf.data_ptr(), self.wbuf.numel(),
+                                        scratch.data_ptr(), scratch.numel(), stream_handle()),
+                  "linear_prepare")
+
+    def matmul(self, x2: torch.Tensor, exact: bool = False, _timer=None) -> torch.Tensor:
+        """Y = x2 @ W for an M x K fp16 CUDA matrix (no bias)."""
+        if not self.weight_stationary:
+            return llm_int8_matmul(x2, self.weight, self.alpha, out_dtype=self.out_dtype,
+                                   exact=exact, validate=False, _timer=_timer).output
+        L = nat.lib()
+        k, n = self.weight.shape
+        m = x2.shape[0]
+        if x2.shape[1] != k:
+            raise ShapeMismatchError(f"inner dimensions differ: X is {m}x{x2.shape[1]}, W is {k}x{n}")
+        kind, dt = _out_kind(self.out_dtype, exact)
+        ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8,
+                         device=x2.device)
+        y = torch.empty((m, n), dtype=dt, device=x2.device)
+        st = stream_handle()
+        w = self.weight
+        nat.check(L.i8mm_linear_prologue(x2.data_ptr(), x2.stride(0), m, w.data_ptr(), w.stride(0),
+                                         self.wbuf.data_ptr(), k, n, self.alpha, ws.data_ptr(),
+                                         ws.numel(), st), "linear_prologue")
+        if _timer is not None:
+            _timer.mark("gemm_begin")
+        nat.check(L.i8mm_linear_gemm(x2.data_ptr(), x2.stride(0), m, w.data_ptr(), w.stride(0),
+                                     self.wbuf.data_ptr(), k, n, y.data_ptr(), n, kind,
+                                     ws.data_ptr(), ws.numel(), st), "linear_gemm")
+        if _timer is not None:
+            _timer.mark("gemm_end")
+        self._last_ws = (ws, m)
+        return y
+
+    def last_stats(self) -> dict:
+        """|O| and the patched-column count of the last weight-stationary call (syncs)."""
+        if self._last_ws is None:
+            return {}
+        import ctypes
+
+        ws, m = self._last_ws
+        k, n = self.weight.shape
+        views = (ctypes.c_void_p * 8)()
+        nat.check(nat.lib().i8mm_linear_workspace_views(ws.data_ptr(), m, k, n, views, 8))
+        # read the two device counters through byte views of the workspace
+        base = ws.data_ptr()
+        o_off = views[0] - base
+        p_off = views[4] - base
+        o = int(ws[o_off:o_off + 4].view(torch.int32).item())
+        p = int(ws[p_off:p_off + 4].view(torch.int32).item())
+        return {"decomposed_cols": o, "patched_cols": p}
 
     @classmethod
     def from_linear(cls, lin: torch.nn.Linear, alpha: float = 6.0) -> "Int8Linear":
@@ -99,11 +174,10 @@ class Int8Linear(torch.nn.Module):
     def out_features(self) -> int:
         return self.weight.shape[1]
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, _timer=None) -> torch.Tensor:
         lead = x.shape[:-1]
-        x2 = x.reshape(-1, x.shape[-1])
-        y = llm_int8_matmul(x2, self.weight, self.alpha, out_dtype=self.out_dtype,
-                            validate=False).output
+        x2 = as_f16_matrix(x.reshape(-1, x.shape[-1]), "x")
+        y = self.matmul(x2, _timer=_timer)
         if self.bias is not None:
             y = y + self.bias
         return y.reshape(*lead, y.shape[-1])

@@ -40,3 +40,13 @@ for (m, k, n) in [(16384, 4096, 16384), (16384, 16384, 4096), (16384, 12288, 491
           f"full {t_full*1e3:.1f}us ({ops/t_full/1e9:.0f} TOPS) | cublas _int_mm {t_ref*1e3:.1f}us ({ops/t_ref/1e9:.0f}) bf16 {t_bf*1e3:.1f}us ({ops/t_bf/1e9:.0f})", flush=True)
     del x, w, xq, wq, c
     torch.cuda.empty_cache()
+
+import paper_2208_07339_b200 as pkg
+for (m, k, n) in [(16384, 4096, 16384), (16384, 16384, 4096), (16384, 12288, 49152)]:
+    x, w, _ = planted_pair_device(m, k, n, 6, 20.0, 0)
+    lin = pkg.Int8Linear(w, 6.0)
+    ops = 2 * m * n * k
+    t = t_ev(lambda: lin(x))
+    print(f"Int8Linear M={m} K={k} N={n}: {t*1e3:.1f}us ({ops/t/1e9:.0f} TOPS) stats={lin.last_stats()}", flush=True)
+    del lin, x, w
+    torch.cuda.empty_cache()

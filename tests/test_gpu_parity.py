@@ -283,3 +283,96 @@ def test_capi_pipeline_entry(p, oracle_mod):
     assert np.array_equal(_np(y), ref.output)
     assert L.i8mm_llm_int8_matmul(x16.data_ptr(), 768, w16.data_ptr(), 320, 200, 768, 320, -1.0,
                                   y.data_ptr(), 320, 0, ws.data_ptr(), ws_bytes, None, st) == 3
+
+
+# ---------------------------------------------------------------- weight-stationary module
+def _ws_case(seed, m, k, n, n_out, heavy_rows=0):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = rng.standard_normal((m, k)).astype(np.float32)
+    cols = rng.choice(k, size=n_out, replace=False)
+    x[:, cols] *= 20.0
+    w = rng.standard_normal((k, n)).astype(np.float32)
+    if heavy_rows:
+        # make outlier rows the column maximisers so their exclusion changes
+        # many column scales (forces patches; > 4 heavy rows forces rescans)
+        w[cols[:heavy_rows], :] *= 4.0
+    return x.astype(np.float16).astype(np.float32), w.astype(np.float16).astype(np.float32)
+
+
+@pytest.mark.parametrize("case", [(0, 256, 1024, 512, 6, 0), (1, 97, 1040, 328, 6, 2),
+                                  (2, 130, 512, 300, 8, 8), (3, 64, 256, 1000, 3, 3),
+                                  (4, 1, 512, 256, 6, 0), (5, 33, 3, 40, 2, 2)])
+def test_weight_stationary_matches_reference_semantics(p, oracle_mod, case):
+    seed, m, k, n, n_out, heavy = case
+    x, w = _ws_case(seed, m, k, n, n_out, heavy)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda(), alpha=6.0)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    y_exact = lin.matmul(x16, exact=True)
+    assert np.array_equal(_np(y_exact), ref.output)
+    st = lin.last_stats()
+    assert st["decomposed_cols"] == len(ref.dims)
+    if heavy:
+        assert st["patched_cols"] > 0
+    y16 = lin(x16)
+    y16_fn = p.llm_int8_matmul(x16, lin.weight, 6.0).output
+    assert torch.equal(y16, y16_fn), "weight-stationary and per-call paths must agree bitwise"
+
+
+def test_weight_stationary_candidates(p):
+    """The cached top-4 |w| candidates per column match a host recomputation."""
+    import ctypes
+
+    from paper_2208_07339_b200 import _native as nat
+
+    rng = np.random.Generator(np.random.PCG64(9))
+    k, n = 1500, 72
+    w = rng.standard_normal((k, n)).astype(np.float16)
+    w[10, 5] = w[20, 5] = w[30, 5] = np.float16(9.0)  # ties keep ascending rows
+    lin = p.Int8Linear(torch.from_numpy(w).cuda())
+    views = (ctypes.c_void_p * 4)()
+    nat.check(nat.lib().i8mm_linear_weight_views(lin.wbuf.data_ptr(), k, n, views, 4))
+    base = lin.wbuf.data_ptr()
+    off_v, off_r = views[2] - base, views[3] - base
+    cv = lin.wbuf[off_v:off_v + 2 * 4 * n].view(torch.int16).cpu().numpy().reshape(4, n)
+    cr = lin.wbuf[off_r:off_r + 4 * 4 * n].view(torch.int32).cpu().numpy().reshape(4, n)
+    a = np.abs(w.astype(np.float32))
+    for j in range(n):
+        order = sorted(range(k), key=lambda r: (-a[r, j], r))[:4]
+        assert list(cr[:, j]) == order
+        assert np.array_equal(cv[:, j].view(np.float16).astype(np.float32), a[order, j])
+    assert list(cr[:3, 5]) == [10, 20, 30]
+
+
+_CG1_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2208_07339_b200 as p
+from oracle import oracle as orc
+for (m, n, k) in [(300, 257, 1000), (384, 768, 2048), (129, 40, 16)]:
+    rng = np.random.Generator(np.random.PCG64(m + n + k))
+    a = rng.integers(-127, 128, size=(m, k), dtype=np.int8)
+    b = rng.integers(-127, 128, size=(k, n), dtype=np.int8)
+    assert np.array_equal(p.int8_gemm_i32(a, b).cpu().numpy(), orc.c_gemm_i32(a, b)), (m, n, k)
+x, w = orc.planted_pair(300, 1024, 520, 6, 20.0, 1)
+x = x.astype(np.float16).astype(np.float32); w = w.astype(np.float16).astype(np.float32)
+ref = orc.c_llm_int8_matmul(x, w, 6.0)
+assert np.array_equal(p.llm_int8_matmul(x, w, 6.0, exact=True).output.cpu().numpy(), ref.output)
+lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+assert np.array_equal(lin.matmul(torch.from_numpy(x.astype(np.float16)).cuda(), exact=True).cpu().numpy(), ref.output)
+print("CG1 OK")
+"""
+
+
+def test_one_cta_kernel_variant(p):
+    """The 1-CTA (cta_group::1) GEMM variant, pinned via I8MM_FORCE_CG1=1."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    env = dict(os.environ, I8MM_FORCE_CG1="1")
+    r = subprocess.run([sys.executable, "-c", _CG1_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "CG1 OK" in r.stdout, r.stdout + r.stderr
