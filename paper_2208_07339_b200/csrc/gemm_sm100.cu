@@ -137,9 +137,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int STAGES = C::STAGES;
     constexpr int B_BYTES = C::B_BYTES;
     constexpr size_t SMEM_OPERANDS = C::SMEM_OPERANDS;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for SWIZZLE_128B, by offsetting within the shared
+    // array (pointer arithmetic keeps the shared address space -> LDS, not LD)
+    uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + static_cast<size_t>(STAGES) * A_BYTES;
     float* smem_wo = reinterpret_cast<float*>(smem + SMEM_OPERANDS);
@@ -385,31 +386,34 @@ __global__ void __launch_bounds__(THREADS, 1)
                             }
                         }
                     } else {
+                        // dequant + outlier FMAs on packed f32x2 (sm_100 FMUL2 / FFMA2)
                         const float4* cf4 = reinterpret_cast<const float4*>(
                             reinterpret_cast<const float*>(smem_col) + ch * 32);
+                        float2* v2 = reinterpret_cast<float2*>(v);
+                        const float2 rf2 = make_float2(rowf, rowf);
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
                             const float4 f = cf4[u];
-                            v[4 * u + 0] = static_cast<float>(static_cast<int32_t>(r[4 * u + 0])) * rowf * f.x;
-                            v[4 * u + 1] = static_cast<float>(static_cast<int32_t>(r[4 * u + 1])) * rowf * f.y;
-                            v[4 * u + 2] = static_cast<float>(static_cast<int32_t>(r[4 * u + 2])) * rowf * f.z;
-                            v[4 * u + 3] = static_cast<float>(static_cast<int32_t>(r[4 * u + 3])) * rowf * f.w;
+                            const float2 c01 = make_float2(static_cast<float>(static_cast<int32_t>(r[4 * u + 0])),
+                                                           static_cast<float>(static_cast<int32_t>(r[4 * u + 1])));
+                            const float2 c23 = make_float2(static_cast<float>(static_cast<int32_t>(r[4 * u + 2])),
+                                                           static_cast<float>(static_cast<int32_t>(r[4 * u + 3])));
+                            v2[2 * u] = __fmul2_rn(__fmul2_rn(c01, rf2), make_float2(f.x, f.y));
+                            v2[2 * u + 1] = __fmul2_rn(__fmul2_rn(c23, rf2), make_float2(f.z, f.w));
                         }
                         if (n_out > 0) {
                             if (stage_wo) {
 #pragma unroll
                                 for (int o = 0; o < WO_CAP; ++o) {
                                     if (o < n_out) {
-                                        const float xv = xo_r[o];
+                                        const float2 xv2 = make_float2(xo_r[o], xo_r[o]);
                                         const float4* wr = reinterpret_cast<const float4*>(
                                             smem_wo + o * BN + ch * 32);
 #pragma unroll
                                         for (int u = 0; u < 8; ++u) {
                                             const float4 f = wr[u];
-                                            v[4 * u + 0] = fmaf(xv, f.x, v[4 * u + 0]);
-                                            v[4 * u + 1] = fmaf(xv, f.y, v[4 * u + 1]);
-                                            v[4 * u + 2] = fmaf(xv, f.z, v[4 * u + 2]);
-                                            v[4 * u + 3] = fmaf(xv, f.w, v[4 * u + 3]);
+                                            v2[2 * u] = __ffma2_rn(xv2, make_float2(f.x, f.y), v2[2 * u]);
+                                            v2[2 * u + 1] = __ffma2_rn(xv2, make_float2(f.z, f.w), v2[2 * u + 1]);
                                         }
                                     }
                                 }

@@ -26,13 +26,10 @@ namespace i8mm {
 // compare: for finite fp16 x, |x| >= a  <=>  (bits(x) & 0x7FFF) >= bits(a_h),
 // where a_h is the smallest fp16 >= (float)alpha (computed on the host), so
 // the test is exactly the reference's float32 comparison (gemm.py:210).
-__device__ __forceinline__ uint32_t half_bits_to_mask8(const uint32_t (&hit)[4]) {
-    uint32_t b = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) b |= ((hit[i] & 1u) << (2 * i)) | (((hit[i] >> 16) & 1u) << (2 * i + 1));
-    return b;
-}
-
+// Per column the kernel keeps max_i (bits(x_ik) & 0x7FFF) with the SIMD
+// unsigned max (two halves per 32-bit word); the column is an outlier iff that
+// max >= bits(a_h). NaN/Inf patterns are >= 0x7C00, so they surface both as
+// outliers and through the nonfinite flag.
 __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M, int64_t K,
                                         int64_t ldx, uint32_t thr_bits, int64_t rows_per_block,
                                         uint32_t* __restrict__ col_mask,
@@ -41,9 +38,7 @@ __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M,
     const int64_t nvec = K >> 3;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
     const int64_t r1 = min(M, r0 + rows_per_block);
-    const uint32_t thr2 = thr_bits * 0x10001u;
-    uint32_t hit[4] = {0, 0, 0, 0};
-    uint32_t bad = 0;
+    uint32_t m[4] = {0, 0, 0, 0};
     if (v < nvec) {
         const __half* p = x + r0 * ldx + (v << 3);
         int64_t r = r0;
@@ -54,27 +49,28 @@ __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M,
             p += 8 * ldx;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const uint32_t w4[4] = {q[u].x & 0x7FFF7FFFu, q[u].y & 0x7FFF7FFFu,
-                                        q[u].z & 0x7FFF7FFFu, q[u].w & 0x7FFF7FFFu};
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    hit[i] |= __vcmpgeu2(w4[i], thr2);
-                    bad |= __vcmpgeu2(w4[i], 0x7C007C00u);
-                }
+                m[0] = __vmaxu2(m[0], q[u].x & 0x7FFF7FFFu);
+                m[1] = __vmaxu2(m[1], q[u].y & 0x7FFF7FFFu);
+                m[2] = __vmaxu2(m[2], q[u].z & 0x7FFF7FFFu);
+                m[3] = __vmaxu2(m[3], q[u].w & 0x7FFF7FFFu);
             }
         }
         for (; r < r1; ++r, p += ldx) {
             const uint4 q = ld_stream_u4(p);
-            const uint32_t w4[4] = {q.x & 0x7FFF7FFFu, q.y & 0x7FFF7FFFu, q.z & 0x7FFF7FFFu,
-                                    q.w & 0x7FFF7FFFu};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                hit[i] |= __vcmpgeu2(w4[i], thr2);
-                bad |= __vcmpgeu2(w4[i], 0x7C007C00u);
-            }
+            m[0] = __vmaxu2(m[0], q.x & 0x7FFF7FFFu);
+            m[1] = __vmaxu2(m[1], q.y & 0x7FFF7FFFu);
+            m[2] = __vmaxu2(m[2], q.z & 0x7FFF7FFFu);
+            m[3] = __vmaxu2(m[3], q.w & 0x7FFF7FFFu);
         }
     }
-    const uint32_t bits = half_bits_to_mask8(hit);
+    uint32_t bits = 0, bad = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t lo = m[i] & 0xFFFFu, hi = m[i] >> 16;
+        bits |= (lo >= thr_bits ? 1u : 0u) << (2 * i);
+        bits |= (hi >= thr_bits ? 1u : 0u) << (2 * i + 1);
+        bad |= (lo >= 0x7C00u || hi >= 0x7C00u) ? 1u : 0u;
+    }
     const uint32_t lane = threadIdx.x & 31u;
     uint32_t word = bits << (8u * (lane & 3u));
     word |= __shfl_xor_sync(0xffffffffu, word, 1);
@@ -194,6 +190,56 @@ __device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t* red) {
     return v;
 }
 
+__device__ __noinline__ int code_of_slow(float x, double s) { return static_cast<int>(code_of(x, s)); }
+
+// Quantize 8 fp16 values (one 16-byte vector) with the row scale: the fp32
+// fast path for all 8, one band test for the vector, and the exact f64 rule
+// only for elements within 2^-14 of a rounding boundary (see code_fast).
+// Rounding uses the 1.5*2^23 magic constant (FADDs on the full-rate FMA pipe,
+// not the quarter-rate conversion pipe): t = p + M rounds p to the nearest
+// integer and the low byte of bits(t) IS the two's-complement int8 code.
+// mbyte bit e set = outlier column -> code 0. Returns the 8 codes packed.
+__device__ __forceinline__ uint2 quant8(const uint4& q, uint32_t mbyte, float s32, double s) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    const __half2* h2 = reinterpret_cast<const __half2*>(&q);
+    const float2 s2 = make_float2(s32, s32);
+    const float2 m2 = make_float2(kMagic, kMagic);
+    const float2 nm2 = make_float2(-kMagic, -kMagic);
+    float2 pf[4], r[4];
+    uint32_t tb[8];
+    float dmax = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // packed f32x2 math (sm_100 FMUL2/FADD2)
+        pf[i] = __fmul2_rn(__half22float2(h2[i]), s2);
+        const float2 t = __fadd2_rn(pf[i], m2);
+        tb[2 * i] = __float_as_uint(t.x);
+        tb[2 * i + 1] = __float_as_uint(t.y);
+        r[i] = __fadd2_rn(t, nm2);
+        const float2 d = __fadd2_rn(pf[i], make_float2(-r[i].x, -r[i].y));
+        dmax = fmaxf(dmax, fmaxf(fabsf(d.x), fabsf(d.y)));
+    }
+    if (dmax >= 0.5f - 6.103515625e-05f) {  // rare: some element near a .5 boundary
+        const __half* h = reinterpret_cast<const __half*>(&q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float pe = (e & 1) ? pf[e >> 1].y : pf[e >> 1].x;
+            const float re = (e & 1) ? r[e >> 1].y : r[e >> 1].x;
+            if (fabsf(pe - re) >= 0.5f - 6.103515625e-05f)
+                tb[e] = static_cast<uint32_t>(code_of_slow(__half2float(h[e]), s));
+        }
+    }
+    if (mbyte != 0u) {  // vector holds an outlier column
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if ((mbyte >> e) & 1u) tb[e] = 0u;
+    }
+    const uint32_t a01 = __byte_perm(tb[0], tb[1], 0x0040);
+    const uint32_t a23 = __byte_perm(tb[2], tb[3], 0x0040);
+    const uint32_t a45 = __byte_perm(tb[4], tb[5], 0x0040);
+    const uint32_t a67 = __byte_perm(tb[6], tb[7], 0x0040);
+    return make_uint2(__byte_perm(a01, a23, 0x5410), __byte_perm(a45, a67, 0x5410));
+}
+
 // One block per row; the row stays in registers (VPT 16-byte vectors/thread).
 // amax over keep columns runs on fp16 bit patterns (monotone for |x|) with
 // 2-way SIMD max; codes use the fp32 fast path with exact f64 fallback.
@@ -224,9 +270,14 @@ __global__ void __launch_bounds__(512) quantize_rows_vec_kernel(
         const int64_t v = threadIdx.x + static_cast<int64_t>(j) * blockDim.x;
         if (v < nvec) {
             const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+            if (mb[j] == 0u) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                am2 = __vmaxu2(am2, (w4[i] & 0x7FFF7FFFu) & keep_word(mb[j], i));
+                for (int i = 0; i < 4; ++i) am2 = __vmaxu2(am2, w4[i] & 0x7FFF7FFFu);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    am2 = __vmaxu2(am2, (w4[i] & 0x7FFF7FFFu) & keep_word(mb[j], i));
+            }
         }
     }
     const uint32_t am_bits = block_max_u32(max(am2 & 0xFFFFu, am2 >> 16), red);
@@ -237,18 +288,7 @@ __global__ void __launch_bounds__(512) quantize_rows_vec_kernel(
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
         const int64_t v = threadIdx.x + static_cast<int64_t>(j) * blockDim.x;
-        if (v < nvec) {
-            const __half* h = reinterpret_cast<const __half*>(&q[j]);
-            uint32_t lo = 0, hi = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int c = ((mb[j] >> e) & 1u) ? 0 : code_fast(__half2float(h[e]), s32, s);
-                const uint32_t b = static_cast<uint32_t>(c) & 0xFFu;
-                if (e < 4) lo |= b << (8 * e);
-                else hi |= b << (8 * (e - 4));
-            }
-            *reinterpret_cast<uint2*>(qr + (v << 3)) = make_uint2(lo, hi);
-        }
+        if (v < nvec) *reinterpret_cast<uint2*>(qr + (v << 3)) = quant8(q[j], mb[j], s32, s);
     }
     if (threadIdx.x == 0) row_amax[row] = amax;
     if (xo != nullptr && o_count != nullptr) {
@@ -257,6 +297,93 @@ __global__ void __launch_bounds__(512) quantize_rows_vec_kernel(
     }
     // zero the K..ldq padding so the codes buffer is fully defined
     for (int64_t k = K + threadIdx.x; k < ldq; k += blockDim.x) qr[k] = 0;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Rows staged through shared memory with a 2-deep cp.async ring: while a
+// block quantizes row r (amax pass + code pass, both from smem), the next
+// row's bytes are already in flight, so HBM sees a continuous stream with a
+// small register footprint (high occupancy). Dynamic smem: 2 * K * 2 bytes of
+// row buffers + the outlier mask words.
+__global__ void __launch_bounds__(256) quantize_rows_smem_kernel(
+    const __half* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
+    const uint32_t* __restrict__ col_mask, const int32_t* __restrict__ o_idx,
+    const int32_t* __restrict__ o_count, int8_t* __restrict__ xq, int64_t ldq,
+    float* __restrict__ row_amax, __half* __restrict__ xo, int64_t o_cap) {
+    extern __shared__ __align__(16) uint8_t qsm[];
+    __shared__ uint32_t red[32];
+    const int nv = static_cast<int>(K >> 3);
+    const int tid = threadIdx.x, bd = blockDim.x;
+    uint4* buf0 = reinterpret_cast<uint4*>(qsm);
+    uint4* buf1 = buf0 + nv;
+    uint32_t* smask = reinterpret_cast<uint32_t*>(buf1 + nv);
+    const uint8_t* smask8 = reinterpret_cast<const uint8_t*>(smask);  // one mask byte per vector
+    const int nwords = static_cast<int>((K + 31) >> 5);
+    for (int i = tid; i < nwords; i += bd) smask[i] = col_mask ? col_mask[i] : 0u;
+    const int n_o = (xo != nullptr && o_count != nullptr) ? static_cast<int>(min(static_cast<int64_t>(*o_count), o_cap)) : 0;
+
+    int64_t row = blockIdx.x;
+    if (row < M) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + row * ldx);
+        for (int v = tid; v < nv; v += bd) cp_async16(buf0 + v, src + v);
+    }
+    cp_async_commit();
+    int stage = 0;
+    for (; row < M; row += gridDim.x) {
+        uint4* cur = stage ? buf1 : buf0;
+        uint4* nxt = stage ? buf0 : buf1;
+        const int64_t nrow = row + gridDim.x;
+        if (nrow < M) {
+            const uint4* src = reinterpret_cast<const uint4*>(x + nrow * ldx);
+            for (int v = tid; v < nv; v += bd) cp_async16(nxt + v, src + v);
+        }
+        cp_async_commit();
+        cp_async_wait<1>();  // this row's group has landed
+        __syncthreads();
+        // pass 1: amax over keep columns on fp16 bit patterns
+        uint32_t am2 = 0;
+        for (int v = tid; v < nv; v += bd) {
+            const uint4 q = cur[v];
+            const uint32_t mb = smask8[v];
+            if (mb == 0u) {
+                am2 = __vmaxu2(am2, q.x & 0x7FFF7FFFu);
+                am2 = __vmaxu2(am2, q.y & 0x7FFF7FFFu);
+                am2 = __vmaxu2(am2, q.z & 0x7FFF7FFFu);
+                am2 = __vmaxu2(am2, q.w & 0x7FFF7FFFu);
+            } else {
+                const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) am2 = __vmaxu2(am2, (w4[i] & 0x7FFF7FFFu) & keep_word(mb, i));
+            }
+        }
+        const uint32_t am_bits = block_max_u32(max(am2 & 0xFFFFu, am2 >> 16), red);
+        const float amax = __half2float(__ushort_as_half(static_cast<unsigned short>(am_bits)));
+        const double s = scale_of(amax);
+        const float s32 = static_cast<float>(s);
+        uint2* qr = reinterpret_cast<uint2*>(xq + row * ldq);
+        // pass 2: codes
+#pragma unroll 2
+        for (int v = tid; v < nv; v += bd) qr[v] = quant8(cur[v], smask8[v], s32, s);
+        if (tid == 0) row_amax[row] = amax;
+        const __half* crow = reinterpret_cast<const __half*>(cur);
+        for (int t = tid; t < n_o; t += bd) xo[row * o_cap + t] = crow[o_idx[t]];
+        int8_t* qb = xq + row * ldq;
+        for (int64_t k = K + tid; k < ldq; k += bd) qb[k] = 0;
+        __syncthreads();  // everyone is done with `cur` (and `red`) before it is refilled
+        stage ^= 1;
+    }
+    cp_async_wait<0>();
 }
 
 // Generic path (any K / alignment): two passes over the row from global.
@@ -380,6 +507,24 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
                                  __half* xo, int64_t o_cap, cudaStream_t st) {
     if (M == 0) return cudaSuccess;
     // register-resident rows up to K = 16 vectors x 8 x 512 threads = 65536
+    const size_t smem_bytes = static_cast<size_t>(K) * 4 + static_cast<size_t>((K + 31) / 32) * 4;
+    const bool aligned = (K % 8 == 0) && (ldx % 8 == 0) && (ldq % 8 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(xq) & 7u) == 0);
+    if (aligned && smem_bytes <= 200 * 1024) {
+        static size_t configured = 0;
+        if (smem_bytes > 48 * 1024 && smem_bytes > configured) {
+            cudaFuncSetAttribute(quantize_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024);
+            configured = 200 * 1024;
+        }
+        const int per_sm = static_cast<int>(imin64(8, (220 * 1024) / static_cast<int64_t>(smem_bytes + 1024)));
+        const int64_t grid = imin64(M, static_cast<int64_t>(num_sms()) * (per_sm > 0 ? per_sm : 1));
+        quantize_rows_smem_kernel<<<static_cast<unsigned>(grid), 256, smem_bytes, st>>>(
+            x, M, K, ldx, mask, o_idx, o_count, xq, ldq, amax, xo, o_cap);
+        count_launch();
+        return cudaGetLastError();
+    }
     const bool vec = (K % 8 == 0) && (K <= 65536) && (ldx % 8 == 0) && (ldq % 8 == 0) &&
                      ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
                      ((reinterpret_cast<uintptr_t>(xq) & 7u) == 0);

@@ -43,9 +43,12 @@ __device__ __forceinline__ double scale_of(float amax) {
 // reference's floor(|p64| + 0.5) with sign (quantize.py:26-29); otherwise
 // (~1e-4 of elements) the exact f64 formulation decides.
 __device__ __forceinline__ int code_fast(float x, float s32, double s) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: t - kMagic = rint(pf)
     const float pf = x * s32;
-    const float r = rintf(pf);
-    if (fabsf(pf - r) < 0.5f - 6.103515625e-05f) return static_cast<int>(r);
+    const float t = pf + kMagic;
+    const float r = t - kMagic;
+    if (fabsf(pf - r) < 0.5f - 6.103515625e-05f)
+        return static_cast<int>(__float_as_int(t) - 0x4B400000);
     return static_cast<int>(code_of(x, s));
 }
 
