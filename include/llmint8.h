@@ -50,6 +50,10 @@ int i8mm_version(void);
 const char* i8mm_status_string(int status);
 /* Number of kernels this library launched since load (for bench accounting). */
 uint64_t i8mm_launch_count(void);
+/* Pin a GEMM kernel variant (A/B measurements, tests): cg_override 1 = the
+ * 1-CTA kernel; mc_override 2 = 4-CTA clusters multicasting WqT between two
+ * CTA pairs (M >= 2048); 0 = defaults (CTA pairs, no multicast). */
+void i8mm_debug_set_gemm_variant(int cg_override, int mc_override);
 
 /* K1. Outlier-column scan.  Replaces extract_outlier_columns' mask
  * (gemm.py:208-210): col_mask bit k is set iff some |X[i,k]| >= (float)alpha.

@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "i8mm_version",
     "i8mm_status_string",
     "i8mm_launch_count",
+    "i8mm_debug_set_gemm_variant",
     "i8mm_outlier_scan",
     "i8mm_outlier_compact",
     "i8mm_quantize_rows",
@@ -69,6 +70,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_version": ([], I32),
         "i8mm_status_string": ([I32], ctypes.c_char_p),
         "i8mm_launch_count": ([], ctypes.c_uint64),
+        "i8mm_debug_set_gemm_variant": ([I32, I32], None),
         "i8mm_outlier_scan": ([P, I64, I64, I64, F32, P, P, P], I32),
         "i8mm_outlier_compact": ([P, I64, P, P, P], I32),
         "i8mm_quantize_rows": ([P, I64, I64, I64, P, P, P, P, I64, P, P, I64, P], I32),

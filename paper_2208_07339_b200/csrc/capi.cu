@@ -81,6 +81,10 @@ const char* i8mm_status_string(int s) {
 
 uint64_t i8mm_launch_count(void) { return g_launches.load(); }
 
+void i8mm_debug_set_gemm_variant(int cg_override, int mc_override) {
+    set_gemm_variant(cg_override, mc_override);
+}
+
 int i8mm_outlier_scan(const void* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                       uint32_t* col_mask, int32_t* nonfinite, void* stream) {
     if (int s = check_device()) return s;

@@ -41,14 +41,19 @@ constexpr int UMMA_K = 32;
 constexpr int MAX_STAGES = 6;
 constexpr int A_BYTES = BM * BK;
 
-template <int CG>
+// CG = CTAs per MMA (cta_group), MC = CTA pairs per cluster sharing each WqT
+// tile through TMA multicast (cluster = CG * MC CTAs along M).
+template <int CG, int MC = 1>
 struct Cfg {
     static constexpr int STAGES = CG == 1 ? 4 : 6;
-    static constexpr int B_ROWS = BN / CG;  // WqT rows loaded by each CTA
+    static constexpr int B_ROWS = BN / CG;        // WqT rows resident in each CTA
+    static constexpr int B_LOAD_ROWS = B_ROWS / MC;  // rows each CTA fetches (then multicasts)
     static constexpr int B_BYTES = B_ROWS * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr size_t SMEM_OPERANDS = static_cast<size_t>(STAGES) * STAGE_BYTES;
-    static constexpr int GROUP_M = CG == 1 ? 16 : 8;
+    static constexpr int GROUP_M = CG == 1 ? 16 : 8 / MC;
+    static constexpr int CLUSTER = CG * MC;
+    static constexpr int TILE_M = BM * CG * MC;    // output rows per cluster tile
 };
 constexpr int WO_CAP = 16;  // outlier rows of W staged in smem per tile
 constexpr int EPI_WARP0 = 4;
@@ -68,9 +73,9 @@ struct __align__(8) Barriers {
 
 constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(float);
 constexpr size_t SMEM_COLS = static_cast<size_t>(BN) * sizeof(double);
-template <int CG>
+template <int CG, int MC>
 constexpr size_t smem_total() {
-    return 1024 /*align slack*/ + Cfg<CG>::SMEM_OPERANDS + SMEM_WO + SMEM_COLS + sizeof(Barriers) + 64;
+    return 1024 /*align slack*/ + Cfg<CG, MC>::SMEM_OPERANDS + SMEM_WO + SMEM_COLS + sizeof(Barriers) + 64;
 }
 
 struct Params {
@@ -129,11 +134,11 @@ __device__ __forceinline__ void tile_coords(const Params& p, const TileSpace& ts
 
 __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0f : a; }
 
-template <int EPI, int CG>
+template <int EPI, int CG, int MC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const Params p) {
-    using C = Cfg<CG>;
+    using C = Cfg<CG, MC>;
     constexpr int STAGES = C::STAGES;
     constexpr int B_BYTES = C::B_BYTES;
     constexpr size_t SMEM_OPERANDS = C::SMEM_OPERANDS;
@@ -150,17 +155,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const TileSpace ts = tile_space(p);
-    const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;  // rank within the CTA pair
+    const uint32_t cl_rank = C::CLUSTER > 1 ? cluster_ctarank() : 0u;
+    const uint32_t crank = cl_rank % CG;            // rank within the CTA pair
+    const uint32_t pair = cl_rank / CG;             // which pair of the cluster
+    const uint32_t leader_rank = pair * CG;         // cluster rank of this pair's MMA leader
     const bool leader = crank == 0;
-    const int cluster_id = static_cast<int>(blockIdx.x) / CG;
-    const int n_clusters = static_cast<int>(gridDim.x) / CG;
+    const int cluster_id = static_cast<int>(blockIdx.x) / C::CLUSTER;
+    const int n_clusters = static_cast<int>(gridDim.x) / C::CLUSTER;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_a);
         tma_prefetch_desc(&tmap_b);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&bars->full[s], 1);
-            mbar_init(&bars->empty[s], 1);
+            mbar_init(&bars->empty[s], MC);  // freed by every pair's MMA (multicast B)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&bars->tmem_full[a], 1);
@@ -175,7 +183,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised + TMEM allocated
+    if constexpr (C::CLUSTER > 1) cluster_sync_all();  // peer barriers initialised + TMEM allocated
     tc_fence_after();
     const uint32_t tmem_base = bars->tmem_slot;
 
@@ -188,17 +196,27 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int t = cluster_id; t < ts.total; t += n_clusters) {
                 int m_blk, n_blk;
                 tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
-                const int a_row = m_blk * (BM * CG) + static_cast<int>(crank) * BM;
-                const int b_row = n_blk * BN + static_cast<int>(crank) * C::B_ROWS;
+                const int a_row = m_blk * C::TILE_M + static_cast<int>(pair) * (BM * CG) +
+                                  static_cast<int>(crank) * BM;
+                const int b_row = n_blk * BN + static_cast<int>(crank) * C::B_ROWS +
+                                  static_cast<int>(pair) * C::B_LOAD_ROWS;
+                // this CTA's B piece is multicast to the CTAs of equal crank in every pair
+                uint16_t b_mask = 0;
+#pragma unroll
+                for (int q = 0; q < MC; ++q) b_mask |= static_cast<uint16_t>(1u << (q * CG + crank));
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1u);
                     if constexpr (CG == 2) {
-                        // the leader's full barrier counts both CTAs' bytes
+                        // the pair leader's full barrier counts every byte landing in the pair
                         if (leader) mbar_arrive_expect_tx(&bars->full[stage], CG * C::STAGE_BYTES);
                         tma_load_2d_pair(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES,
                                          kb * BK, a_row, pol);
-                        tma_load_2d_pair(&tmap_b, &bars->full[stage], smem_b + stage * B_BYTES,
-                                         kb * BK, b_row, pol);
+                        uint8_t* bdst = smem_b + stage * B_BYTES + pair * (C::B_LOAD_ROWS * BK);
+                        if constexpr (MC > 1)
+                            tma_load_2d_pair_mc(&tmap_b, &bars->full[stage], bdst, kb * BK, b_row,
+                                                b_mask, pol);
+                        else
+                            tma_load_2d_pair(&tmap_b, &bars->full[stage], bdst, kb * BK, b_row, pol);
                     } else {
                         mbar_arrive_expect_tx(&bars->full[stage], C::STAGE_BYTES);
                         tma_load_2d(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES, kb * BK,
@@ -239,7 +257,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                         else mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
                     // frees the smem slot (in both CTAs of a pair) when the MMAs finish
-                    if constexpr (CG == 2) mma_commit_pair(&bars->empty[stage], 0x3);
+                    // (with MC > 1 the slot also holds B pieces written by the other
+                    // pairs' producers, so every CTA of the cluster is told)
+                    if constexpr (CG == 2)
+                        mma_commit_pair(&bars->empty[stage],
+                                        static_cast<uint16_t>((1u << C::CLUSTER) - 1u));
                     else mma_commit(&bars->empty[stage]);
                 }
                 __syncwarp();
@@ -249,7 +271,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
             if (lane == 0) {  // accumulator ready (both CTAs' epilogues)
-                if constexpr (CG == 2) mma_commit_pair(&bars->tmem_full[acc], 0x3);
+                if constexpr (CG == 2)
+                    mma_commit_pair(&bars->tmem_full[acc], static_cast<uint16_t>(0x3u << leader_rank));
                 else mma_commit(&bars->tmem_full[acc]);
             }
             __syncwarp();
@@ -270,7 +293,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            const int64_t row = static_cast<int64_t>(m_blk) * (BM * CG) + crank * BM + quad * 32 + lane;
+            const int64_t row = static_cast<int64_t>(m_blk) * C::TILE_M + pair * (BM * CG) +
+                                crank * BM + quad * 32 + lane;
             const int64_t col0 = static_cast<int64_t>(n_blk) * BN;
             const bool row_ok = row < p.M;
             const bool mapped = p.col_map != nullptr;
@@ -472,14 +496,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (CG == 2) mbar_arrive_remote(&bars->tmem_empty[acc], 0);
+                if constexpr (CG == 2) mbar_arrive_remote(&bars->tmem_empty[acc], leader_rank);
                 else mbar_arrive(&bars->tmem_empty[acc]);
             }
         }
     }
 
     __syncthreads();
-    if constexpr (CG == 2) cluster_sync_all();  // both CTAs done with TMEM and barriers
+    if constexpr (C::CLUSTER > 1) cluster_sync_all();  // all CTAs done with TMEM and barriers
     if (warp == 2) {
         tc_fence_after();
         if constexpr (CG == 2) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
@@ -523,31 +547,44 @@ static bool make_tmap_i8(CUtensorMap* map, const int8_t* base, int64_t rows, int
     return r == CUDA_SUCCESS;
 }
 
-template <int EPI, int CG>
+template <int EPI, int CG, int MC>
 static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                              int grid, cudaStream_t st) {
+                              int64_t max_tiles, cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
-    constexpr size_t smem = smem_total<CG>();
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(gemm_i8_kernel<EPI, CG>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem));
-    });
-    if (attr_err != cudaSuccess) return attr_err;
+    static int max_clusters = 0;
+    constexpr size_t smem = smem_total<CG, MC>();
+    constexpr int CL = CG * MC;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG>, ta, tb, p);
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(gemm_i8_kernel<EPI, CG, MC>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem));
+        // how many clusters of this shape the GPC layout can co-schedule
+        cudaLaunchConfig_t q = cfg;
+        q.gridDim = dim3(static_cast<unsigned>(num_sms() / CL * CL));
+        int n = 0;
+        if (attr_err == cudaSuccess &&
+            cudaOccupancyMaxActiveClusters(&n, gemm_i8_kernel<EPI, CG, MC>, &q) == cudaSuccess && n > 0)
+            max_clusters = n;
+        else
+            max_clusters = num_sms() / CL;
+        cudaGetLastError();
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    const int64_t clusters = max_tiles < max_clusters ? max_tiles : max_clusters;
+    cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, p);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -555,20 +592,33 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
 
 template <int EPI>
 static cudaError_t launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                             int grid, int cg, cudaStream_t st) {
-    return cg == 2 ? launch_epi<EPI, 2>(ta, tb, p, grid, st) : launch_epi<EPI, 1>(ta, tb, p, grid, st);
+                             int64_t max_tiles, int cg, int mc, cudaStream_t st) {
+    if (cg == 2 && mc == 2) return launch_epi<EPI, 2, 2>(ta, tb, p, max_tiles, st);
+    if (cg == 2) return launch_epi<EPI, 2, 1>(ta, tb, p, max_tiles, st);
+    return launch_epi<EPI, 1, 1>(ta, tb, p, max_tiles, st);
 }
 
 }  // namespace gemm
 
-// I8MM_FORCE_CG1=1 pins the 1-CTA kernel (tests cover both variants)
-static bool force_cg1() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("I8MM_FORCE_CG1");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
+// Kernel-variant overrides for tests / A-B measurements:
+//   I8MM_FORCE_CG1=1 pins the 1-CTA kernel; I8MM_GEMM_MC=2 enables the
+//   B-multicast cluster of two CTA pairs (M >= 2048).
+static int env_int(const char* name) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : 0;
+}
+static int g_cg_override = -1, g_mc_override = -1;
+static int gemm_cg_override() {
+    if (g_cg_override < 0) g_cg_override = env_int("I8MM_FORCE_CG1") == 1 ? 1 : 0;
+    return g_cg_override;
+}
+static int gemm_mc_override() {
+    if (g_mc_override < 0) g_mc_override = env_int("I8MM_GEMM_MC");
+    return g_mc_override;
+}
+void set_gemm_variant(int cg, int mc) {
+    g_cg_override = cg;
+    g_mc_override = mc;
 }
 
 cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
@@ -577,19 +627,23 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     if ((a.lda % 16) || (a.ldb % 16) || (reinterpret_cast<uintptr_t>(a.a) & 15) ||
         (reinterpret_cast<uintptr_t>(a.b) & 15))
         return cudaErrorInvalidValue;
-    // CTA pairs (cta_group::2, 256-row tiles) unless M fits one 128-row tile
-    const int cg = (a.M > BM && !force_cg1()) ? 2 : 1;
+    // CTA pairs (cta_group::2, 256-row tiles) unless M fits one 128-row tile.
+    // The 4-CTA cluster that multicasts WqT between two pairs (MC=2) halves the
+    // B-operand L2 reads but only 132 SMs can host 4-CTA clusters; measured
+    // (profiles/) it does not beat plain pairs, so it is opt-in (I8MM_GEMM_MC=2).
+    const int cg = (a.M > BM && gemm_cg_override() != 1) ? 2 : 1;
+    const int mc = (cg == 2 && a.M >= 2048 && gemm_mc_override() == 2) ? 2 : 1;
     CUtensorMap ta, tb;
     const int64_t kdim = a.K > 0 ? a.K : 16;
     if (!make_tmap_i8(&ta, a.a, a.M, kdim, a.lda, BM)) return cudaErrorInvalidValue;
-    if (!make_tmap_i8(&tb, a.b, a.N, kdim, a.ldb, BN / cg)) return cudaErrorInvalidValue;
+    if (!make_tmap_i8(&tb, a.b, a.N, kdim, a.ldb, BN / cg / mc)) return cudaErrorInvalidValue;
     Params p{};
     p.M = a.M;
     p.N = a.N;
     p.K = a.K;
     p.num_kb = static_cast<int>((a.K + BK - 1) / BK);
     if (p.num_kb == 0) p.num_kb = 1;  // K == 0: one zero-filled block -> C = 0
-    p.m_tiles = static_cast<int>((a.M + BM * cg - 1) / (BM * cg));
+    p.m_tiles = static_cast<int>((a.M + BM * cg * mc - 1) / (BM * cg * mc));
     const int64_t max_tiles = static_cast<int64_t>(p.m_tiles) * ((a.N + BN - 1) / BN);
     p.y = a.y;
     p.ldy = a.ldy;
@@ -610,13 +664,11 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     p.n_count = a.n_count;
     const int elt = (epi == EPI_F16) ? 2 : 4;
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
-    const int64_t clusters = num_sms() / cg;
-    const int grid = cg * static_cast<int>(max_tiles < clusters ? max_tiles : clusters);
     switch (epi) {
-        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, p, grid, cg, st);
-        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, p, grid, cg, st);
-        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, p, grid, cg, st);
-        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, p, grid, cg, st);
+        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, p, max_tiles, cg, mc, st);
+        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, p, max_tiles, cg, mc, st);
+        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, p, max_tiles, cg, mc, st);
+        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, p, max_tiles, cg, mc, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -76,5 +76,6 @@ struct GemmArgs {
 };
 
 cudaError_t launch_gemm_sm100(const GemmArgs& args, int epi, cudaStream_t st);
+void set_gemm_variant(int cg_override, int mc_override);
 
 }  // namespace i8mm

@@ -166,6 +166,19 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_
         "l"(policy)
         : "memory");
 }
+// Same, multicast: the tile lands at the same smem offset in every CTA of
+// `mask`; each destination pair's leader barrier counts its bytes.
+__device__ __forceinline__ void tma_load_2d_pair_mc(const CUtensorMap* map, uint64_t* bar,
+                                                    void* dst, int32_t c0, int32_t c1,
+                                                    uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(
+            smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar) & 0xFEFFFFFFu), "h"(mask),
+        "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot_smem) {  // whole warp, both CTAs
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

@@ -169,6 +169,7 @@ def test_error_contract(p):
 
 
 @pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 300, 129), (130, 257, 4112), (257, 513, 1000),
+                                 (2048, 384, 1024), (3000, 520, 528),
                                  (384, 768, 2048), (1, 4096, 4096), (300, 40, 16)])
 def test_int8_gemm_matches_oracle(p, oracle_mod, mnk):
     m, n, k = mnk
@@ -349,7 +350,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, {root!r})
 import paper_2208_07339_b200 as p
 from oracle import oracle as orc
-for (m, n, k) in [(300, 257, 1000), (384, 768, 2048), (129, 40, 16)]:
+for (m, n, k) in [(300, 257, 1000), (384, 768, 2048), (129, 40, 16), (2100, 300, 640)]:
     rng = np.random.Generator(np.random.PCG64(m + n + k))
     a = rng.integers(-127, 128, size=(m, k), dtype=np.int8)
     b = rng.integers(-127, 128, size=(k, n), dtype=np.int8)
@@ -360,19 +361,40 @@ ref = orc.c_llm_int8_matmul(x, w, 6.0)
 assert np.array_equal(p.llm_int8_matmul(x, w, 6.0, exact=True).output.cpu().numpy(), ref.output)
 lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
 assert np.array_equal(lin.matmul(torch.from_numpy(x.astype(np.float16)).cuda(), exact=True).cpu().numpy(), ref.output)
-print("CG1 OK")
+print("VARIANT OK")
 """
 
 
-def test_one_cta_kernel_variant(p):
-    """The 1-CTA (cta_group::1) GEMM variant, pinned via I8MM_FORCE_CG1=1."""
+@pytest.mark.parametrize("variant", [{"I8MM_FORCE_CG1": "1"}, {"I8MM_GEMM_MC": "2"}],
+                         ids=["cta_group1", "pair_multicast_cluster4"])
+def test_gemm_kernel_variants(p, variant):
+    """The 1-CTA (cta_group::1) GEMM and the 4-CTA-cluster GEMM multicasting
+    WqT between two CTA pairs, pinned via environment overrides (the default
+    CTA-pair path is covered above)."""
     import os
     import subprocess
     import sys
     from pathlib import Path
 
     root = str(Path(__file__).resolve().parent.parent)
-    env = dict(os.environ, I8MM_FORCE_CG1="1")
+    env = dict(os.environ, **variant)
     r = subprocess.run([sys.executable, "-c", _CG1_SCRIPT.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "CG1 OK" in r.stdout, r.stdout + r.stderr
+    assert r.returncode == 0 and "VARIANT OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("shape", [(4096, 1024, 768), (2600, 1040, 1000)])
+def test_large_m_multicast_path_vs_oracle(p, oracle_mod, shape):
+    """Large M through the CTA-pair GEMM (many pair tiles, ragged edges)."""
+    m, k, n = shape
+    x, w = oracle_mod.planted_pair(m, k, n, 6, 20.0, 5)
+    x = x.astype(np.float16).astype(np.float32)
+    w = w.astype(np.float16).astype(np.float32)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    r = p.llm_int8_matmul(x, w, 6.0, exact=True)
+    assert np.array_equal(_np(r.output), ref.output)
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    assert np.array_equal(_np(lin.matmul(x16, exact=True)), ref.output)
+    y16 = _np(lin(x16)).astype(np.float64)
+    assert (np.abs(y16 - ref.output) <= _golden.fp16_tolerance(ref.output)).all()
