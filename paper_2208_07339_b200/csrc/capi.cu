@@ -262,7 +262,7 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
     w.xo = reinterpret_cast<__half*>(take(sizeof(__half) * static_cast<size_t>(M * kOCap)));
     w.wo = reinterpret_cast<__half*>(take(sizeof(__half) * static_cast<size_t>(kOCap * round_up(N, 8))));
     if (linear) {
-        w.p_count = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 4));
+        w.p_count = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (4 + (N + 31) / 32)));
         w.p_idx = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
         w.p_amax = reinterpret_cast<float*>(take(sizeof(float) * N));
         w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
@@ -461,13 +461,14 @@ int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64
     g.wo = ws.wo;
     g.ldwo = round_up(N, 8);
     g.wo_cap = ws.o_cap;
+    // patched columns (their amax over keep rows differs from the cached one)
+    // run as extra tiles of the same launch
+    g.b_patch = ws.wq_p;
+    g.patch_count = ws.p_count;
+    g.patch_idx = ws.p_idx;
+    g.patch_amax = ws.p_amax;
+    g.patch_mask = reinterpret_cast<const uint32_t*>(ws.p_count) + 4;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (launch_gemm_sm100(g, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
-    // patched columns: their amax over keep rows differs from the cached one
-    g.b = ws.wq_p;
-    g.col_amax = ws.p_amax;
-    g.col_map = ws.p_idx;
-    g.n_count = ws.p_count;
     if (launch_gemm_sm100(g, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
     return I8MM_OK;
 }

@@ -97,31 +97,43 @@ struct Params {
     const __half* wo;
     int64_t ldwo;
     int64_t wo_cap;
-    const int32_t* col_map;
-    const int32_t* n_count;
+    // weight-stationary patches: extra N-tiles appended after the main tiles,
+    // B from the patch codes (tmap_p), output column j -> Y column patch_idx[j],
+    // column amax patch_amax[j], live count *patch_count (read on the device)
+    const int32_t* patch_count;
+    const int32_t* patch_idx;
+    const float* patch_amax;
+    const uint32_t* patch_mask;  // bit j: Y column j is written by a patch tile instead
     int vec_store;  // 1: y rows 16-byte aligned and row pitch a multiple of 16 B
 };
 
 struct TileSpace {
-    int n_live, n_tiles, total;
+    int n_tiles, main_total, patch_n, total;
 };
 
 __device__ __forceinline__ TileSpace tile_space(const Params& p) {
     TileSpace ts;
-    int64_t n = p.N;
-    if (p.n_count != nullptr) {
-        const int64_t c = *p.n_count;
-        n = c < n ? c : n;
+    ts.n_tiles = static_cast<int>((p.N + BN - 1) / BN);
+    ts.main_total = p.m_tiles * ts.n_tiles;
+    int64_t pn = 0;
+    if (p.patch_count != nullptr) {
+        pn = *p.patch_count;
+        pn = pn < p.N ? pn : p.N;
     }
-    ts.n_live = static_cast<int>(n);
-    ts.n_tiles = static_cast<int>((n + BN - 1) / BN);
-    ts.total = p.m_tiles * ts.n_tiles;
+    ts.patch_n = static_cast<int>(pn);
+    ts.total = ts.main_total + p.m_tiles * static_cast<int>((pn + BN - 1) / BN);
     return ts;
 }
 
 template <int GROUP_M>
-__device__ __forceinline__ void tile_coords(const Params& p, const TileSpace& ts, int t,
+__device__ __forceinline__ bool tile_coords(const Params& p, const TileSpace& ts, int t,
                                             int& m_blk, int& n_blk) {
+    if (t >= ts.main_total) {  // patch tiles (weight-stationary fixup), m fastest
+        const int local = t - ts.main_total;
+        m_blk = local % p.m_tiles;
+        n_blk = local / p.m_tiles;
+        return true;
+    }
     // grouped raster: GROUP_M m-tiles share each B panel while it is hot in L2
     const int per_group = GROUP_M * ts.n_tiles;
     const int g = t / per_group;
@@ -130,6 +142,7 @@ __device__ __forceinline__ void tile_coords(const Params& p, const TileSpace& ts
     const int local = t - g * per_group;
     m_blk = first_m + local % gm;
     n_blk = local / gm;
+    return false;
 }
 
 __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0f : a; }
@@ -137,7 +150,8 @@ __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0
 template <int EPI, int CG, int MC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                   const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+                   const __grid_constant__ CUtensorMap tmap_b,
+                   const __grid_constant__ CUtensorMap tmap_p, const Params p) {
     using C = Cfg<CG, MC>;
     constexpr int STAGES = C::STAGES;
     constexpr int B_BYTES = C::B_BYTES;
@@ -166,6 +180,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_a);
         tma_prefetch_desc(&tmap_b);
+        if (p.patch_count != nullptr) tma_prefetch_desc(&tmap_p);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], MC);  // freed by every pair's MMA (multicast B)
@@ -195,7 +210,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t phase = 0;
             for (int t = cluster_id; t < ts.total; t += n_clusters) {
                 int m_blk, n_blk;
-                tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
+                const bool is_patch = tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
+                const CUtensorMap* map_b = is_patch ? &tmap_p : &tmap_b;
                 const int a_row = m_blk * C::TILE_M + static_cast<int>(pair) * (BM * CG) +
                                   static_cast<int>(crank) * BM;
                 const int b_row = n_blk * BN + static_cast<int>(crank) * C::B_ROWS +
@@ -213,15 +229,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                                          kb * BK, a_row, pol);
                         uint8_t* bdst = smem_b + stage * B_BYTES + pair * (C::B_LOAD_ROWS * BK);
                         if constexpr (MC > 1)
-                            tma_load_2d_pair_mc(&tmap_b, &bars->full[stage], bdst, kb * BK, b_row,
+                            tma_load_2d_pair_mc(map_b, &bars->full[stage], bdst, kb * BK, b_row,
                                                 b_mask, pol);
                         else
-                            tma_load_2d_pair(&tmap_b, &bars->full[stage], bdst, kb * BK, b_row, pol);
+                            tma_load_2d_pair(map_b, &bars->full[stage], bdst, kb * BK, b_row, pol);
                     } else {
                         mbar_arrive_expect_tx(&bars->full[stage], C::STAGE_BYTES);
                         tma_load_2d(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES, kb * BK,
                                     a_row, pol);
-                        tma_load_2d(&tmap_b, &bars->full[stage], smem_b + stage * B_BYTES, kb * BK,
+                        tma_load_2d(map_b, &bars->full[stage], smem_b + stage * B_BYTES, kb * BK,
                                     b_row, pol);
                     }
                     if (++stage == STAGES) {
@@ -290,14 +306,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         int it = 0;
         for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
             int m_blk, n_blk;
-            tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
+            const bool is_patch = tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            const int64_t n_live = is_patch ? ts.patch_n : p.N;
+            const float* camax = is_patch ? p.patch_amax : p.col_amax;
+            const int32_t* cmap = p.patch_idx;
             const int64_t row = static_cast<int64_t>(m_blk) * C::TILE_M + pair * (BM * CG) +
                                 crank * BM + quad * 32 + lane;
             const int64_t col0 = static_cast<int64_t>(n_blk) * BN;
             const bool row_ok = row < p.M;
-            const bool mapped = p.col_map != nullptr;
+            const bool mapped = is_patch;
 
             float xo_r[WO_CAP];
             float rowf = 0.0f;
@@ -307,14 +326,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 named_bar_sync(1, EPI_THREADS);  // previous tile's readers are done
                 for (int j = et; j < BN; j += EPI_THREADS) {
                     const int64_t c = col0 + j;
-                    const float aw = c < ts.n_live ? amax_or_127(p.col_amax[c]) : 127.0f;
+                    const float aw = c < n_live ? amax_or_127(camax[c]) : 127.0f;
                     if constexpr (EPI == EPI_F32_EXACT)
                         smem_col[j] = 127.0 / static_cast<double>(aw);
                     else
                         reinterpret_cast<float*>(smem_col)[j] = aw * (1.0f / 16129.0f);
                 }
                 if (stage_wo) {
-                    if (wo_fast && !mapped && col0 + BN <= ts.n_live && (p.ldwo % 8) == 0) {
+                    if (wo_fast && !mapped && col0 + BN <= n_live && (p.ldwo % 8) == 0) {
                         // 16-byte vector loads of the compact outlier rows
                         for (int i = et; i < n_out * (BN / 8); i += EPI_THREADS) {
                             const int o = i / (BN / 8), v = i % (BN / 8);
@@ -332,8 +351,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                             const int o = i / BN, j = i % BN;
                             const int64_t c = col0 + j;
                             float v = 0.0f;
-                            if (c < ts.n_live) {
-                                const int64_t gc = mapped ? p.col_map[c] : c;
+                            if (c < n_live) {
+                                const int64_t gc = mapped ? cmap[c] : c;
                                 v = wo_fast ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + gc])
                                             : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + gc]);
                             }
@@ -368,8 +387,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tmem_ld_32x32b_x32(t_row + ch * 32, r);
                 tmem_ld_wait();
                 const int64_t cbase = col0 + ch * 32;
-                if (!row_ok || cbase >= ts.n_live) continue;
-                const bool full_chunk = !mapped && p.vec_store && cbase + 32 <= ts.n_live;
+                if (!row_ok || cbase >= n_live) continue;
+                // columns owned by a patch tile are skipped by the main tile (same launch)
+                const uint32_t pm = (!mapped && p.patch_mask != nullptr) ? p.patch_mask[cbase >> 5] : 0u;
+                const bool full_chunk = !mapped && pm == 0u && p.vec_store && cbase + 32 <= n_live;
                 if constexpr (EPI == EPI_I32) {
                     int32_t* yr = reinterpret_cast<int32_t*>(p.y) + row * p.ldy;
                     if (full_chunk) {
@@ -380,7 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     } else {
                         for (int j = 0; j < 32; ++j) {
                             const int64_t c = cbase + j;
-                            if (c < ts.n_live) yr[mapped ? p.col_map[c] : c] = static_cast<int32_t>(r[j]);
+                            if (c < n_live && !((pm >> j) & 1u)) yr[mapped ? cmap[c] : c] = static_cast<int32_t>(r[j]);
                         }
                     }
                 } else {
@@ -397,8 +418,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (n_out > 0) {
                             for (int j = 0; j < 32; ++j) {
                                 const int64_t c = cbase + j;
-                                if (c >= ts.n_live) break;
-                                const int64_t gc = mapped ? p.col_map[c] : c;
+                                if (c >= n_live) break;
+                                const int64_t gc = mapped ? cmap[c] : c;
                                 double hacc = 0.0;
                                 for (int o = 0; o < n_out; ++o) {
                                     const int64_t k = p.o_idx[o];
@@ -448,8 +469,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                                     for (int j = 0; j < 32; ++j) {
                                         const int64_t c = cbase + j;
                                         float wv = 0.0f;
-                                        if (c < ts.n_live)
-                                            wv = __half2float(p.w[k * p.ldw + (mapped ? p.col_map[c] : c)]);
+                                        if (c < n_live)
+                                            wv = __half2float(p.w[k * p.ldw + (mapped ? cmap[c] : c)]);
                                         v[j] = fmaf(xv, wv, v[j]);
                                     }
                                 }
@@ -473,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         } else {
                             for (int j = 0; j < 32; ++j) {
                                 const int64_t c = cbase + j;
-                                if (c < ts.n_live) yr[mapped ? p.col_map[c] : c] = __float2half_rn(v[j]);
+                                if (c < n_live && !((pm >> j) & 1u)) yr[mapped ? cmap[c] : c] = __float2half_rn(v[j]);
                             }
                         }
                     } else {
@@ -486,7 +507,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         } else {
                             for (int j = 0; j < 32; ++j) {
                                 const int64_t c = cbase + j;
-                                if (c < ts.n_live) yr[mapped ? p.col_map[c] : c] = v[j];
+                                if (c < n_live && !((pm >> j) & 1u)) yr[mapped ? cmap[c] : c] = v[j];
                             }
                         }
                     }
@@ -548,8 +569,8 @@ static bool make_tmap_i8(CUtensorMap* map, const int8_t* base, int64_t rows, int
 }
 
 template <int EPI, int CG, int MC>
-static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                              int64_t max_tiles, cudaStream_t st) {
+static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tp,
+                              const Params& p, int64_t max_tiles, cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
@@ -584,18 +605,18 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
     if (attr_err != cudaSuccess) return attr_err;
     const int64_t clusters = max_tiles < max_clusters ? max_tiles : max_clusters;
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, tp, p);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 template <int EPI>
-static cudaError_t launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                             int64_t max_tiles, int cg, int mc, cudaStream_t st) {
-    if (cg == 2 && mc == 2) return launch_epi<EPI, 2, 2>(ta, tb, p, max_tiles, st);
-    if (cg == 2) return launch_epi<EPI, 2, 1>(ta, tb, p, max_tiles, st);
-    return launch_epi<EPI, 1, 1>(ta, tb, p, max_tiles, st);
+static cudaError_t launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tp,
+                             const Params& p, int64_t max_tiles, int cg, int mc, cudaStream_t st) {
+    if (cg == 2 && mc == 2) return launch_epi<EPI, 2, 2>(ta, tb, tp, p, max_tiles, st);
+    if (cg == 2) return launch_epi<EPI, 2, 1>(ta, tb, tp, p, max_tiles, st);
+    return launch_epi<EPI, 1, 1>(ta, tb, tp, p, max_tiles, st);
 }
 
 }  // namespace gemm
@@ -637,6 +658,10 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     const int64_t kdim = a.K > 0 ? a.K : 16;
     if (!make_tmap_i8(&ta, a.a, a.M, kdim, a.lda, BM)) return cudaErrorInvalidValue;
     if (!make_tmap_i8(&tb, a.b, a.N, kdim, a.ldb, BN / cg / mc)) return cudaErrorInvalidValue;
+    CUtensorMap tp = tb;
+    if (a.patch_count != nullptr &&
+        !make_tmap_i8(&tp, a.b_patch, a.N, kdim, a.ldb, BN / cg / mc))
+        return cudaErrorInvalidValue;
     Params p{};
     p.M = a.M;
     p.N = a.N;
@@ -644,7 +669,10 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     p.num_kb = static_cast<int>((a.K + BK - 1) / BK);
     if (p.num_kb == 0) p.num_kb = 1;  // K == 0: one zero-filled block -> C = 0
     p.m_tiles = static_cast<int>((a.M + BM * cg * mc - 1) / (BM * cg * mc));
-    const int64_t max_tiles = static_cast<int64_t>(p.m_tiles) * ((a.N + BN - 1) / BN);
+    // upper bound on tiles (patches at most double the N-tiles); the kernel
+    // computes the live count on the device
+    const int64_t max_tiles = static_cast<int64_t>(p.m_tiles) * ((a.N + BN - 1) / BN) *
+                              (a.patch_count != nullptr ? 2 : 1);
     p.y = a.y;
     p.ldy = a.ldy;
     p.row_amax = a.row_amax;
@@ -660,15 +688,17 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     p.wo = a.wo;
     p.ldwo = a.ldwo;
     p.wo_cap = a.wo ? a.wo_cap : 0;
-    p.col_map = a.col_map;
-    p.n_count = a.n_count;
+    p.patch_count = a.patch_count;
+    p.patch_idx = a.patch_idx;
+    p.patch_amax = a.patch_amax;
+    p.patch_mask = a.patch_mask;
     const int elt = (epi == EPI_F16) ? 2 : 4;
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
     switch (epi) {
-        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, p, max_tiles, cg, mc, st);
-        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, p, max_tiles, cg, mc, st);
-        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, p, max_tiles, cg, mc, st);
-        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, p, max_tiles, cg, mc, st);
+        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, tp, p, max_tiles, cg, mc, st);
+        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, tp, p, max_tiles, cg, mc, st);
+        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, tp, p, max_tiles, cg, mc, st);
+        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, tp, p, max_tiles, cg, mc, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -34,6 +34,7 @@ constexpr int kTopT = 4;  // cached |w| candidates per column (weight-stationary
 cudaError_t launch_weight_prepare(const __half* w, int64_t K, int64_t N, int64_t ldw, int8_t* wq_t,
                                   int64_t ldq, float* col_amax, uint16_t* cand_v, int32_t* cand_r,
                                   uint32_t* scratch_v, int32_t* scratch_r, cudaStream_t st);
+// p_count points at [count, pad x3, patched-column bit mask (ceil(N/32) words)]
 cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                 const uint32_t* mask, const float* amax_full,
                                 const uint16_t* cand_v, const int32_t* cand_r, int32_t* p_count,
@@ -68,11 +69,14 @@ struct GemmArgs {
     const __half* wo;
     int64_t ldwo;
     int64_t wo_cap;
-    // column remap for the weight-stationary patch GEMM (nullable): output
-    // column c of this GEMM is Y column col_map[c]; the live column count is
-    // *n_count (<= N) read on the device.
-    const int32_t* col_map;
-    const int32_t* n_count;
+    // weight-stationary patches (nullable): b_patch holds the re-derived codes
+    // (K-major, ldb) of *patch_count columns, patched column j is Y column
+    // patch_idx[j] with amax patch_amax[j]; run as extra tiles of the same launch
+    const int8_t* b_patch;
+    const int32_t* patch_count;
+    const int32_t* patch_idx;
+    const float* patch_amax;
+    const uint32_t* patch_mask;  // bit j set: column j is patched (main tiles skip it)
 };
 
 cudaError_t launch_gemm_sm100(const GemmArgs& args, int epi, cudaStream_t st);

@@ -322,26 +322,40 @@ __global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N,
         const int32_t p = atomicAdd(p_count, 1);
         p_idx[p] = static_cast<int32_t>(j);
         p_amax[p] = a_new;
+        atomicOr(reinterpret_cast<uint32_t*>(p_count) + 4 + (j >> 5), 1u << (j & 31));
     }
 }
 
-// codes of the patched columns (K-major rows of WqP), outlier rows = 0
-__global__ void patch_quantize_kernel(const __half* __restrict__ w, int64_t K, int64_t ldw,
-                                      const uint32_t* __restrict__ mask,
-                                      const int32_t* __restrict__ p_count,
-                                      const int32_t* __restrict__ p_idx,
-                                      const float* __restrict__ p_amax, int8_t* __restrict__ wq_p,
-                                      int64_t ldq) {
+// codes of the patched columns (K-major rows of WqP), outlier rows = 0.
+// grid.x covers ldq in chunks of 2048 (8 consecutive k per thread: 8
+// independent strided loads in flight), grid.y strides over the patches.
+__global__ void __launch_bounds__(256) patch_quantize_kernel(
+    const __half* __restrict__ w, int64_t K, int64_t ldw, const uint32_t* __restrict__ mask,
+    const int32_t* __restrict__ p_count, const int32_t* __restrict__ p_idx,
+    const float* __restrict__ p_amax, int8_t* __restrict__ wq_p, int64_t ldq) {
     const int32_t np = *p_count;
-    for (int32_t p = blockIdx.x; p < np; p += gridDim.x) {
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 2048 + threadIdx.x * 8;
+    if (k0 >= ldq) return;
+    for (int32_t p = blockIdx.y; p < np; p += gridDim.y) {
         const int64_t j = p_idx[p];
         const double s = scale_of(p_amax[p]);
         const float s32 = static_cast<float>(s);
-        int8_t* dst = wq_p + static_cast<int64_t>(p) * ldq;
-        for (int64_t k = threadIdx.x; k < ldq; k += blockDim.x) {
-            int c = 0;
-            if (k < K && !row_is_out(mask, k)) c = code_fast(__half2float(w[k * ldw + j]), s32, s);
-            dst[k] = static_cast<int8_t>(c);
+        __half h[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) h[e] = (k0 + e < K) ? w[(k0 + e) * ldw + j] : __float2half(0.0f);
+        uint32_t b[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int64_t k = k0 + e;
+            const int c = (k < K && !row_is_out(mask, k)) ? code_fast(__half2float(h[e]), s32, s) : 0;
+            b[e] = static_cast<uint32_t>(c) & 0xFFu;
+        }
+        int8_t* dst = wq_p + static_cast<int64_t>(p) * ldq + k0;
+        if (k0 + 8 <= ldq) {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24,
+                                                        b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24);
+        } else {
+            for (int e = 0; k0 + e < ldq; ++e) dst[e] = static_cast<int8_t>(b[e]);
         }
     }
 }
@@ -424,13 +438,15 @@ cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t l
                                 const uint16_t* cand_v, const int32_t* cand_r, int32_t* p_count,
                                 int32_t* p_idx, float* p_amax, int8_t* wq_p, int64_t ldq,
                                 cudaStream_t st) {
-    zero_words_kernel<<<1, 32, 0, st>>>(reinterpret_cast<uint32_t*>(p_count), 1);
+    const int64_t zw = 4 + (N + 31) / 32;  // count + patched-column mask
+    zero_words_kernel<<<static_cast<unsigned>(imin64((zw + 255) / 256, 64)), 256, 0, st>>>(
+        reinterpret_cast<uint32_t*>(p_count), zw);
     count_launch();
     fixup_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(
         w, K, N, ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax);
     count_launch();
-    patch_quantize_kernel<<<static_cast<unsigned>(imin64(N, static_cast<int64_t>(num_sms()) * 4)), 256,
-                            0, st>>>(w, K, ldw, mask, p_count, p_idx, p_amax, wq_p, ldq);
+    const dim3 pgrid(static_cast<unsigned>((ldq + 2047) / 2048), static_cast<unsigned>(imin64(N, 256)));
+    patch_quantize_kernel<<<pgrid, 256, 0, st>>>(w, K, ldw, mask, p_count, p_idx, p_amax, wq_p, ldq);
     count_launch();
     return cudaGetLastError();
 }
