@@ -130,7 +130,10 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
  * Int8 linear module (weight-stationary). Replaces the reference's module
  * boundary LinearBackend("llm_int8") + _linear (transformer.py:45-66,
  * 257-267), which re-quantizes W on every call (transformer.py:260, 267).
- * prepare() caches WqT with full-column scales plus each column's top-4 |w|
+ * prepare() caches WqT with full-column scales, the codes q2 under each
+ * column's second-largest |w| (what a patched column needs when only its
+ * top-1 row is an outlier: one contiguous row instead of a strided column of
+ * W; 1 byte per parameter), plus each column's top-4 |w|
  * candidates; forward() reproduces the per-call column scales over the keep
  * rows EXACTLY (quantize.py:182-187 on w[keep, :], gemm.py:243) by patching
  * only the columns whose cached maximisers are all outlier rows. Outputs are
@@ -155,9 +158,24 @@ int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, in
                         const void* wbuf, int64_t K, int64_t N, float alpha, void* y, int64_t ldy,
                         int out_kind, void* workspace, size_t workspace_bytes,
                         int32_t* o_count_dev, void* stream);
+/* Decode routing. Calls with M <= max_m (default 16, env I8MM_DECODE_MAX_M,
+ * at most 256) whose per-CTA slice of X fits shared memory run ONE
+ * cooperative kernel (decode_sm100.cu): outlier scan, row
+ * quantization, column fixup, patched-column dot products and a swap-AB
+ * stream-K tcgen05 GEMM that streams WqT once over all SMs (weight tiles are
+ * prefetched while the prologue runs). i8mm_linear_forward issues exactly that
+ * launch; with the split entries, i8mm_linear_prologue only records alpha and
+ * i8mm_linear_gemm runs the kernel. Outputs are bit-identical to the prefill
+ * kernels. The workspace layout depends on the routing, so set max_m before
+ * sizing a workspace. */
+void i8mm_debug_set_decode_max_m(int max_m);
+int i8mm_linear_uses_decode(int64_t M, int64_t K, int64_t N);
+/* Dev tool: per-CTA %globaltimer stamps of the decode kernel (16 u64 per CTA,
+ * device buffer sized for one CTA per SM; NULL disables). */
+void i8mm_debug_decode_timeline(void* stamps);
 /* introspection (tests): device pointers into the workspace / weight buffer.
  * workspace views: [o_count, o_idx, xq, row_amax, p_count, p_idx, p_amax, wq_p]
- * weight views:    [wq_t, col_amax, cand_v, cand_r] */
+ * weight views:    [wq_t, col_amax, cand_v, cand_r(, q2)] */
 int i8mm_linear_workspace_views(void* workspace, int64_t M, int64_t K, int64_t N, void** views,
                                 int n_views);
 int i8mm_linear_weight_views(void* wbuf, int64_t K, int64_t N, void** views, int n_views);

@@ -55,6 +55,9 @@ EXPORTED_SYMBOLS = (
     "i8mm_linear_forward",
     "i8mm_linear_workspace_views",
     "i8mm_linear_weight_views",
+    "i8mm_debug_set_decode_max_m",
+    "i8mm_linear_uses_decode",
+    "i8mm_debug_decode_timeline",
 )
 
 _lib = None
@@ -71,6 +74,9 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_status_string": ([I32], ctypes.c_char_p),
         "i8mm_launch_count": ([], ctypes.c_uint64),
         "i8mm_debug_set_gemm_variant": ([I32, I32], None),
+        "i8mm_debug_set_decode_max_m": ([I32], None),
+        "i8mm_linear_uses_decode": ([I64, I64, I64], I32),
+        "i8mm_debug_decode_timeline": ([P], None),
         "i8mm_outlier_scan": ([P, I64, I64, I64, F32, P, P, P], I32),
         "i8mm_outlier_compact": ([P, I64, P, P, P], I32),
         "i8mm_quantize_rows": ([P, I64, I64, I64, P, P, P, P, I64, P, P, I64, P], I32),

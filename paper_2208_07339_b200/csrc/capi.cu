@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/llmint8.h"
@@ -232,11 +233,41 @@ struct Workspace {
     int32_t* p_count;
     int32_t* p_idx;
     float* p_amax;
+    int32_t* p_src;
     int8_t* wq_p;
+    // decode path (M <= decode_max_m(), weight-stationary only)
+    bool decode;
+    uint32_t* part;
+    uint32_t* ramax_bits;
+    int32_t* patch_pos;
+    int32_t* pc;
+    int32_t* c32;
+    int64_t c32_words;
+    int32_t* tile_cnt;
+    int64_t n_tiles;
+    int32_t* pc_cnt;
+    uint32_t* thr_word;  // alpha threshold bits, written by the prologue entry
     int64_t ldq, o_cap;
     size_t bytes;
 };
-constexpr int64_t kOCap = 64;  // compacted outlier slice width (wider |O| reads X directly)
+constexpr int64_t kOCap = 64;
+
+// Largest M routed to the decode kernels (decode_sm100.cu). Default from
+// I8MM_DECODE_MAX_M (0 disables), else 16 (measured crossover, profiles/r1); capped at kDecodeMaxM.
+int g_decode_max_m = -1;
+int decode_max_m() {
+    if (g_decode_max_m < 0) {
+        const char* e = getenv("I8MM_DECODE_MAX_M");
+        g_decode_max_m = (e && e[0]) ? atoi(e) : 16;
+        if (g_decode_max_m > kDecodeMaxM) g_decode_max_m = kDecodeMaxM;
+        if (g_decode_max_m < 0) g_decode_max_m = 0;
+    }
+    return g_decode_max_m;
+}
+
+bool uses_decode(int64_t M, int64_t K, int64_t N) {
+    return M > 0 && M <= decode_max_m() && decode_fits(M, K, N);
+}  // compacted outlier slice width (wider |O| reads X directly)
 
 // Per-call workspace. `linear` = weight-stationary layout: no WqT (it lives in
 // the prepared weight buffer) but room for the patched columns (worst case N).
@@ -265,7 +296,26 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
         w.p_count = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (4 + (N + 31) / 32)));
         w.p_idx = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
         w.p_amax = reinterpret_cast<float*>(take(sizeof(float) * N));
-        w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
+        w.p_src = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
+        w.decode = uses_decode(M, K, N);
+        if (w.decode) {
+            // patched columns are dotted in the prologue: no patch codes, but
+            // split-K accumulators, partial mask words and per-column state
+            const int64_t grid = decode_grid(K, N);
+            w.part = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * grid * M));
+            w.ramax_bits = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * M));
+            w.patch_pos = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
+            w.pc = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(N * M)));
+            // split-tile partials: two [M x 128] int32 slots per CTA
+            w.c32_words = 2 * grid * M * 128;
+            w.c32 = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(w.c32_words)));
+            w.n_tiles = (N + 127) / 128;
+            w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (w.n_tiles + 2)));
+            w.pc_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
+            w.thr_word = reinterpret_cast<uint32_t*>(w.tile_cnt + w.n_tiles + 1);
+        } else {
+            w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
+        }
     }
     w.bytes = p - p0;
     return w;
@@ -274,6 +324,7 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
 // Prepared weight buffer of the weight-stationary linear layer.
 struct WeightBuf {
     int8_t* wq_t;     // N x ldq codes with the full-column scale
+    int8_t* q2;       // N x ldq codes with the second-candidate scale (patched columns)
     float* col_amax;  // N, amax over all K rows
     uint16_t* cand_v; // kTopT x N, |w| fp16 bits, descending
     int32_t* cand_r;  // kTopT x N, rows
@@ -292,6 +343,7 @@ WeightBuf carve_weight(void* base, int64_t K, int64_t N) {
         return r;
     };
     b.wq_t = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * b.ldq)));
+    b.q2 = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * b.ldq)));
     b.col_amax = reinterpret_cast<float*>(take(sizeof(float) * N));
     b.cand_v = reinterpret_cast<uint16_t*>(take(sizeof(uint16_t) * kTopT * N));
     b.cand_r = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * kTopT * N));
@@ -350,6 +402,16 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
 }
 
 // ---------------------------------------------------------------- linear layer
+void i8mm_debug_set_decode_max_m(int max_m) {
+    g_decode_max_m = max_m < 0 ? 0 : (max_m > kDecodeMaxM ? kDecodeMaxM : max_m);
+}
+
+void i8mm_debug_decode_timeline(void* stamps) {
+    set_decode_timeline(static_cast<unsigned long long*>(stamps));
+}
+
+int i8mm_linear_uses_decode(int64_t M, int64_t K, int64_t N) { return uses_decode(M, K, N) ? 1 : 0; }
+
 size_t i8mm_linear_weight_bytes(int64_t K, int64_t N) {
     if (K <= 0 || N <= 0) return 0;
     return carve_weight(nullptr, K, N).bytes + 256;
@@ -376,7 +438,7 @@ int i8mm_linear_prepare(const void* w, int64_t ldw, int64_t K, int64_t N, void* 
     const int64_t chunks = (K + rpb - 1) / rpb;
     uint32_t* sv = reinterpret_cast<uint32_t*>(round_up(reinterpret_cast<intptr_t>(scratch), 256));
     int32_t* sr = reinterpret_cast<int32_t*>(sv + chunks * kTopT * N);
-    return cuda_status(launch_weight_prepare(static_cast<const __half*>(w), K, N, ldw, b.wq_t, b.ldq,
+    return cuda_status(launch_weight_prepare(static_cast<const __half*>(w), K, N, ldw, b.wq_t, b.q2, b.ldq,
                                              b.col_amax, b.cand_v, b.cand_r, sv, sr,
                                              static_cast<cudaStream_t>(stream)));
 }
@@ -394,6 +456,53 @@ static int linear_ws(void* workspace, size_t bytes, int64_t M, int64_t K, int64_
     return I8MM_OK;
 }
 
+static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __half* x, int64_t ldx,
+                              int64_t M, int64_t K, const __half* w, int64_t ldw, int64_t N,
+                              float alpha, void* y, int64_t ldy) {
+    DecodeArgs d{};
+    d.x = x;
+    d.ldx = ldx;
+    d.M = M;
+    d.K = K;
+    d.N = N;
+    d.x_vec = (ldx % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
+    d.thr_bits = alpha_threshold_bits(alpha);
+    d.part = ws.part;
+    d.mask = ws.mask;
+    d.o_idx = ws.o_idx;
+    d.o_count = ws.o_count;
+    d.ramax_bits = ws.ramax_bits;
+    d.row_amax = ws.row_amax;
+    d.xq = ws.xq;
+    d.ldq = ws.ldq;
+    d.xo = ws.xo;
+    d.o_cap = ws.o_cap;
+    d.w = w;
+    d.ldw = ldw;
+    d.w_vec = (N % 8 == 0) && (ldw % 8 == 0) && ((reinterpret_cast<uintptr_t>(w) & 15u) == 0);
+    d.wq_t = b.wq_t;
+    d.amax_full = b.col_amax;
+    d.cand_v = b.cand_v;
+    d.cand_r = b.cand_r;
+    d.wo = ws.wo;
+    d.ldwo = round_up(N, 8);
+    d.p_count = ws.p_count;
+    d.p_idx = ws.p_idx;
+    d.p_amax = ws.p_amax;
+    d.patch_pos = ws.patch_pos;
+    d.pc = ws.pc;
+    d.p_src = ws.p_src;
+    d.q2 = b.q2;
+    d.c32 = ws.c32;
+    d.c32_words = ws.c32_words;
+    d.tile_cnt = ws.tile_cnt;
+    d.n_tiles = ws.n_tiles;
+    d.pc_cnt = ws.pc_cnt;
+    d.y = y;
+    d.ldy = ldy;
+    return d;
+}
+
 int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
                          const void* wbuf, int64_t K, int64_t N, float alpha, void* workspace,
                          size_t workspace_bytes, void* stream) {
@@ -409,6 +518,10 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const __half* xh = static_cast<const __half*>(x);
     const __half* wh = static_cast<const __half*>(w);
+    // decode routing: the whole layer is one launch in i8mm_linear_gemm; the
+    // prologue entry only records the threshold for it (i8mm_linear_forward
+    // passes it directly and skips this launch)
+    if (ws.decode) return cuda_status(launch_set_word(ws.thr_word, alpha_threshold_bits(alpha), st));
     if (launch_outlier_scan(xh, M, K, ldx, alpha, ws.mask, nullptr, st)) return I8MM_ERR_CUDA;
     if (launch_outlier_compact(ws.mask, K, ws.o_idx, ws.o_count, st)) return I8MM_ERR_CUDA;
     if (launch_quantize_rows(xh, M, K, ldx, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
@@ -416,8 +529,8 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
         return I8MM_ERR_CUDA;
     if (launch_gather_rows(wh, ldw, N, ws.o_idx, ws.o_count, ws.o_cap, ws.wo, round_up(N, 8), st))
         return I8MM_ERR_CUDA;
-    if (launch_weight_fixup(wh, K, N, ldw, ws.mask, b.col_amax, b.cand_v, b.cand_r, ws.p_count,
-                            ws.p_idx, ws.p_amax, ws.wq_p, ws.ldq, st))
+    if (launch_weight_fixup(wh, K, N, ldw, ws.mask, b.col_amax, b.cand_v, b.cand_r, b.q2,
+                            ws.p_count, ws.p_idx, ws.p_amax, ws.p_src, ws.wq_p, ws.ldq, st))
         return I8MM_ERR_CUDA;
     return I8MM_OK;
 }
@@ -437,6 +550,12 @@ int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64
         case I8MM_OUT_F32: epi = EPI_F32; break;
         case I8MM_OUT_F32_EXACT: epi = EPI_F32_EXACT; break;
         default: return I8MM_ERR_ARGUMENT;
+    }
+    if (ws.decode) {
+        DecodeArgs d = decode_args(ws, b, static_cast<const __half*>(x), ldx, M, K,
+                                   static_cast<const __half*>(w), ldw, N, 6.0f, y, ldy);
+        d.thr_bits_dev = ws.thr_word;
+        return cuda_status(launch_decode(d, epi, static_cast<cudaStream_t>(stream)));
     }
     GemmArgs g{};
     g.a = ws.xq;
@@ -477,6 +596,33 @@ int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, in
                         const void* wbuf, int64_t K, int64_t N, float alpha, void* y, int64_t ldy,
                         int out_kind, void* workspace, size_t workspace_bytes,
                         int32_t* o_count_dev, void* stream) {
+    if (uses_decode(M, K, N)) {  // decode routing: one launch
+        if (int s = check_device()) return s;
+        if (int s = check_inner(K)) return s;
+        if (!(alpha > 0.0f) || !std::isfinite(alpha)) return I8MM_ERR_ALPHA;
+        if (K <= 0 || N <= 0 || ldx < K || ldw < N || ldy < N || !x || !w || !y || !wbuf ||
+            !workspace)
+            return I8MM_ERR_ARGUMENT;
+        int epi;
+        switch (out_kind) {
+            case I8MM_OUT_F16: epi = EPI_F16; break;
+            case I8MM_OUT_F32: epi = EPI_F32; break;
+            case I8MM_OUT_F32_EXACT: epi = EPI_F32_EXACT; break;
+            default: return I8MM_ERR_ARGUMENT;
+        }
+        Workspace ws;
+        if (int s = linear_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
+        const WeightBuf b = carve_weight(
+            reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)), K, N);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const DecodeArgs d = decode_args(ws, b, static_cast<const __half*>(x), ldx, M, K,
+                                         static_cast<const __half*>(w), ldw, N, alpha, y, ldy);
+        if (launch_decode(d, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
+        if (o_count_dev && cudaMemcpyAsync(o_count_dev, ws.o_count, sizeof(int32_t),
+                                           cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return I8MM_ERR_CUDA;
+        return I8MM_OK;
+    }
     int s = i8mm_linear_prologue(x, ldx, M, w, ldw, wbuf, K, N, alpha, workspace, workspace_bytes,
                                  stream);
     if (s) return s;
@@ -512,6 +658,9 @@ int i8mm_linear_workspace_views(void* workspace, int64_t M, int64_t K, int64_t N
 
 int i8mm_linear_weight_views(void* wbuf, int64_t K, int64_t N, void** views, int n_views) {
     if (!wbuf || !views || n_views < 4) return I8MM_ERR_ARGUMENT;
+    if (n_views >= 5)
+        views[4] = carve_weight(reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)),
+                                K, N).q2;
     WeightBuf b = carve_weight(reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)),
                                K, N);
     views[0] = b.wq_t;

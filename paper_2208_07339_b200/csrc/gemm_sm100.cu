@@ -553,7 +553,7 @@ static EncodeTiledFn get_encode_fn() {
 }
 
 // int8 K-major operand [rows x K] with row pitch ld bytes; box = box_rows x 128 B.
-static bool make_tmap_i8(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t K, int64_t ld,
+bool make_tmap_i8(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t K, int64_t ld,
                          int box_rows) {
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return false;
@@ -620,6 +620,11 @@ static cudaError_t launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const
 }
 
 }  // namespace gemm
+
+bool make_tmap_i8_rows(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t K, int64_t ld,
+                       int box_rows) {
+    return gemm::make_tmap_i8(map, base, rows, K, ld, box_rows);
+}
 
 // Kernel-variant overrides for tests / A-B measurements:
 //   I8MM_FORCE_CG1=1 pins the 1-CTA kernel; I8MM_GEMM_MC=2 enables the

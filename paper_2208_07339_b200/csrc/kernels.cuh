@@ -32,14 +32,18 @@ cudaError_t launch_col_amax(const __half* w, int64_t K, int64_t N, int64_t ldw,
 int64_t topt_chunk_rows(int64_t K);
 constexpr int kTopT = 4;  // cached |w| candidates per column (weight-stationary fixup)
 cudaError_t launch_weight_prepare(const __half* w, int64_t K, int64_t N, int64_t ldw, int8_t* wq_t,
-                                  int64_t ldq, float* col_amax, uint16_t* cand_v, int32_t* cand_r,
-                                  uint32_t* scratch_v, int32_t* scratch_r, cudaStream_t st);
+                                  int8_t* q2, int64_t ldq, float* col_amax, uint16_t* cand_v,
+                                  int32_t* cand_r, uint32_t* scratch_v, int32_t* scratch_r,
+                                  cudaStream_t st);
 // p_count points at [count, pad x3, patched-column bit mask (ceil(N/32) words)]
+// q2: cached codes under each column's second-largest |w| (K-major, ldq);
+// p_src[p] = 1 when patch p's codes are q2's row (its top-1 row is the only
+// outlier among the candidates), else they are re-derived from W
 cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                 const uint32_t* mask, const float* amax_full,
-                                const uint16_t* cand_v, const int32_t* cand_r, int32_t* p_count,
-                                int32_t* p_idx, float* p_amax, int8_t* wq_p, int64_t ldq,
-                                cudaStream_t st);
+                                const uint16_t* cand_v, const int32_t* cand_r, const int8_t* q2,
+                                int32_t* p_count, int32_t* p_idx, float* p_amax, int32_t* p_src,
+                                int8_t* wq_p, int64_t ldq, cudaStream_t st);
 cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int64_t lds,
                                 int8_t* dst, int64_t ldd, cudaStream_t st);
 
@@ -80,6 +84,60 @@ struct GemmArgs {
 };
 
 cudaError_t launch_gemm_sm100(const GemmArgs& args, int epi, cudaStream_t st);
+
+// smallest fp16 bit pattern h (as |x| bits) with float(h) >= alpha (prologue.cu)
+uint32_t alpha_threshold_bits(float alpha);
+
+// Decode path (decode_sm100.cu): weight-stationary linear layer for M <= 256.
+struct DecodeArgs {
+    const __half* x;
+    int64_t ldx;
+    int64_t M, K, N;
+    int x_vec;  // X rows 16-byte aligned (ldx % 8 == 0, base aligned)
+    uint32_t thr_bits;
+    const uint32_t* thr_bits_dev;  // nullable: threshold bits stored by i8mm_linear_prologue
+    uint32_t* part;       // [grid] x [M] per-CTA partial row absmax (fp16 bits)
+    uint32_t* mask;       // [ceil(K/32)]
+    int32_t* o_idx;       // [K]
+    int32_t* o_count;     // [1]
+    uint32_t* ramax_bits; // [M] row amax as fp16 bits
+    float* row_amax;      // [M]
+    int8_t* xq;           // [M x ldq]
+    int64_t ldq;
+    __half* xo;           // [M x o_cap]
+    int64_t o_cap;
+    const __half* w;      // K x N fp16 (resident)
+    int64_t ldw;
+    int w_vec;
+    const int8_t* wq_t;   // N x ldq cached codes
+    const float* amax_full;
+    const uint16_t* cand_v;
+    const int32_t* cand_r;
+    __half* wo;           // [o_cap x ldwo]
+    int64_t ldwo;
+    int32_t* p_count;
+    int32_t* p_idx;
+    float* p_amax;
+    int32_t* patch_pos;   // [N]: 1 + patch index, 0 = not patched
+    int32_t* pc;          // [N x M] exact int32 sums of the patched columns
+    int32_t* p_src;       // [N] 1: patch codes are the cached q2 row
+    const int8_t* q2;     // N x ldq second-candidate codes (weight buffer)
+    int32_t* c32;         // [2 x grid] x [M x 128] split-tile partial slots
+    int64_t c32_words;
+    int32_t* tile_cnt;    // [n_tiles]
+    int64_t n_tiles;
+    int32_t* pc_cnt;      // [N] K-chunks of each patched column completed
+    void* y;
+    int64_t ldy;
+};
+constexpr int kDecodeMaxM = 256;
+int decode_stages(int64_t M);
+int decode_grid(int64_t K, int64_t N);
+bool decode_fits(int64_t M, int64_t K, int64_t N);
+// one cooperative launch: prologue + swap-AB stream-K GEMM + epilogue
+cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st);
+cudaError_t launch_set_word(uint32_t* dst, uint32_t value, cudaStream_t st);
+void set_decode_timeline(unsigned long long* stamps);
 void set_gemm_variant(int cg_override, int mc_override);
 
 }  // namespace i8mm

@@ -451,7 +451,7 @@ __global__ void transpose_i8_kernel(const int8_t* __restrict__ src, int64_t rows
 
 // ------------------------------------------------------------------ launchers
 // smallest fp16 bit pattern h (as |x| bits) with float(h) >= alpha (alpha > 0)
-static uint32_t alpha_threshold_bits(float alpha) {
+uint32_t alpha_threshold_bits(float alpha) {
     if (!(alpha <= 65504.0f)) return 0x7C00u;  // only +-inf would qualify
     __half h = __float2half_rn(alpha);
     uint32_t b = __half_as_ushort(h) & 0x7FFFu;

@@ -135,6 +135,10 @@ __global__ void __launch_bounds__(256) quantize_cols_t_kernel(
                 for (int e = 0; e < 8; ++e)
                     if (n0 + nv + e < N) c8[e] = code_fast(__half2float(src[e]), sc32[nv + e], sc[nv + e]);
             }
+            // |x| above the column amax only occurs for the q2 codes (top-1 row
+            // under the second candidate's scale): clip like quantize.py:117
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c8[e] = max(-127, min(127, c8[e]));
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e)
@@ -290,24 +294,27 @@ __global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N,
                              const uint32_t* __restrict__ mask, const float* __restrict__ amax_full,
                              const uint16_t* __restrict__ cand_v, const int32_t* __restrict__ cand_r,
                              int32_t* __restrict__ p_count, int32_t* __restrict__ p_idx,
-                             float* __restrict__ p_amax) {
+                             float* __restrict__ p_amax, int32_t* __restrict__ p_src) {
     const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= N) return;
     const int32_t r0 = cand_r[j];
     if (r0 < 0 || !row_is_out(mask, r0)) return;  // cached maximiser is a keep row
     float a_new = -1.0f;
     bool exhausted = true;
+    int src = 0;  // 1: the new amax is candidate 1's, so the cached q2 codes apply
 #pragma unroll
     for (int i = 1; i < TOPT; ++i) {
         const int32_t r = cand_r[i * N + j];
         if (r < 0) {  // fewer than T rows exist: every row was listed
             exhausted = false;
             a_new = 0.0f;
+            src = i == 1;
             break;
         }
         if (!row_is_out(mask, r)) {
             exhausted = false;
             a_new = half_bits_to_float(cand_v[i * N + j]);
+            src = i == 1;
             break;
         }
     }
@@ -322,6 +329,7 @@ __global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N,
         const int32_t p = atomicAdd(p_count, 1);
         p_idx[p] = static_cast<int32_t>(j);
         p_amax[p] = a_new;
+        p_src[p] = src;
         atomicOr(reinterpret_cast<uint32_t*>(p_count) + 4 + (j >> 5), 1u << (j & 31));
     }
 }
@@ -332,12 +340,20 @@ __global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N,
 __global__ void __launch_bounds__(256) patch_quantize_kernel(
     const __half* __restrict__ w, int64_t K, int64_t ldw, const uint32_t* __restrict__ mask,
     const int32_t* __restrict__ p_count, const int32_t* __restrict__ p_idx,
-    const float* __restrict__ p_amax, int8_t* __restrict__ wq_p, int64_t ldq) {
+    const float* __restrict__ p_amax, const int32_t* __restrict__ p_src,
+    const int8_t* __restrict__ q2, int8_t* __restrict__ wq_p, int64_t ldq) {
     const int32_t np = *p_count;
     const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 2048 + threadIdx.x * 8;
     if (k0 >= ldq) return;
     for (int32_t p = blockIdx.y; p < np; p += gridDim.y) {
         const int64_t j = p_idx[p];
+        if (p_src[p]) {  // cached second-candidate codes: one contiguous row
+            int8_t* dst = wq_p + static_cast<int64_t>(p) * ldq + k0;
+            const int8_t* src = q2 + j * ldq + k0;
+            if (k0 + 8 <= ldq) *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(src);
+            else for (int e = 0; k0 + e < ldq; ++e) dst[e] = src[e];
+            continue;
+        }
         const double s = scale_of(p_amax[p]);
         const float s32 = static_cast<float>(s);
         __half h[8];
@@ -358,6 +374,15 @@ __global__ void __launch_bounds__(256) patch_quantize_kernel(
             for (int e = 0; k0 + e < ldq; ++e) dst[e] = static_cast<int8_t>(b[e]);
         }
     }
+}
+
+// amax over all rows but the top-1 (candidate 1; 0 when K < 2): the scale of
+// the q2 codes a column needs when its top-1 row is an outlier
+__global__ void second_amax_kernel(int64_t N, const uint16_t* __restrict__ cand_v,
+                                   const int32_t* __restrict__ cand_r, float* __restrict__ out) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    out[j] = cand_r[N + j] >= 0 ? half_bits_to_float(cand_v[N + j]) : 0.0f;
 }
 
 // ------------------------------------------------------------------ launchers
@@ -417,8 +442,9 @@ cudaError_t launch_gather_rows(const __half* w, int64_t ldw, int64_t N, const in
 int64_t topt_chunk_rows(int64_t K) { return K < 512 ? (K > 0 ? K : 1) : 512; }
 
 cudaError_t launch_weight_prepare(const __half* w, int64_t K, int64_t N, int64_t ldw, int8_t* wq_t,
-                                  int64_t ldq, float* col_amax, uint16_t* cand_v, int32_t* cand_r,
-                                  uint32_t* scratch_v, int32_t* scratch_r, cudaStream_t st) {
+                                  int8_t* q2, int64_t ldq, float* col_amax, uint16_t* cand_v,
+                                  int32_t* cand_r, uint32_t* scratch_v, int32_t* scratch_r,
+                                  cudaStream_t st) {
     cudaError_t e = launch_quantize_cols_t(w, K, N, ldw, nullptr, wq_t, ldq, col_amax, st);
     if (e != cudaSuccess) return e;
     const int64_t rpb = topt_chunk_rows(K);
@@ -430,23 +456,33 @@ cudaError_t launch_weight_prepare(const __half* w, int64_t K, int64_t N, int64_t
     topt_merge_kernel<<<static_cast<unsigned>((N + 127) / 128), 128, 0, st>>>(N, chunks, scratch_v,
                                                                               scratch_r, cand_v, cand_r);
     count_launch();
+    // q2: codes under the second candidate's amax (scratch_v reused as float[N])
+    float* amax2 = reinterpret_cast<float*>(scratch_v);
+    second_amax_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(N, cand_v, cand_r, amax2);
+    count_launch();
+    const int vec = (ldw % 8 == 0) && aligned16(w);
+    const int64_t kt = (ldq + 63) / 64;
+    quantize_cols_t_kernel<<<dim3(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>(kt)),
+                             256, 0, st>>>(w, K, N, ldw, nullptr, amax2, q2, ldq, vec);
+    count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                 const uint32_t* mask, const float* amax_full,
-                                const uint16_t* cand_v, const int32_t* cand_r, int32_t* p_count,
-                                int32_t* p_idx, float* p_amax, int8_t* wq_p, int64_t ldq,
-                                cudaStream_t st) {
+                                const uint16_t* cand_v, const int32_t* cand_r, const int8_t* q2,
+                                int32_t* p_count, int32_t* p_idx, float* p_amax, int32_t* p_src,
+                                int8_t* wq_p, int64_t ldq, cudaStream_t st) {
     const int64_t zw = 4 + (N + 31) / 32;  // count + patched-column mask
     zero_words_kernel<<<static_cast<unsigned>(imin64((zw + 255) / 256, 64)), 256, 0, st>>>(
         reinterpret_cast<uint32_t*>(p_count), zw);
     count_launch();
     fixup_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(
-        w, K, N, ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax);
+        w, K, N, ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax, p_src);
     count_launch();
     const dim3 pgrid(static_cast<unsigned>((ldq + 2047) / 2048), static_cast<unsigned>(imin64(N, 256)));
-    patch_quantize_kernel<<<pgrid, 256, 0, st>>>(w, K, ldw, mask, p_count, p_idx, p_amax, wq_p, ldq);
+    patch_quantize_kernel<<<pgrid, 256, 0, st>>>(w, K, ldw, mask, p_count, p_idx, p_amax, p_src, q2,
+                                                 wq_p, ldq);
     count_launch();
     return cudaGetLastError();
 }

@@ -1,0 +1,51 @@
+"""Per-CTA timeline of the decode kernels (dev tool): %globaltimer stamps.
+
+    python scripts/decode_timeline.py fc1 1
+"""
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import paper_2208_07339_b200 as pkg  # noqa: E402
+from paper_2208_07339_b200 import _native as nat  # noqa: E402
+from paper_2208_07339_b200.synthetic import planted_pair_device  # noqa: E402
+
+PROJ = {"qkvo": (5120, 5120), "fc1": (5120, 20480), "fc2": (20480, 5120)}
+name, m = sys.argv[1], int(sys.argv[2])
+k, n = PROJ[name]
+L = nat.lib()
+L.i8mm_debug_set_decode_max_m(256)
+x, w, _ = planted_pair_device(m, k, n, 6, 20.0, seed=3, device="cuda")
+lin = pkg.Int8Linear(w, 6.0)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+g = torch.zeros(sms * 16, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    lin(x)
+torch.cuda.synchronize()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush.zero_()
+L.i8mm_debug_decode_timeline(g.data_ptr())
+lin(x)
+torch.cuda.synchronize()
+L.i8mm_debug_decode_timeline(None)
+G = g.view(sms, 16).cpu().double()
+t0 = G[:, 0][G[:, 0] > 0].min()
+
+
+def col(i):
+    v = G[:, i]
+    v = v[v > 0] - t0
+    if v.numel() == 0:
+        return "-"
+    return f"min {v.min() / 1e3:7.2f} med {v.median() / 1e3:7.2f} max {v.max() / 1e3:7.2f} us"
+
+
+labels = {0: "start", 1: "P1 done", 3: "P2 done", 4: "sync2 out",
+          5: "first MMA", 9: "patches", 6: "MMA done", 7: "epi done", 8: "end"}
+for i, lab in labels.items():
+    v = G[:, i]
+    arg = int(torch.argmax(v)) if (v > 0).any() else -1
+    print(f"{lab:10s} {col(i)}  (max at CTA {arg})")

@@ -344,6 +344,21 @@ def test_weight_stationary_candidates(p):
         assert list(cr[:, j]) == order
         assert np.array_equal(cv[:, j].view(np.float16).astype(np.float32), a[order, j])
     assert list(cr[:3, 5]) == [10, 20, 30]
+    # q2: every column's codes under its second-largest |w| (reference rounding,
+    # quantize.py:26-29 with the f64 scale 127 / amax2), stored K-major
+    views5 = (ctypes.c_void_p * 5)()
+    nat.check(nat.lib().i8mm_linear_weight_views(lin.wbuf.data_ptr(), k, n, views5, 5))
+    ldq = (k + 15) // 16 * 16
+    off_q = views5[4] - base
+    q2 = lin.wbuf[off_q:off_q + n * ldq].view(torch.int8).cpu().numpy().reshape(n, ldq)
+    amax2 = np.array([a[sorted(range(k), key=lambda r: (-a[r, j], r))[1], j] for j in range(n)],
+                     dtype=np.float64)
+    prod = w.astype(np.float64) * (127.0 / np.where(amax2 == 0, 127.0, amax2))[None, :]
+    ref_codes = np.clip(np.copysign(np.floor(np.abs(prod) + 0.5), prod), -127, 127).astype(np.int8)
+    bad = np.argwhere(q2[:, :k].T != ref_codes)
+    assert bad.size == 0, (len(bad), bad[:5].tolist(),
+                           [(int(q2[j, r]), int(ref_codes[r, j]), float(w[r, j]), float(amax2[j]))
+                            for r, j in bad[:5].tolist()])
 
 
 _CG1_SCRIPT = r"""
@@ -399,3 +414,93 @@ def test_large_m_multicast_path_vs_oracle(p, oracle_mod, shape):
     assert np.array_equal(_np(lin.matmul(x16, exact=True)), ref.output)
     y16 = _np(lin(x16)).astype(np.float64)
     assert (np.abs(y16 - ref.output) <= _golden.fp16_tolerance(ref.output)).all()
+
+
+# ---------------------------------------------------------------- decode path (M <= 256)
+@pytest.fixture()
+def decode_max(p):
+    from paper_2208_07339_b200 import _native as nat
+
+    L = nat.lib()
+
+    def set_max(m):
+        L.i8mm_debug_set_decode_max_m(m)
+
+    yield set_max
+    L.i8mm_debug_set_decode_max_m(16)
+
+
+@pytest.mark.parametrize("case", [
+    # seed, m, k, n, planted outlier cols, heavy outlier rows of W
+    (10, 1, 5120, 640, 6, 0), (11, 5, 1024, 1000, 6, 2), (12, 16, 2048, 384, 6, 6),
+    (13, 17, 1001, 257, 4, 1), (14, 64, 4096, 1024, 8, 3), (15, 128, 768, 2050, 6, 0),
+    (16, 200, 512, 600, 20, 5), (17, 256, 1536, 768, 6, 2), (18, 3, 256, 130, 70, 0),
+    (19, 40, 8192, 136, 2, 2), (20, 32, 1024, 2000, 6, 6)])
+def test_decode_path_vs_oracle_and_prefill(p, oracle_mod, decode_max, case):
+    """The decode kernels (cooperative prologue + swap-AB stream-K tcgen05 GEMM):
+    exact output bit-identical to the oracle, fp16 output bit-identical to the
+    prefill kernels, |O| and patched columns as the reference semantics imply."""
+    from paper_2208_07339_b200 import _native as nat
+
+    seed, m, k, n, n_out, heavy = case
+    x, w = _ws_case(seed, m, k, n, n_out, heavy)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda(), alpha=6.0)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    decode_max(256)
+    assert nat.lib().i8mm_linear_uses_decode(m, k, n) == 1
+    y_exact = lin.matmul(x16, exact=True)
+    assert np.array_equal(_np(y_exact), ref.output)
+    st = lin.last_stats()
+    assert st["decomposed_cols"] == len(ref.dims)
+    if heavy:
+        assert st["patched_cols"] > 0
+    y16 = lin(x16)
+    decode_max(0)
+    assert nat.lib().i8mm_linear_uses_decode(m, k, n) == 0
+    y16_prefill = lin(x16)
+    assert torch.equal(y16, y16_prefill), "decode and prefill kernels must agree bitwise"
+    st2 = lin.last_stats()
+    assert st2 == st
+
+
+def test_decode_path_repeated_calls_and_strided_x(p, oracle_mod, decode_max):
+    """Per-call state (split-K accumulators, counters) is reset by every call;
+    a row-strided (non 16-byte aligned) X takes the element-load path."""
+    decode_max(256)
+    x, w = _ws_case(21, 24, 1000, 520, 6, 2)
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda(), alpha=6.0)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    big = torch.zeros((24, 1003), dtype=torch.float16, device="cuda")
+    big[:, 1:1001] = torch.from_numpy(x.astype(np.float16)).cuda()
+    xs = big[:, 1:1001]
+    assert xs.stride(0) == 1003
+    for _ in range(3):
+        assert np.array_equal(_np(lin.matmul(xs, exact=True)), ref.output)
+    x2, _ = _ws_case(22, 24, 1000, 520, 3, 0)
+    ref2 = oracle_mod.c_llm_int8_matmul(x2, w, 6.0)
+    assert np.array_equal(_np(lin.matmul(torch.from_numpy(x2.astype(np.float16)).cuda(), exact=True)),
+                          ref2.output)
+
+
+class _MarkTimer:
+    """Stand-in for bench.py's EventTimer: forces the split prologue/gemm entries."""
+
+    def mark(self, name):
+        pass
+
+
+@pytest.mark.parametrize("alpha", [6.0, 4.5])
+def test_decode_split_entries_carry_alpha(p, oracle_mod, decode_max, alpha):
+    """i8mm_linear_prologue + i8mm_linear_gemm in decode routing (the threshold
+    travels through the workspace) == i8mm_linear_forward == the oracle."""
+    decode_max(16)
+    x, w = _ws_case(31, 9, 2048, 700, 5, 1)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, alpha)
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda(), alpha=alpha)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    y_fwd = lin(x16)
+    y_split = lin.matmul(x16, _timer=_MarkTimer())
+    assert torch.equal(y_fwd, y_split)
+    assert lin.last_stats()["decomposed_cols"] == len(ref.dims)
+    assert (np.abs(_np(y_fwd).astype(np.float64) - ref.output) <= _golden.fp16_tolerance(ref.output)).all()
