@@ -38,7 +38,8 @@ enum {
     I8MM_ERR_PARAMS = 4,     /* ParamsMismatchError  (gemm.py:45, 136-146)          */
     I8MM_ERR_ARGUMENT = 5,   /* bad pointer / alignment / workspace too small        */
     I8MM_ERR_CUDA = 6,       /* CUDA launch or driver error                           */
-    I8MM_ERR_UNSUPPORTED = 7 /* device is not sm_100                                  */
+    I8MM_ERR_UNSUPPORTED = 7, /* device is not sm_100                                 */
+    I8MM_ERR_ZEROPOINT = 8   /* ValueError: zeropoint outside int16 (quantize.py:162-166) */
 };
 
 enum { I8MM_OUT_F16 = 0, I8MM_OUT_F32 = 1, I8MM_OUT_F32_EXACT = 2 };
@@ -179,6 +180,52 @@ void i8mm_debug_decode_timeline(void* stamps);
 int i8mm_linear_workspace_views(void* workspace, int64_t M, int64_t K, int64_t N, void** views,
                                 int n_views);
 int i8mm_linear_weight_views(void* wbuf, int64_t K, int64_t N, void** views, int n_views);
+
+/* ---------------------------------------------------------------------------
+ * Sibling schemes of the backend plugin point (LinearBackend kinds "absmax"
+ * and "zeropoint", transformer.py:42-62): tensor-wise quantization and its
+ * matmuls on the same tcgen05 int8 GEMM.
+ */
+/* One pass over X: out3 = [max|x|, min x, max x] (float, device); scratch =
+ * 3 int32 of device memory. (quantize.py:141, 157-158) */
+int i8mm_tensor_stats(const void* x, int64_t rows, int64_t cols, int64_t ld, int32_t* scratch,
+                      float* out3, void* stream);
+/* absmax_quantize codes (quantize.py:137-151): clip(rha(127/amax * x)), amax
+ * read from device memory (0 -> all-zero codes). transpose = 1 writes the
+ * K-major layout (cols x ldq) the GEMM uses for B; padding written 0. */
+int i8mm_absmax_quantize(const void* x, int64_t rows, int64_t cols, int64_t ld, const float* amax,
+                         int8_t* q, int64_t ldq, int transpose, void* stream);
+/* Host-side zeropoint parameters from the tensor's min/max, exactly as
+ * quantize.py:153-166: constant tensor -> (nd 1, zp 0, offset lo); else
+ * nd = 254/(hi-lo), zp = rha(nd*lo) + 127, I8MM_ERR_ZEROPOINT outside int16. */
+int i8mm_zeropoint_params(float lo, float hi, double* nd, int32_t* zp, double* offset);
+/* zeropoint_quantize codes (quantize.py:167-171): clip(rha(nd*x) - zp). */
+int i8mm_zeropoint_quantize(const void* x, int64_t rows, int64_t cols, int64_t ld, double nd, int32_t zp,
+                            int8_t* q, int64_t ldq, int transpose, void* stream);
+/* out[r] = sum of the int8 row r (rowsum(A); colsum(B) of a K-major B). */
+int i8mm_rowsum_i8(const int8_t* q, int64_t rows, int64_t cols, int64_t ld, int32_t* out, void* stream);
+/* absmax dequantization (gemm.py:133): f32(f64(c) / (s_x * s_w)), s = 127/amax. */
+int i8mm_dequantize_absmax(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const float* amax_x,
+                           const float* amax_w, float* out, int64_t ldo, void* stream);
+/* zeropoint_gemm_i32 (gemm.py:85-104, unrolled form, exact int64) with the
+ * int32 range check (gemm.py:71-75 -> *overflow = 1) and, when out != NULL,
+ * the dequantization + constant-offset terms of zeropoint_matmul
+ * (gemm.py:175-187); acc_out (nullable) receives the int32 accumulator. */
+int i8mm_zeropoint_combine(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const int32_t* rowsum_a,
+                           const int32_t* colsum_b, int64_t K, int32_t zp_a, int32_t zp_b, double nd_a,
+                           double nd_b, double off_a, double off_b, float* out, int64_t ldo,
+                           int32_t* acc_out, int32_t* overflow, void* stream);
+/* Whole pipelines, fp16 X (M x K) and W (K x N), float32 Y. */
+size_t i8mm_scalar_workspace_size(int64_t M, int64_t K, int64_t N);
+/* absmax_matmul (gemm.py:150-156); never synchronizes the host. */
+int i8mm_absmax_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M, int64_t K,
+                       int64_t N, float* y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                       void* stream);
+/* zeropoint_matmul (gemm.py:159-187; unrolled and direct forms are identical).
+ * Synchronizes the stream: the zeropoints are validated on the host. */
+int i8mm_zeropoint_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M, int64_t K,
+                          int64_t N, float* y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                          void* stream);
 
 #ifdef __cplusplus
 }

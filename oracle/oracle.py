@@ -181,6 +181,70 @@ def vectorwise_matmul(x: np.ndarray, w: np.ndarray) -> np.ndarray:
     return dequantize_output(int8_gemm_i32(qx, qw), sx, sw)
 
 
+# ---- sibling schemes (tensor-wise), quantize.py:120-171, gemm.py:85-104, 150-187
+
+ZP_INT16_MIN, ZP_INT16_MAX = -(1 << 15), (1 << 15) - 1  # quantize.py:22-23
+
+
+def absmax_quantize(x: np.ndarray) -> tuple[np.ndarray, float]:
+    """quantize.py:137-151 -- codes, scale (all-zero input: zero codes, scale 1)."""
+    data = np.asarray(x, dtype=np.float64)
+    amax = float(np.abs(data).max())
+    if amax == 0.0:
+        return np.zeros(data.shape, dtype=np.int8), 1.0
+    scale = 127.0 / amax
+    return to_codes(scale * data), scale
+
+
+def zeropoint_quantize(x: np.ndarray) -> tuple[np.ndarray, float, int, float]:
+    """quantize.py:153-171 -- codes, nd, zp, offset; ValueError outside int16."""
+    data = np.asarray(x, dtype=np.float64)
+    lo, hi = float(data.min()), float(data.max())
+    if hi == lo:
+        return np.zeros(data.shape, dtype=np.int8), 1.0, 0, lo
+    nd = 254.0 / (hi - lo)
+    zp = int(round_half_away(np.float64(nd * lo))) + 127
+    if not (ZP_INT16_MIN <= zp <= ZP_INT16_MAX):
+        raise ValueError(f"input offset too extreme for a 16-bit zeropoint (zp={zp})")
+    stored = round_half_away(nd * data) - zp
+    return np.clip(stored, -127, 127).astype(np.int8), nd, zp, 0.0
+
+
+def zeropoint_gemm_i32(a: np.ndarray, b: np.ndarray, zp_a: int, zp_b: int) -> np.ndarray:
+    """gemm.py:85-104 -- (A + zp_a)(B + zp_b) exactly; OverflowError outside int32
+    (gemm.py:71-75). The int64 matmul is done as exact float64 BLAS on the
+    codes (see module docstring) plus the integer unrolled terms."""
+    a64 = a.astype(np.int64)
+    b64 = b.astype(np.int64)
+    acc = (int8_gemm_i32(a, b).astype(np.int64) + zp_b * a64.sum(axis=1, keepdims=True)
+           + zp_a * b64.sum(axis=0, keepdims=True) + a.shape[1] * zp_a * zp_b)
+    if acc.min(initial=0) < np.iinfo(np.int32).min or acc.max(initial=0) > np.iinfo(np.int32).max:
+        raise OverflowError("accumulated values exceed the signed 32-bit range")
+    return acc.astype(np.int32)
+
+
+def absmax_matmul(x: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """gemm.py:150-156 -- f32( f64(C) / (s_x * s_w) )."""
+    qx, sx = absmax_quantize(x)
+    qw, sw = absmax_quantize(w)
+    return (int8_gemm_i32(qx, qw).astype(np.float64) / (sx * sw)).astype(np.float32)
+
+
+def zeropoint_matmul(x: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """gemm.py:159-187 -- shifted product, dequant by nd_x*nd_w, offset terms."""
+    qx, ndx, zpx, offx = zeropoint_quantize(x)
+    qw, ndw, zpw, offw = zeropoint_quantize(w)
+    h = qx.shape[1]
+    c = zeropoint_gemm_i32(qx, qw, zpx, zpw)
+    out = c.astype(np.float64) / (ndx * ndw)
+    if offx != 0.0 or offw != 0.0:
+        ta = qx.astype(np.int64) + zpx
+        tb = qw.astype(np.int64) + zpw
+        out = (out + (offw / ndx) * ta.sum(axis=1, keepdims=True)
+               + (offx / ndw) * tb.sum(axis=0, keepdims=True) + offx * offw * h)
+    return out.astype(np.float32)
+
+
 def planted_pair(rows, inner, cols, outlier_cols, outlier_scale, seed):
     """sweep.py:60-77 -- Gaussian X with scaled planted columns, Gaussian W."""
     rng = np.random.Generator(np.random.PCG64(seed))

@@ -8,13 +8,16 @@ CUDA kernels for sm_100a (tcgen05 + TMA + TMEM) behind the C ABI in
 """
 
 from .errors import GemmOverflowError, ParamsMismatchError, ShapeMismatchError
-from .gemm import (MAX_INNER_DIM, MatmulResult, dequantize_output, extract_outlier_columns,
-                   int8_gemm_i32, llm_int8_matmul, vectorwise_matmul)
+from .gemm import (MAX_INNER_DIM, MatmulResult, absmax_matmul, dequantize_output,
+                   extract_outlier_columns, int8_gemm_i32, llm_int8_matmul, vectorwise_matmul,
+                   zeropoint_gemm_i32, zeropoint_matmul)
 from .linear import (ABSMAX, BACKEND_KINDS, EXACT, VECTORWISE, ZEROPOINT, Int8Linear,
                      LinearBackend, _linear, linear, llm_int8_backend)
-from .quantize import colwise_quantize, rowwise_quantize, vectorwise_params
+from .quantize import (absmax_quantize, colwise_quantize, rowwise_quantize, vectorwise_params,
+                       zeropoint_quantize)
 from .synthetic import planted_pair
-from .types import ColwiseParams, OutlierSet, QuantizedTensor, RowwiseParams
+from .types import (AbsmaxParams, ColwiseParams, OutlierSet, QuantizedTensor, RowwiseParams,
+                    ZeropointParams)
 
 __version__ = "0.1.0"
 
@@ -25,4 +28,6 @@ __all__ = [
     "vectorwise_matmul", "rowwise_quantize", "colwise_quantize", "vectorwise_params",
     "BACKEND_KINDS", "LinearBackend", "EXACT", "ABSMAX", "ZEROPOINT", "VECTORWISE",
     "llm_int8_backend", "linear", "_linear", "Int8Linear", "planted_pair",
+    "AbsmaxParams", "ZeropointParams", "absmax_quantize", "zeropoint_quantize",
+    "absmax_matmul", "zeropoint_matmul", "zeropoint_gemm_i32",
 ]

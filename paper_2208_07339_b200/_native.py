@@ -24,6 +24,7 @@ I8MM_ERR_PARAMS = 4
 I8MM_ERR_ARGUMENT = 5
 I8MM_ERR_CUDA = 6
 I8MM_ERR_UNSUPPORTED = 7
+I8MM_ERR_ZEROPOINT = 8
 
 OUT_F16 = 0
 OUT_F32 = 1
@@ -58,6 +59,16 @@ EXPORTED_SYMBOLS = (
     "i8mm_debug_set_decode_max_m",
     "i8mm_linear_uses_decode",
     "i8mm_debug_decode_timeline",
+    "i8mm_tensor_stats",
+    "i8mm_absmax_quantize",
+    "i8mm_zeropoint_params",
+    "i8mm_zeropoint_quantize",
+    "i8mm_rowsum_i8",
+    "i8mm_dequantize_absmax",
+    "i8mm_zeropoint_combine",
+    "i8mm_scalar_workspace_size",
+    "i8mm_absmax_matmul",
+    "i8mm_zeropoint_matmul",
 )
 
 _lib = None
@@ -69,6 +80,8 @@ class NativeLibraryError(RuntimeError):
 
 def _declare(lib: ctypes.CDLL) -> None:
     P, I64, I32, F32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+    F64 = ctypes.c_double
+    SZ = ctypes.c_size_t
     sigs = {
         "i8mm_version": ([], I32),
         "i8mm_status_string": ([I32], ctypes.c_char_p),
@@ -102,6 +115,17 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_llm_int8_workspace_size": ([I64, I64, I64], ctypes.c_size_t),
         "i8mm_llm_int8_matmul": ([P, I64, P, I64, I64, I64, I64, F32, P, I64, I32, P,
                                   ctypes.c_size_t, P, P], I32),
+        "i8mm_tensor_stats": ([P, I64, I64, I64, P, P, P], I32),
+        "i8mm_absmax_quantize": ([P, I64, I64, I64, P, P, I64, I32, P], I32),
+        "i8mm_zeropoint_params": ([F32, F32, P, P, P], I32),
+        "i8mm_zeropoint_quantize": ([P, I64, I64, I64, F64, I32, P, I64, I32, P], I32),
+        "i8mm_rowsum_i8": ([P, I64, I64, I64, P, P], I32),
+        "i8mm_dequantize_absmax": ([P, I64, I64, I64, P, P, P, I64, P], I32),
+        "i8mm_zeropoint_combine": ([P, I64, I64, I64, P, P, I64, I32, I32, F64, F64, F64, F64, P,
+                                    I64, P, P, P], I32),
+        "i8mm_scalar_workspace_size": ([I64, I64, I64], SZ),
+        "i8mm_absmax_matmul": ([P, I64, P, I64, I64, I64, I64, P, I64, P, SZ, P], I32),
+        "i8mm_zeropoint_matmul": ([P, I64, P, I64, I64, I64, I64, P, I64, P, SZ, P], I32),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -149,7 +173,7 @@ def check(status: int, what: str = "") -> None:
         raise ValueError(msg)
     if status == I8MM_ERR_UNSUPPORTED:
         raise NativeLibraryError(msg)
-    if status == I8MM_ERR_ARGUMENT:
+    if status in (I8MM_ERR_ARGUMENT, I8MM_ERR_ZEROPOINT):
         raise ValueError(msg)
     raise RuntimeError(msg)
 

@@ -8,6 +8,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstring>
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
@@ -76,6 +77,7 @@ const char* i8mm_status_string(int s) {
         case I8MM_ERR_ARGUMENT: return "invalid argument";
         case I8MM_ERR_CUDA: return "CUDA error";
         case I8MM_ERR_UNSUPPORTED: return "device is not sm_100 (B200)";
+        case I8MM_ERR_ZEROPOINT: return "input offset too extreme for a 16-bit zeropoint";
         default: return "unknown status";
     }
 }
@@ -668,6 +670,218 @@ int i8mm_linear_weight_views(void* wbuf, int64_t K, int64_t N, void** views, int
     views[2] = b.cand_v;
     views[3] = b.cand_r;
     return I8MM_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- sibling schemes
+// Tensor-wise absmax / zeropoint pipelines (quantize.py:120-171,
+// gemm.py:85-104, 150-187) on the same tcgen05 int8 GEMM.
+namespace {
+struct ScalarWs {
+    int8_t* xq;
+    int8_t* wq_t;
+    int32_t* c;
+    int32_t* stats;   // 2 x 4 int32
+    float* fstats;    // 2 x 4 floats: [amax, min, max, -]
+    int32_t* rowsum;  // M
+    int32_t* colsum;  // N
+    int32_t* flag;    // overflow
+    int64_t ldq;
+    size_t bytes;
+};
+ScalarWs carve_scalar(void* base, int64_t M, int64_t K, int64_t N) {
+    ScalarWs w{};
+    w.ldq = round_up(K, 16);
+    uintptr_t p = reinterpret_cast<uintptr_t>(base);
+    const uintptr_t p0 = p;
+    auto take = [&](size_t bytes) {
+        uintptr_t r = p;
+        p += static_cast<uintptr_t>(round_up(static_cast<int64_t>(bytes), 256));
+        return r;
+    };
+    w.xq = reinterpret_cast<int8_t*>(take(static_cast<size_t>(M * w.ldq)));
+    w.wq_t = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
+    w.c = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(M * N)));
+    w.stats = reinterpret_cast<int32_t*>(take(8 * sizeof(int32_t)));
+    w.fstats = reinterpret_cast<float*>(take(8 * sizeof(float)));
+    w.rowsum = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * M));
+    w.colsum = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
+    w.flag = reinterpret_cast<int32_t*>(take(sizeof(int32_t)));
+    w.bytes = p - p0;
+    return w;
+}
+
+double rha(double v) { return std::copysign(std::floor(std::fabs(v) + 0.5), v); }
+}  // namespace
+
+extern "C" {
+
+int i8mm_tensor_stats(const void* x, int64_t rows, int64_t cols, int64_t ld, int32_t* scratch,
+                      float* out3, void* stream) {
+    if (int s = check_device()) return s;
+    if (rows <= 0 || cols <= 0 || ld < cols || !x || !scratch || !out3) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_tensor_stats(static_cast<const __half*>(x), rows, cols, ld, scratch, out3,
+                                           static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_absmax_quantize(const void* x, int64_t rows, int64_t cols, int64_t ld, const float* amax,
+                         int8_t* q, int64_t ldq, int transpose, void* stream) {
+    if (int s = check_device()) return s;
+    const int64_t need = transpose ? rows : cols;
+    if (rows <= 0 || cols <= 0 || ld < cols || ldq < need || !x || !amax || !q) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_quantize_scalar(static_cast<const __half*>(x), rows, cols, ld, 0, amax, 0.0, 0,
+                                              q, ldq, transpose, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_zeropoint_params(float lo, float hi, double* nd, int32_t* zp, double* offset) {
+    if (!nd || !zp || !offset) return I8MM_ERR_ARGUMENT;
+    if (hi == lo) {  // quantize.py:156-160: constant tensor -> offset, nd 1, zp 0
+        *nd = 1.0;
+        *zp = 0;
+        *offset = static_cast<double>(lo);
+        return I8MM_OK;
+    }
+    const double n = 254.0 / (static_cast<double>(hi) - static_cast<double>(lo));
+    const double z = rha(n * static_cast<double>(lo)) + 127.0;  // quantize.py:162
+    if (!(z >= -32768.0 && z <= 32767.0)) return I8MM_ERR_ZEROPOINT;
+    *nd = n;
+    *zp = static_cast<int32_t>(z);
+    *offset = 0.0;
+    return I8MM_OK;
+}
+
+int i8mm_zeropoint_quantize(const void* x, int64_t rows, int64_t cols, int64_t ld, double nd, int32_t zp,
+                            int8_t* q, int64_t ldq, int transpose, void* stream) {
+    if (int s = check_device()) return s;
+    const int64_t need = transpose ? rows : cols;
+    if (rows <= 0 || cols <= 0 || ld < cols || ldq < need || !x || !q || !(nd > 0.0)) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_quantize_scalar(static_cast<const __half*>(x), rows, cols, ld, 1, nullptr, nd, zp,
+                                              q, ldq, transpose, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_rowsum_i8(const int8_t* q, int64_t rows, int64_t cols, int64_t ld, int32_t* out, void* stream) {
+    if (int s = check_device()) return s;
+    if (rows < 0 || cols < 0 || ld < cols || !q || !out) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_rowsum_i8(q, rows, cols, ld, out, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_dequantize_absmax(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const float* amax_x,
+                           const float* amax_w, float* out, int64_t ldo, void* stream) {
+    if (int s = check_device()) return s;
+    if (M <= 0 || N <= 0 || ldc < N || ldo < N || !c || !amax_x || !amax_w || !out) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_dequant_absmax(c, M, N, ldc, amax_x, amax_w, out, ldo,
+                                             static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_zeropoint_combine(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const int32_t* rowsum_a,
+                           const int32_t* colsum_b, int64_t K, int32_t zp_a, int32_t zp_b, double nd_a,
+                           double nd_b, double off_a, double off_b, float* out, int64_t ldo,
+                           int32_t* acc_out, int32_t* overflow, void* stream) {
+    if (int s = check_device()) return s;
+    if (M <= 0 || N <= 0 || ldc < N || !c || !rowsum_a || !colsum_b || !overflow || (out && ldo < N))
+        return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_zeropoint_combine(c, M, N, ldc, rowsum_a, colsum_b, K, zp_a, zp_b, nd_a, nd_b,
+                                                off_a, off_b, out, ldo, acc_out, overflow,
+                                                static_cast<cudaStream_t>(stream)));
+}
+
+size_t i8mm_scalar_workspace_size(int64_t M, int64_t K, int64_t N) {
+    if (M <= 0 || K <= 0 || N <= 0) return 0;
+    return carve_scalar(nullptr, M, K, N).bytes + 256;
+}
+
+static int scalar_ws(void* workspace, size_t bytes, int64_t M, int64_t K, int64_t N, ScalarWs* ws) {
+    void* base = reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(workspace), 256));
+    *ws = carve_scalar(base, M, K, N);
+    if (ws->bytes + (static_cast<char*>(base) - static_cast<char*>(workspace)) > bytes)
+        return I8MM_ERR_ARGUMENT;
+    return I8MM_OK;
+}
+
+static int gemm_codes(const ScalarWs& ws, int64_t M, int64_t K, int64_t N, cudaStream_t st) {
+    GemmArgs g{};
+    g.a = ws.xq;
+    g.lda = ws.ldq;
+    g.b = ws.wq_t;
+    g.ldb = ws.ldq;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.y = ws.c;
+    g.ldy = N;
+    return launch_gemm_sm100(g, EPI_I32, st) == cudaSuccess ? I8MM_OK : I8MM_ERR_CUDA;
+}
+
+// absmax_matmul (gemm.py:150-156): never synchronizes the host
+int i8mm_absmax_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M, int64_t K,
+                       int64_t N, float* y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+    if (int s = check_device()) return s;
+    if (int s = check_inner(K)) return s;
+    if (M <= 0 || K <= 0 || N <= 0 || ldx < K || ldw < N || ldy < N || !x || !w || !y || !workspace)
+        return I8MM_ERR_ARGUMENT;
+    ScalarWs ws;
+    if (int s = scalar_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const __half* xh = static_cast<const __half*>(x);
+    const __half* wh = static_cast<const __half*>(w);
+    if (launch_tensor_stats(xh, M, K, ldx, ws.stats, ws.fstats, st)) return I8MM_ERR_CUDA;
+    if (launch_tensor_stats(wh, K, N, ldw, ws.stats + 4, ws.fstats + 4, st)) return I8MM_ERR_CUDA;
+    if (launch_quantize_scalar(xh, M, K, ldx, 0, ws.fstats, 0.0, 0, ws.xq, ws.ldq, 0, st)) return I8MM_ERR_CUDA;
+    if (launch_quantize_scalar(wh, K, N, ldw, 0, ws.fstats + 4, 0.0, 0, ws.wq_t, ws.ldq, 1, st))
+        return I8MM_ERR_CUDA;
+    if (int s = gemm_codes(ws, M, K, N, st)) return s;
+    return cuda_status(launch_dequant_absmax(ws.c, M, N, N, ws.fstats, ws.fstats + 4, y, ldy, st));
+}
+
+// zeropoint_matmul (gemm.py:159-187). The zeropoints are validated on the host
+// exactly as quantize.py:162-166 and the int32 range as gemm.py:71-75, so this
+// entry synchronizes the stream twice (after the min/max pass and at the end).
+int i8mm_zeropoint_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M, int64_t K,
+                          int64_t N, float* y, int64_t ldy, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+    if (int s = check_device()) return s;
+    if (int s = check_inner(K)) return s;
+    if (M <= 0 || K <= 0 || N <= 0 || ldx < K || ldw < N || ldy < N || !x || !w || !y || !workspace)
+        return I8MM_ERR_ARGUMENT;
+    ScalarWs ws;
+    if (int s = scalar_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const __half* xh = static_cast<const __half*>(x);
+    const __half* wh = static_cast<const __half*>(w);
+    if (launch_tensor_stats(xh, M, K, ldx, ws.stats, ws.fstats, st)) return I8MM_ERR_CUDA;
+    if (launch_tensor_stats(wh, K, N, ldw, ws.stats + 4, ws.fstats + 4, st)) return I8MM_ERR_CUDA;
+    float h[8];
+    if (cudaMemcpyAsync(h, ws.fstats, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return I8MM_ERR_CUDA;
+    double nd_x, nd_w, off_x, off_w;
+    int32_t zp_x, zp_w;
+    if (int s = i8mm_zeropoint_params(h[1], h[2], &nd_x, &zp_x, &off_x)) return s;
+    if (int s = i8mm_zeropoint_params(h[5], h[6], &nd_w, &zp_w, &off_w)) return s;
+    if (off_x != 0.0 || h[1] == h[2]) {
+        if (cudaMemsetAsync(ws.xq, 0, static_cast<size_t>(M * ws.ldq), st) != cudaSuccess) return I8MM_ERR_CUDA;
+    } else if (launch_quantize_scalar(xh, M, K, ldx, 1, nullptr, nd_x, zp_x, ws.xq, ws.ldq, 0, st)) {
+        return I8MM_ERR_CUDA;
+    }
+    if (off_w != 0.0 || h[5] == h[6]) {
+        if (cudaMemsetAsync(ws.wq_t, 0, static_cast<size_t>(N * ws.ldq), st) != cudaSuccess) return I8MM_ERR_CUDA;
+    } else if (launch_quantize_scalar(wh, K, N, ldw, 1, nullptr, nd_w, zp_w, ws.wq_t, ws.ldq, 1, st)) {
+        return I8MM_ERR_CUDA;
+    }
+    if (int s = gemm_codes(ws, M, K, N, st)) return s;
+    if (launch_rowsum_i8(ws.xq, M, K, ws.ldq, ws.rowsum, st)) return I8MM_ERR_CUDA;
+    if (launch_rowsum_i8(ws.wq_t, N, K, ws.ldq, ws.colsum, st)) return I8MM_ERR_CUDA;
+    if (cudaMemsetAsync(ws.flag, 0, sizeof(int32_t), st) != cudaSuccess) return I8MM_ERR_CUDA;
+    if (launch_zeropoint_combine(ws.c, M, N, N, ws.rowsum, ws.colsum, K, zp_x, zp_w, nd_x, nd_w, off_x, off_w,
+                                 y, ldy, nullptr, ws.flag, st))
+        return I8MM_ERR_CUDA;
+    int32_t flag = 0;
+    if (cudaMemcpyAsync(&flag, ws.flag, sizeof(flag), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return I8MM_ERR_CUDA;
+    return flag ? I8MM_ERR_OVERFLOW : I8MM_OK;
 }
 
 }  // extern "C"

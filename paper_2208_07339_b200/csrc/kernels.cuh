@@ -47,6 +47,24 @@ cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t l
 cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int64_t lds,
                                 int8_t* dst, int64_t ldd, cudaStream_t st);
 
+// Sibling schemes (siblings.cu): tensor-wise absmax / zeropoint.
+// stats_scratch: 3 int32 (device); out3: [amax, min, max] floats (device)
+cudaError_t launch_tensor_stats(const __half* x, int64_t rows, int64_t cols, int64_t ld,
+                                int32_t* stats_scratch, float* out3, cudaStream_t st);
+// mode 0 = absmax (amax_dev), 1 = zeropoint (nd, zp); transpose writes K-major (cols x ld_out)
+cudaError_t launch_quantize_scalar(const __half* x, int64_t rows, int64_t cols, int64_t ld, int mode,
+                                   const float* amax_dev, double nd, int32_t zp, int8_t* out,
+                                   int64_t ld_out, int transpose, cudaStream_t st);
+cudaError_t launch_rowsum_i8(const int8_t* q, int64_t rows, int64_t cols, int64_t ld, int32_t* out,
+                             cudaStream_t st);
+cudaError_t launch_dequant_absmax(const int32_t* c, int64_t M, int64_t N, int64_t ldc, const float* amax_x,
+                                  const float* amax_w, float* out, int64_t ldo, cudaStream_t st);
+cudaError_t launch_zeropoint_combine(const int32_t* c, int64_t M, int64_t N, int64_t ldc,
+                                     const int32_t* rowsum_a, const int32_t* colsum_b, int64_t K,
+                                     int32_t zp_a, int32_t zp_b, double nd_a, double nd_b, double off_a,
+                                     double off_b, float* out, int64_t ldo, int32_t* acc_out,
+                                     int32_t* overflow, cudaStream_t st);
+
 // Output kinds of the tcgen05 GEMM epilogue.
 enum EpiKind : int { EPI_I32 = 0, EPI_F16 = 1, EPI_F32 = 2, EPI_F32_EXACT = 3 };
 

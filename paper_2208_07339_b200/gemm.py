@@ -13,6 +13,11 @@ Operator map (reference -> kernels):
   vectorwise_matmul        gemm.py:197-200 -> K2 + K3 + K4 (fused dequant)
   llm_int8_matmul          gemm.py:214-247 -> K1 + K2 + K3 + K4 (fused dequant
                                               + outlier term in the epilogue)
+  absmax_matmul            gemm.py:150-156 -> tensor stats + scalar quantizers
+                                              + K4 (int32) + f64 dequant
+  zeropoint_gemm_i32       gemm.py:85-104  -> K4 (int32) + row sums + exact
+                                              int64 zeropoint identity
+  zeropoint_matmul         gemm.py:159-187 -> the above + f64 dequant/offsets
 """
 
 from __future__ import annotations
@@ -24,14 +29,16 @@ from . import _native as nat
 from ._tensors import (as_f16_matrix, as_i8_matrix, check_inner, device, kmajor_i8, round_up,
                        stream_handle)
 from .errors import GemmOverflowError, ParamsMismatchError, ShapeMismatchError
-from .types import ColwiseParams, MatmulResult, OutlierSet, QuantizedTensor, RowwiseParams
+from .types import (AbsmaxParams, ColwiseParams, MatmulResult, OutlierSet, QuantizedTensor,
+                    RowwiseParams, ZeropointParams)
 
 MAX_INNER_DIM = 1 << 17  # gemm.py:35: 127^2 * 2^17 < 2^31
 
 __all__ = [
     "MAX_INNER_DIM", "GemmOverflowError", "ParamsMismatchError", "ShapeMismatchError",
     "MatmulResult", "extract_outlier_columns", "int8_gemm_i32", "dequantize_output",
-    "vectorwise_matmul", "llm_int8_matmul",
+    "vectorwise_matmul", "llm_int8_matmul", "absmax_matmul", "zeropoint_matmul",
+    "zeropoint_gemm_i32",
 ]
 
 OUT_KINDS = {torch.float16: nat.OUT_F16, torch.float32: nat.OUT_F32}
@@ -152,12 +159,10 @@ def int8_gemm_i32(a, b) -> torch.Tensor:
 
 
 def dequantize_output(c, params_x, params_w) -> torch.Tensor:
-    """Divide an int32 accumulation by the outer product of the scales
-    (gemm.py:120-147, row x col branch), exactly as the reference: f32 of the
-    f64 quotient. Tensor-wise / zeropoint params are out of scope here."""
-    if not (isinstance(params_x, RowwiseParams) and isinstance(params_w, ColwiseParams)):
-        raise ParamsMismatchError(
-            f"unsupported params pairing: {type(params_x).__name__} x {type(params_w).__name__}")
+    """Divide an int32 accumulation by the operands' scaling constants
+    (gemm.py:120-147), exactly as the reference: f32 of the f64 quotient.
+    Tensor-wise params divide by the scalar product, zeropoint params by
+    nd_x * nd_w, row x col params by the outer product of the scale vectors."""
     if isinstance(c, torch.Tensor):
         ct = c
     else:
@@ -165,12 +170,24 @@ def dequantize_output(c, params_x, params_w) -> torch.Tensor:
     dev = device()
     ct = ct.to(device=dev, dtype=torch.int32).contiguous()
     m, n = ct.shape
-    if params_x.size != m or params_w.size != n:
+    if isinstance(params_x, AbsmaxParams) and isinstance(params_w, AbsmaxParams):
+        sx_h = np.full(m, params_x.scale, dtype=np.float64)
+        sw_h = np.full(n, params_w.scale, dtype=np.float64)
+    elif isinstance(params_x, ZeropointParams) and isinstance(params_w, ZeropointParams):
+        sx_h = np.full(m, params_x.nd, dtype=np.float64)
+        sw_h = np.full(n, params_w.nd, dtype=np.float64)
+    elif isinstance(params_x, RowwiseParams) and isinstance(params_w, ColwiseParams):
+        if params_x.size != m or params_w.size != n:
+            raise ParamsMismatchError(
+                f"scale vector lengths ({params_x.size}, {params_w.size}) "
+                f"do not match output shape {(m, n)}")
+        sx_h, sw_h = params_x.scales, params_w.scales
+    else:
         raise ParamsMismatchError(
-            f"scale vector lengths ({params_x.size}, {params_w.size}) "
-            f"do not match output shape {(m, n)}")
-    sx = torch.from_numpy(np.ascontiguousarray(params_x.scales)).to(dev)
-    sw = torch.from_numpy(np.ascontiguousarray(params_w.scales)).to(dev)
+            f"unsupported params pairing: {type(params_x).__name__} x {type(params_w).__name__}")
+    # the same f64 op order for every branch: q = c / (s_x[i] * s_w[j])
+    sx = torch.from_numpy(np.array(sx_h, dtype=np.float64)).to(dev)
+    sw = torch.from_numpy(np.array(sw_h, dtype=np.float64)).to(dev)
     out = torch.empty((m, n), dtype=torch.float32, device=dev)
     nat.check(nat.lib().i8mm_dequantize_output(ct.data_ptr(), m, n, n, sx.data_ptr(),
                                                sw.data_ptr(), out.data_ptr(), n,
@@ -290,3 +307,118 @@ def llm_int8_trace(x, w, alpha: float = 6.0) -> dict:
     yex = _gemm_dequant(xq, wq_t, ldq, m, n, k, ax, aw, x16, w16, xo, scan, None, True, wo)
     return {"scan": scan, "xq": xq[:, :k], "row_amax": ax, "wq_t": wq_t[:, :k], "col_amax": aw,
             "c": c, "y16": y16, "y32": y32, "y_exact": yex, "xo": xo}
+
+
+# ---------------------------------------------------------------- sibling schemes
+def _stats(t16: torch.Tensor) -> torch.Tensor:
+    """[max|x|, min x, max x] of an fp16 matrix, on the device (one pass)."""
+    rows, cols = t16.shape
+    scratch = torch.empty((4,), dtype=torch.int32, device=t16.device)
+    out = torch.empty((4,), dtype=torch.float32, device=t16.device)
+    nat.check(nat.lib().i8mm_tensor_stats(t16.data_ptr(), rows, cols, t16.stride(0),
+                                          scratch.data_ptr(), out.data_ptr(), stream_handle()),
+              "tensor_stats")
+    return out
+
+
+def _absmax_codes(t16: torch.Tensor, transpose: bool):
+    """absmax codes (quantize.py:137-151) row-major (rows x ldq) or K-major."""
+    rows, cols = t16.shape
+    st = _stats(t16)
+    ld = round_up(rows if transpose else cols, 16)
+    codes = torch.empty((cols if transpose else rows, ld), dtype=torch.int8, device=t16.device)
+    nat.check(nat.lib().i8mm_absmax_quantize(t16.data_ptr(), rows, cols, t16.stride(0),
+                                             st.data_ptr(), codes.data_ptr(), ld, int(transpose),
+                                             stream_handle()), "absmax_quantize")
+    return codes, st[0:1]
+
+
+def _zeropoint_params(st: torch.Tensor) -> ZeropointParams:
+    import ctypes
+
+    lo, hi = (float(v) for v in st[1:3].cpu().tolist())
+    nd, zp, off = ctypes.c_double(), ctypes.c_int32(), ctypes.c_double()
+    nat.check(nat.lib().i8mm_zeropoint_params(lo, hi, ctypes.byref(nd), ctypes.byref(zp),
+                                              ctypes.byref(off)), "zeropoint_quantize")
+    return ZeropointParams(nd=nd.value, zp=int(zp.value), offset=off.value)
+
+
+def _zeropoint_codes(t16: torch.Tensor, transpose: bool):
+    """zeropoint codes (quantize.py:153-171); params validated on the host."""
+    rows, cols = t16.shape
+    params = _zeropoint_params(_stats(t16))
+    ld = round_up(rows if transpose else cols, 16)
+    if params.offset != 0.0:  # constant tensor: its value rides in the offset, codes 0
+        codes = torch.zeros((cols if transpose else rows, ld), dtype=torch.int8, device=t16.device)
+        return codes, params
+    codes = torch.empty((cols if transpose else rows, ld), dtype=torch.int8, device=t16.device)
+    nat.check(nat.lib().i8mm_zeropoint_quantize(t16.data_ptr(), rows, cols, t16.stride(0),
+                                                float(params.nd), int(params.zp), codes.data_ptr(),
+                                                ld, int(transpose), stream_handle()),
+              "zeropoint_quantize")
+    return codes, params
+
+
+def zeropoint_gemm_i32(a, b, zp_a: int, zp_b: int, unrolled: bool = False) -> torch.Tensor:
+    """Integer product of zeropoint-shifted codes (A + zp_a)(B + zp_b)
+    (gemm.py:85-104). Computed as the unrolled identity
+    A@B + zp_b*rowsum(A) + zp_a*colsum(B) + h*zp_a*zp_b in exact int64 (the
+    direct and unrolled forms are bit-identical); GemmOverflowError when a
+    result leaves int32 (gemm.py:71-75). One host sync for the range flag."""
+    a = as_i8_matrix(a, "A")
+    b = as_i8_matrix(b, "B")
+    m, k = a.shape
+    k2, n = b.shape
+    check_inner(k, k2, f"A is {m}x{k}, B is {k2}x{n}")
+    c = int8_gemm_i32(a, b)
+    L = nat.lib()
+    st = stream_handle()
+    a_buf, lda = kmajor_i8(a)
+    bt = b.t().contiguous()
+    ra = torch.empty((m,), dtype=torch.int32, device=a.device)
+    cb = torch.empty((n,), dtype=torch.int32, device=a.device)
+    nat.check(L.i8mm_rowsum_i8(a_buf.data_ptr(), m, k, lda, ra.data_ptr(), st), "rowsum")
+    nat.check(L.i8mm_rowsum_i8(bt.data_ptr(), n, k, k, cb.data_ptr(), st), "colsum")
+    flag = torch.zeros((1,), dtype=torch.int32, device=a.device)
+    acc = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    nat.check(L.i8mm_zeropoint_combine(c.data_ptr(), m, n, n, ra.data_ptr(), cb.data_ptr(), k,
+                                       int(zp_a), int(zp_b), 1.0, 1.0, 0.0, 0.0, None, 0,
+                                       acc.data_ptr(), flag.data_ptr(), st), "zeropoint_combine")
+    if int(flag.item()):
+        raise GemmOverflowError("accumulated values exceed the signed 32-bit range")
+    return acc
+
+
+def absmax_matmul(x, w) -> MatmulResult:
+    """X @ W via tensor-wise absmax quantization of both operands
+    (gemm.py:150-156); float32 output, no host synchronisation."""
+    x16 = as_f16_matrix(x, "x")
+    w16 = as_f16_matrix(w, "w")
+    (m, k), (k2, n) = x16.shape, w16.shape
+    check_inner(k, k2, f"X is {m}x{k}, W is {k2}x{n}")
+    L = nat.lib()
+    ws = torch.empty(L.i8mm_scalar_workspace_size(m, k, n), dtype=torch.uint8, device=x16.device)
+    y = torch.empty((m, n), dtype=torch.float32, device=x16.device)
+    nat.check(L.i8mm_absmax_matmul(x16.data_ptr(), x16.stride(0), w16.data_ptr(), w16.stride(0),
+                                   m, k, n, y.data_ptr(), n, ws.data_ptr(), ws.numel(),
+                                   stream_handle()), "absmax_matmul")
+    return MatmulResult(y, "absmax", None, k)
+
+
+def zeropoint_matmul(x, w, unrolled: bool = False) -> MatmulResult:
+    """X @ W via tensor-wise zeropoint quantization of both operands
+    (gemm.py:159-187), including the constant-tensor offset terms; float32
+    output. ``unrolled`` selects between two bit-identical forms in the
+    reference and is accepted for API parity. Synchronises the stream (the
+    zeropoints are validated on the host like quantize.py:162-166)."""
+    x16 = as_f16_matrix(x, "x")
+    w16 = as_f16_matrix(w, "w")
+    (m, k), (k2, n) = x16.shape, w16.shape
+    check_inner(k, k2, f"X is {m}x{k}, W is {k2}x{n}")
+    L = nat.lib()
+    ws = torch.empty(L.i8mm_scalar_workspace_size(m, k, n), dtype=torch.uint8, device=x16.device)
+    y = torch.empty((m, n), dtype=torch.float32, device=x16.device)
+    nat.check(L.i8mm_zeropoint_matmul(x16.data_ptr(), x16.stride(0), w16.data_ptr(),
+                                      w16.stride(0), m, k, n, y.data_ptr(), n, ws.data_ptr(),
+                                      ws.numel(), stream_handle()), "zeropoint_matmul")
+    return MatmulResult(y, "zeropoint", None, k)

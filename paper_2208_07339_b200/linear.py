@@ -16,7 +16,8 @@ import torch
 from . import _native as nat
 from ._tensors import as_f16_matrix, stream_handle
 from .errors import ShapeMismatchError
-from .gemm import _out_kind, llm_int8_matmul, vectorwise_matmul
+from .gemm import (_out_kind, absmax_matmul, llm_int8_matmul, vectorwise_matmul,
+                   zeropoint_matmul)
 
 BACKEND_KINDS = ("exact", "absmax", "zeropoint", "vectorwise", "llm_int8")
 
@@ -49,9 +50,9 @@ def llm_int8_backend(alpha: float = 6.0) -> LinearBackend:
 def linear(x, w, backend: LinearBackend, out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
     """x @ w through the selected backend (transformer.py:257-267).
 
-    The reference returns float32; ``out_dtype`` defaults to that. ``absmax``
-    and ``zeropoint`` are sibling schemes outside this build's scope
-     and raise ``NotImplementedError``.
+    The reference returns float32; ``out_dtype`` defaults to that (the
+    tensor-wise ``absmax`` / ``zeropoint`` schemes compute in float32 and are
+    cast when another dtype is requested).
     """
     if backend.kind == "exact":
         x16 = as_f16_matrix(x, "x")
@@ -61,8 +62,11 @@ def linear(x, w, backend: LinearBackend, out_dtype: torch.dtype = torch.float32)
         return vectorwise_matmul(x, w, out_dtype=out_dtype, validate=False).output
     if backend.kind == "llm_int8":
         return llm_int8_matmul(x, w, backend.alpha, out_dtype=out_dtype, validate=False).output
-    raise NotImplementedError(
-        f"backend {backend.kind!r} is not part of the B200 LLM.int8() path (SURVEY.md 8f)")
+    if backend.kind == "absmax":
+        return absmax_matmul(x, w).output.to(out_dtype)
+    if backend.kind == "zeropoint":
+        return zeropoint_matmul(x, w).output.to(out_dtype)
+    raise ValueError(f"backend kind must be one of {BACKEND_KINDS}, got {backend.kind!r}")
 
 
 _linear = linear

@@ -3,6 +3,8 @@
 * ``OutlierSet``      -- outliers.py:27-50
 * ``RowwiseParams``   -- quantize.py:74-81 (scales = 127/amax per row, f64)
 * ``ColwiseParams``   -- quantize.py:84-91 (scales = 127/amax per column, f64)
+* ``AbsmaxParams``    -- quantize.py:32-41 (tensor-wise scale)
+* ``ZeropointParams`` -- quantize.py:44-61 (nd, zp, offset)
 * ``QuantizedTensor`` -- quantize.py:97-112
 * ``MatmulResult``    -- gemm.py:49-60
 
@@ -102,12 +104,46 @@ class ColwiseParams(_VectorParams):
     _what = "column scales"
 
 
+ZP_INT16_MIN = -(1 << 15)  # quantize.py:22-23
+ZP_INT16_MAX = (1 << 15) - 1
+
+
+@dataclass(frozen=True)
+class AbsmaxParams:
+    """Tensor-wise symmetric scale: codes = round(scale * x), scale = 127 / max|x|
+    (quantize.py:32-41)."""
+
+    scale: float
+
+    def __post_init__(self) -> None:
+        if not np.isfinite(self.scale) or self.scale <= 0:
+            raise ValueError(f"scale must be positive and finite, got {self.scale}")
+
+
+@dataclass(frozen=True)
+class ZeropointParams:
+    """Affine scale/shift: stored code = round(nd * x) - zp, zp a 16-bit integer;
+    ``offset`` carries a constant tensor's value (quantize.py:44-61)."""
+
+    nd: float
+    zp: int
+    offset: float = 0.0
+
+    def __post_init__(self) -> None:
+        if not np.isfinite(self.nd) or self.nd <= 0:
+            raise ValueError(f"nd must be positive and finite, got {self.nd}")
+        if not (ZP_INT16_MIN <= self.zp <= ZP_INT16_MAX):
+            raise ValueError(f"zeropoint {self.zp} outside the signed 16-bit range")
+        if not np.isfinite(self.offset):
+            raise ValueError("offset must be finite")
+
+
 @dataclass(frozen=True, eq=False)
 class QuantizedTensor:
     """Int8 codes with the constants that dequantize them (quantize.py:97-112)."""
 
     codes: torch.Tensor
-    params: RowwiseParams | ColwiseParams
+    params: RowwiseParams | ColwiseParams | AbsmaxParams | ZeropointParams
 
     def __post_init__(self) -> None:
         if isinstance(self.params, RowwiseParams) and self.params.size != self.codes.shape[0]:

@@ -258,8 +258,8 @@ def test_int8_linear_module(p, oracle_mod):
     # the backend plugin point (transformer.py:257-267)
     y2 = p.linear(x, w, p.llm_int8_backend(6.0))
     assert y2.dtype == torch.float32
-    with pytest.raises(NotImplementedError):
-        p.linear(x, w, p.ABSMAX)
+    for kind in ("absmax", "zeropoint", "vectorwise", "exact"):  # every BACKEND_KINDS entry
+        assert p.linear(x, w, p.LinearBackend(kind)).shape == (64, 256)
 
 
 def test_capi_pipeline_entry(p, oracle_mod):
@@ -504,3 +504,80 @@ def test_decode_split_entries_carry_alpha(p, oracle_mod, decode_max, alpha):
     assert torch.equal(y_fwd, y_split)
     assert lin.last_stats()["decomposed_cols"] == len(ref.dims)
     assert (np.abs(_np(y_fwd).astype(np.float64) - ref.output) <= _golden.fp16_tolerance(ref.output)).all()
+
+
+# ---------------------------------------------------------------- sibling schemes
+def _sib():
+    from pathlib import Path
+
+    d = np.load(Path(__file__).resolve().parent / "golden" / "siblings_cases.npz")
+    return d, [str(n) for n in d["names"]]
+
+
+def test_sibling_quantizers_match_reference_goldens(p):
+    """absmax_quantize / zeropoint_quantize on the GPU vs the reference's codes
+    and params (quantize.py:137-171), bit-exact, incl. the int16 range error."""
+    d, names = _sib()
+    for name in names:
+        for tag in ("x", "w"):
+            t = d[f"{name}/{tag}"]
+            qa = p.absmax_quantize(t)
+            assert np.array_equal(_np(qa.codes), d[f"{name}/abs_{tag}_codes"]), (name, tag)
+            assert qa.params.scale == float(d[f"{name}/abs_{tag}_scale"])
+            if f"{name}/zp_{tag}_error" in d:
+                with pytest.raises(ValueError):
+                    p.zeropoint_quantize(t)
+                continue
+            qz = p.zeropoint_quantize(t)
+            assert np.array_equal(_np(qz.codes), d[f"{name}/zp_{tag}_codes"]), (name, tag)
+            assert [qz.params.nd, qz.params.zp, qz.params.offset] == \
+                d[f"{name}/zp_{tag}_params"].tolist(), (name, tag)
+
+
+def test_sibling_matmuls_match_reference_goldens(p):
+    """absmax_matmul / zeropoint_gemm_i32 / zeropoint_matmul vs the reference
+    (gemm.py:85-104, 150-187): float32 outputs and int32 accumulators
+    bit-identical; GemmOverflowError / ValueError where the reference raises."""
+    d, names = _sib()
+    for name in names:
+        x, w = d[f"{name}/x"], d[f"{name}/w"]
+        assert np.array_equal(_np(p.absmax_matmul(x, w).output), d[f"{name}/abs_out"]), name
+        assert np.array_equal(_np(p.linear(x, w, p.ABSMAX)), d[f"{name}/abs_out"]), name
+        if f"{name}/zp_out" in d:
+            for unrolled in (False, True):
+                r = p.zeropoint_matmul(x, w, unrolled=unrolled)
+                assert r.scheme == "zeropoint"
+                assert np.array_equal(_np(r.output), d[f"{name}/zp_out"]), name
+            qx, qw = p.zeropoint_quantize(x), p.zeropoint_quantize(w)
+            c = p.zeropoint_gemm_i32(qx.codes, qw.codes, qx.params.zp, qw.params.zp)
+            assert np.array_equal(_np(c), d[f"{name}/zp_c"]), name
+            # dequantize_output's zeropoint branch = c / (nd_x * nd_w) (gemm.py:135)
+            if qx.params.offset == 0.0 and qw.params.offset == 0.0:
+                assert np.array_equal(_np(p.dequantize_output(c, qx.params, qw.params)),
+                                      d[f"{name}/zp_out"]), name
+        elif int(d[f"{name}/zp_out_error"]) == 2:
+            with pytest.raises(p.GemmOverflowError):
+                p.zeropoint_matmul(x, w)
+            qx, qw = p.zeropoint_quantize(x), p.zeropoint_quantize(w)
+            with pytest.raises(p.GemmOverflowError):
+                p.zeropoint_gemm_i32(qx.codes, qw.codes, qx.params.zp, qw.params.zp)
+        else:
+            with pytest.raises(ValueError):
+                p.zeropoint_matmul(x, w)
+        qa, qb = p.absmax_quantize(x), p.absmax_quantize(w)
+        c = p.int8_gemm_i32(qa.codes, qb.codes)
+        assert np.array_equal(_np(p.dequantize_output(c, qa.params, qb.params)),
+                              d[f"{name}/abs_out"]), name
+        with pytest.raises(p.ParamsMismatchError):  # mixed pairing (gemm.py:143-146)
+            p.dequantize_output(c, qa.params, p.rowwise_quantize(x).params)
+
+
+@pytest.mark.parametrize("shape", [(300, 1000, 700), (2048, 1024, 512), (1, 4096, 384)])
+def test_sibling_matmuls_large_vs_oracle(p, oracle_mod, shape):
+    """Larger shapes (CTA-pair GEMM, ragged edges) vs the numpy restatement."""
+    m, k, n = shape
+    rng = np.random.Generator(np.random.PCG64(m + k + n))
+    x = (rng.standard_normal((m, k)) * 2 + 0.3).astype(np.float16).astype(np.float32)
+    w = (rng.standard_normal((k, n)) * 0.2).astype(np.float16).astype(np.float32)
+    assert np.array_equal(_np(p.absmax_matmul(x, w).output), oracle_mod.absmax_matmul(x, w))
+    assert np.array_equal(_np(p.zeropoint_matmul(x, w).output), oracle_mod.zeropoint_matmul(x, w))

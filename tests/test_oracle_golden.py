@@ -8,6 +8,7 @@ bit-exact against outputs produced by the reference package itself
 from __future__ import annotations
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -105,3 +106,72 @@ def test_cfg1_digest_c_oracle(oracle_mod):
     assert sha(tr.c) == dig["sha256"]["c"]
     assert sha(tr.output) == dig["sha256"]["out"]
     assert np.array_equal(tr.output[dig["sample_rows"]], sample)
+
+
+# ---------------------------------------------------------------- sibling schemes
+SIB = Path(__file__).resolve().parent / "golden" / "siblings_cases.npz"
+
+
+def _sib_cases():
+    d = np.load(SIB)
+    return d, [str(n) for n in d["names"]]
+
+
+def test_oracle_siblings_match_reference_goldens():
+    """absmax / zeropoint restatements vs the reference's own outputs
+    (tests/golden/make_golden_siblings.py), bit-exact."""
+    from oracle import oracle as orc
+
+    d, names = _sib_cases()
+    assert len(names) >= 12
+    for name in names:
+        x = d[f"{name}/x"].astype(np.float32)
+        w = d[f"{name}/w"].astype(np.float32)
+        for tag, mat in (("x", x), ("w", w)):
+            codes, scale = orc.absmax_quantize(mat)
+            assert np.array_equal(codes, d[f"{name}/abs_{tag}_codes"]), (name, tag)
+            assert scale == float(d[f"{name}/abs_{tag}_scale"]), (name, tag)
+            if f"{name}/zp_{tag}_error" in d:
+                with pytest.raises(ValueError):
+                    orc.zeropoint_quantize(mat)
+            else:
+                codes, nd, zp, off = orc.zeropoint_quantize(mat)
+                assert np.array_equal(codes, d[f"{name}/zp_{tag}_codes"]), (name, tag)
+                assert [nd, zp, off] == d[f"{name}/zp_{tag}_params"].tolist(), (name, tag)
+        assert np.array_equal(orc.absmax_matmul(x, w), d[f"{name}/abs_out"]), name
+        if f"{name}/zp_out" in d:
+            assert np.array_equal(orc.zeropoint_matmul(x, w), d[f"{name}/zp_out"]), name
+            qx, _, zpx, _ = orc.zeropoint_quantize(x)
+            qw, _, zpw, _ = orc.zeropoint_quantize(w)
+            assert np.array_equal(orc.zeropoint_gemm_i32(qx, qw, zpx, zpw), d[f"{name}/zp_c"]), name
+        elif int(d[f"{name}/zp_out_error"]) == 2:
+            with pytest.raises(OverflowError):
+                orc.zeropoint_matmul(x, w)
+        else:
+            with pytest.raises(ValueError):
+                orc.zeropoint_matmul(x, w)
+
+
+def test_host_zeropoint_params_match_reference():
+    """i8mm_zeropoint_params (host C, no GPU) reproduces the reference's
+    nd / zp / offset and its int16 range error (quantize.py:153-166)."""
+    import ctypes
+
+    from paper_2208_07339_b200 import _native as nat
+
+    L = nat.load_library()
+    d, names = _sib_cases()
+    seen_error = False
+    for name in names:
+        for tag in ("x", "w"):
+            t = d[f"{name}/{tag}"].astype(np.float32)
+            nd, zp, off = ctypes.c_double(), ctypes.c_int32(), ctypes.c_double()
+            st = L.i8mm_zeropoint_params(float(t.min()), float(t.max()), ctypes.byref(nd),
+                                         ctypes.byref(zp), ctypes.byref(off))
+            if f"{name}/zp_{tag}_error" in d:
+                assert st == nat.I8MM_ERR_ZEROPOINT, (name, tag)
+                seen_error = True
+            else:
+                assert st == 0
+                assert [nd.value, zp.value, off.value] == d[f"{name}/zp_{tag}_params"].tolist(), (name, tag)
+    assert seen_error
