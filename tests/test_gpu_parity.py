@@ -581,3 +581,24 @@ def test_sibling_matmuls_large_vs_oracle(p, oracle_mod, shape):
     w = (rng.standard_normal((k, n)) * 0.2).astype(np.float16).astype(np.float32)
     assert np.array_equal(_np(p.absmax_matmul(x, w).output), oracle_mod.absmax_matmul(x, w))
     assert np.array_equal(_np(p.zeropoint_matmul(x, w).output), oracle_mod.zeropoint_matmul(x, w))
+
+
+def test_qt8_roundtrip_through_device_pipeline(p, oracle_mod, tmp_path):
+    """Golden-vector I/O on the device: QT8 files (reference format, qt8.py)
+    load straight into CUDA tensors that feed the LLM.int8() path, and the
+    int32 / float32 results round-trip bit-exactly."""
+    from paper_2208_07339_b200 import qt8
+
+    x, w = oracle_mod.planted_pair(48, 256, 40, 3, 20.0, 6)
+    x = x.astype(np.float16).astype(np.float32)
+    w = w.astype(np.float16).astype(np.float32)
+    qt8.write_tensor(tmp_path / "x.qt8", x)
+    qt8.write_tensor(tmp_path / "w.qt8", w)
+    xd = qt8.read_tensor(tmp_path / "x.qt8")
+    assert xd.is_cuda and xd.dtype == torch.float32
+    tr = p.gemm.llm_int8_trace(xd, qt8.read_tensor(tmp_path / "w.qt8"), 6.0)
+    ref = oracle_mod.llm_int8_matmul(x, w, 6.0)
+    qt8.write_tensor(tmp_path / "c.qt8", tr["c"])
+    qt8.write_tensor(tmp_path / "y.qt8", tr["y_exact"])
+    assert np.array_equal(_np(qt8.read_tensor(tmp_path / "c.qt8")), ref.c)
+    assert np.array_equal(_np(qt8.read_tensor(tmp_path / "y.qt8")), ref.output)

@@ -159,3 +159,30 @@ def test_nshard_allgather_gloo_world2():
         pr.join(timeout=120)
     results = sorted(q.get(timeout=5) for _ in range(world))
     assert results == [(0, True), (1, True)]
+
+
+def test_qt8_mirror_matches_reference_files(tmp_path):
+    """QT8 reader/writer vs files written by the reference (qt8.py:65-107):
+    identical bytes on re-write, identical error classes on malformed files."""
+    import numpy as np
+    import torch
+
+    from paper_2208_07339_b200 import qt8
+
+    gold = Path(__file__).resolve().parent / "golden" / "qt8"
+    for name, dt in (("f32", torch.float32), ("i8", torch.int8), ("i32", torch.int32)):
+        t = qt8.read_tensor(gold / f"{name}.qt8", device="cpu")
+        assert t.dtype == dt and t.ndim == 2
+        qt8.write_tensor(tmp_path / f"{name}.qt8", t)
+        assert (tmp_path / f"{name}.qt8").read_bytes() == (gold / f"{name}.qt8").read_bytes()
+    # fp16 tensors widen to f32 exactly
+    h = torch.tensor([[1.5, -2.25]], dtype=torch.float16)
+    qt8.write_tensor(tmp_path / "h.qt8", h)
+    assert torch.equal(qt8.read_tensor(tmp_path / "h.qt8", device="cpu"), h.float())
+    for bad, exc in (("bad_magic", qt8.BadMagicError), ("bad_version", qt8.UnsupportedVersionError),
+                     ("bad_dtype", qt8.UnknownDtypeError), ("short_header", qt8.TruncatedFileError),
+                     ("short_payload", qt8.TruncatedFileError), ("trailing", qt8.QT8Error)):
+        with pytest.raises(exc):
+            qt8.read_tensor(gold / f"{bad}.qt8", device="cpu")
+    with pytest.raises(TypeError):
+        qt8.write_tensor(tmp_path / "x.qt8", np.zeros((2, 2), dtype=np.float64))
