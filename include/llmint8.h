@@ -154,6 +154,16 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
 int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
                      const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
                      void* workspace, size_t workspace_bytes, void* stream);
+/* GEMM + epilogue over rows [row0, row0 + rows) only, after one
+ * i8mm_linear_prologue over all M rows (same workspace; y is the full output,
+ * rows outside the range are untouched). Rows are independent once O and the
+ * row scales are known (gemm.py:210, 242), so a caller can pipeline output
+ * transfers (all-gather, device-to-host) behind later row ranges. Prefill
+ * routing only (decode calls are a single launch: row0 = 0, rows = M). */
+int i8mm_linear_gemm_rows(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                          const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
+                          void* workspace, size_t workspace_bytes, int64_t row0, int64_t rows,
+                          void* stream);
 /* prologue + gemm; *o_count_dev (nullable) receives |O| */
 int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
                         const void* wbuf, int64_t K, int64_t N, float alpha, void* y, int64_t ldy,

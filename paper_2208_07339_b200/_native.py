@@ -53,6 +53,7 @@ EXPORTED_SYMBOLS = (
     "i8mm_linear_workspace_size",
     "i8mm_linear_prologue",
     "i8mm_linear_gemm",
+    "i8mm_linear_gemm_rows",
     "i8mm_linear_forward",
     "i8mm_linear_workspace_views",
     "i8mm_linear_weight_views",
@@ -106,6 +107,8 @@ def _declare(lib: ctypes.CDLL) -> None:
                                  I32),
         "i8mm_linear_gemm": ([P, I64, I64, P, I64, P, I64, I64, P, I64, I32, P, ctypes.c_size_t,
                               P], I32),
+        "i8mm_linear_gemm_rows": ([P, I64, I64, P, I64, P, I64, I64, P, I64, I32, P,
+                                   ctypes.c_size_t, I64, I64, P], I32),
         "i8mm_linear_forward": ([P, I64, I64, P, I64, P, I64, I64, F32, P, I64, I32, P,
                                  ctypes.c_size_t, P, P], I32),
         "i8mm_linear_workspace_views": ([P, I64, I64, I64, P, I32], I32),

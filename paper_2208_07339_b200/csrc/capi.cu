@@ -537,45 +537,51 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
     return I8MM_OK;
 }
 
-int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
-                     const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
-                     void* workspace, size_t workspace_bytes, void* stream) {
+// GEMM + epilogue over rows [row0, row0 + rows) of a prologue's workspace
+// (rows are independent once O and the row scales are known, gemm.py:210, 242)
+static int linear_gemm_rows_impl(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                                 const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy,
+                                 int out_kind, void* workspace, size_t workspace_bytes, int64_t row0,
+                                 int64_t rows, void* stream) {
     if (int s = check_device()) return s;
     if (M <= 0 || K <= 0 || N <= 0 || ldy < N || !y || !wbuf || !workspace) return I8MM_ERR_ARGUMENT;
+    if (row0 < 0 || rows < 0 || row0 + rows > M) return I8MM_ERR_ARGUMENT;
     Workspace ws;
     if (int s = linear_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
     const WeightBuf b = carve_weight(
         reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)), K, N);
-    int epi;
+    int epi, elt;
     switch (out_kind) {
-        case I8MM_OUT_F16: epi = EPI_F16; break;
-        case I8MM_OUT_F32: epi = EPI_F32; break;
-        case I8MM_OUT_F32_EXACT: epi = EPI_F32_EXACT; break;
+        case I8MM_OUT_F16: epi = EPI_F16; elt = 2; break;
+        case I8MM_OUT_F32: epi = EPI_F32; elt = 4; break;
+        case I8MM_OUT_F32_EXACT: epi = EPI_F32_EXACT; elt = 4; break;
         default: return I8MM_ERR_ARGUMENT;
     }
     if (ws.decode) {
+        if (row0 != 0 || rows != M) return I8MM_ERR_ARGUMENT;  // one launch for the whole call
         DecodeArgs d = decode_args(ws, b, static_cast<const __half*>(x), ldx, M, K,
                                    static_cast<const __half*>(w), ldw, N, 6.0f, y, ldy);
         d.thr_bits_dev = ws.thr_word;
         return cuda_status(launch_decode(d, epi, static_cast<cudaStream_t>(stream)));
     }
+    if (rows == 0) return I8MM_OK;
     GemmArgs g{};
-    g.a = ws.xq;
+    g.a = ws.xq + row0 * ws.ldq;
     g.lda = ws.ldq;
     g.b = b.wq_t;
     g.ldb = b.ldq;
-    g.M = M;
+    g.M = rows;
     g.N = N;
     g.K = K;
-    g.y = y;
+    g.y = static_cast<char*>(y) + row0 * ldy * elt;
     g.ldy = ldy;
-    g.row_amax = ws.row_amax;
+    g.row_amax = ws.row_amax + row0;
     g.col_amax = b.col_amax;
-    g.x = static_cast<const __half*>(x);
+    g.x = static_cast<const __half*>(x) + row0 * ldx;
     g.ldx = ldx;
     g.w = static_cast<const __half*>(w);
     g.ldw = ldw;
-    g.xo = ws.xo;
+    g.xo = ws.xo + row0 * ws.o_cap;
     g.o_cap = ws.o_cap;
     g.o_idx = ws.o_idx;
     g.o_count = ws.o_count;
@@ -592,6 +598,21 @@ int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (launch_gemm_sm100(g, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
     return I8MM_OK;
+}
+
+int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                     const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    return linear_gemm_rows_impl(x, ldx, M, w, ldw, wbuf, K, N, y, ldy, out_kind, workspace,
+                                 workspace_bytes, 0, M, stream);
+}
+
+int i8mm_linear_gemm_rows(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                          const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
+                          void* workspace, size_t workspace_bytes, int64_t row0, int64_t rows,
+                          void* stream) {
+    return linear_gemm_rows_impl(x, ldx, M, w, ldw, wbuf, K, N, y, ldy, out_kind, workspace,
+                                 workspace_bytes, row0, rows, stream);
 }
 
 int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,

@@ -154,6 +154,57 @@ class Int8Linear(torch.nn.Module):
         self._last_ws = (ws, m)
         return y
 
+    def uses_decode(self, m: int) -> bool:
+        """True when an M-row call runs the single-launch decode kernel."""
+        k, n = self.weight.shape
+        return self.weight_stationary and bool(nat.lib().i8mm_linear_uses_decode(m, k, n))
+
+    def matmul_rows(self, x2: torch.Tensor, bounds, on_rows=None, y: torch.Tensor | None = None,
+                    ldy: int | None = None) -> torch.Tensor:
+        """Y = x2 @ W with the GEMM issued per row range.
+
+        One prologue over all M rows (the outlier set and the row scales need
+        every row, gemm.py:210, 242), then ``i8mm_linear_gemm_rows`` for each
+        ``(r0, r1)`` in ``bounds``; ``on_rows(r0, r1, y)`` runs on the host
+        after each range is enqueued, so a caller can start that range's
+        transfer (all-gather, device-to-host copy) on another stream while the
+        next range computes. ``y`` / ``ldy`` let the caller supply a wider
+        (padded) output buffer. Results are bitwise those of ``matmul``.
+        """
+        if not self.weight_stationary or self.uses_decode(x2.shape[0]):
+            out = self.matmul(x2)
+            if y is not None:
+                y[:, : out.shape[1]].copy_(out)
+                out = y
+            if on_rows is not None:
+                on_rows(0, x2.shape[0], out)
+            return out
+        L = nat.lib()
+        k, n = self.weight.shape
+        m = x2.shape[0]
+        if x2.shape[1] != k:
+            raise ShapeMismatchError(f"inner dimensions differ: X is {m}x{x2.shape[1]}, W is {k}x{n}")
+        kind, dt = _out_kind(self.out_dtype, False)
+        ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8, device=x2.device)
+        if y is None:
+            y = torch.empty((m, n), dtype=dt, device=x2.device)
+            ldy = n
+        ldy = int(ldy if ldy is not None else y.stride(0))
+        st = stream_handle()
+        w = self.weight
+        nat.check(L.i8mm_linear_prologue(x2.data_ptr(), x2.stride(0), m, w.data_ptr(), w.stride(0),
+                                         self.wbuf.data_ptr(), k, n, self.alpha, ws.data_ptr(),
+                                         ws.numel(), st), "linear_prologue")
+        for r0, r1 in bounds:
+            nat.check(L.i8mm_linear_gemm_rows(x2.data_ptr(), x2.stride(0), m, w.data_ptr(),
+                                              w.stride(0), self.wbuf.data_ptr(), k, n, y.data_ptr(),
+                                              ldy, kind, ws.data_ptr(), ws.numel(), r0, r1 - r0, st),
+                      "linear_gemm_rows")
+            if on_rows is not None:
+                on_rows(r0, r1, y)
+        self._last_ws = (ws, m)
+        return y
+
     def last_stats(self) -> dict:
         """|O| and the patched-column count of the last weight-stationary call (syncs)."""
         if self._last_ws is None:

@@ -1,0 +1,70 @@
+"""Host-buffer execution of Int8 linear layers with the PCIe copies overlapped.
+
+The reference computes on host arrays (its DenseMatrix lives in host memory);
+a drop-in caller hands host buffers in and expects host buffers back. Doing
+that naively serialises host->device copy, compute and device->host copy.
+``HostIOPipeline`` keeps the copy engines and the tensor cores busy at once:
+
+* all inputs are copied host->device on one stream, in call order, so layer
+  i+1's input streams in while layer i computes;
+* each layer runs one prologue over all its rows, then the GEMM per row range
+  (``Int8Linear.matmul_rows``), and every finished range is copied back
+  device->host on a third stream while the next range computes. PCIe is full
+  duplex, so the two directions overlap each other as well.
+
+Results are bitwise those of ``Int8Linear.forward`` on device tensors.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .linear import Int8Linear
+from .sharded import row_ranges
+
+
+class HostIOPipeline:
+    """Run ``[(module, x_host, y_host), ...]`` with overlapped transfers.
+
+    ``x_host`` (M x K fp16) and ``y_host`` (M x N, the module's out dtype)
+    should be pinned for the copies to be asynchronous. ``run`` returns once
+    everything is enqueued; the host buffers are valid after the caller's
+    current stream is synchronised.
+    """
+
+    def __init__(self, device=None, chunks: int = 4) -> None:
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.chunks = int(chunks)
+        self.h2d = torch.cuda.Stream(device=self.device)
+        self.d2h = torch.cuda.Stream(device=self.device)
+
+    def run(self, calls: list[tuple[Int8Linear, torch.Tensor, torch.Tensor]]) -> None:
+        compute = torch.cuda.current_stream(self.device)
+        self.h2d.wait_stream(compute)  # host buffers may be rewritten after the last sync
+        staged = []
+        with torch.cuda.stream(self.h2d):
+            for _, xh, _ in calls:
+                xd = xh.to(self.device, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.h2d)
+                staged.append((xd, ev))
+        for (mod, _, yh), (xd, ev) in zip(calls, staged):
+            compute.wait_event(ev)
+            xd.record_stream(compute)
+
+            def on_rows(r0: int, r1: int, y: torch.Tensor, yh=yh) -> None:
+                done = torch.cuda.Event()
+                done.record(compute)
+                self.d2h.wait_event(done)
+                with torch.cuda.stream(self.d2h):
+                    yh[r0:r1].copy_(y[r0:r1], non_blocking=True)
+                y.record_stream(self.d2h)
+
+            mod.matmul_rows(xd, row_ranges(xd.shape[0], self.chunks), on_rows)
+        compute.wait_stream(self.d2h)
+
+
+def run_host_io(calls, chunks: int = 4) -> None:
+    """Functional form of ``HostIOPipeline(...).run(calls)``."""
+    HostIOPipeline(chunks=chunks).run(calls)

@@ -7,6 +7,11 @@ reassembles Y. Parity survives sharding exactly: the outlier set O and the
 row scales depend only on X (gemm.py:210, 242, identical on every rank), and
 the column scales are per column (quantize.py:186), so every output element
 is computed exactly as on one GPU.
+
+The all-gather is pipelined behind the GEMM: after one
+prologue over all rows, the GEMM runs per row range and each range's block is
+gathered on a communication stream while the next range computes, so the
+NVLink transfer overlaps the tensor-core work except for the last range.
 """
 
 from __future__ import annotations
@@ -54,6 +59,67 @@ def gather_columns(y_local: torch.Tensor, n_total: int, group=None) -> torch.Ten
     return out
 
 
+def row_ranges(m: int, chunks: int) -> list[tuple[int, int]]:
+    """Balanced contiguous row ranges; multiples of 256 (a CTA-pair tile) when possible."""
+    chunks = max(1, min(int(chunks), -(-m // 256)))
+    step = -(-m // chunks)
+    step = -(-step // 256) * 256 if m >= 256 * chunks else step
+    out, r = [], 0
+    while r < m:
+        out.append((r, min(m, r + step)))
+        r += step
+    return out
+
+
+class _GatherPipeline:
+    """Gathers row ranges of the padded per-rank blocks as they are produced.
+
+    ``push(r0, r1, y_pad)`` (called right after range r0:r1 is enqueued on the
+    compute stream) all-gathers those rows on the communication stream and
+    places every rank's block into ``out``; ``finish()`` joins the streams.
+    """
+
+    def __init__(self, m: int, n_total: int, width: int, dtype, device, group):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.n_total, self.width = n_total, width
+        self.out = torch.empty((m, n_total), dtype=dtype, device=device)
+        self.cuda = device.type == "cuda"
+        self.comm = torch.cuda.Stream(device=device) if self.cuda else None
+        self.gloo = dist.get_backend(group) == "gloo"
+
+    def push(self, r0: int, r1: int, y_pad: torch.Tensor) -> None:
+        rows = r1 - r0
+        src = y_pad[r0:r1]
+        if self.cuda:
+            ev = torch.cuda.Event()
+            ev.record()
+            self.comm.wait_event(ev)
+            ctx = torch.cuda.stream(self.comm)
+        else:
+            import contextlib
+
+            ctx = contextlib.nullcontext()
+        with ctx:
+            buf = torch.empty((self.world, rows, self.width), dtype=src.dtype, device=src.device)
+            if self.gloo:
+                dist.all_gather(list(buf.unbind(0)), src.contiguous(), group=self.group)
+            else:
+                dist.all_gather_into_tensor(buf, src, group=self.group)
+            for r in range(self.world):
+                lo, hi = shard_bounds(self.n_total, self.world, r)
+                self.out[r0:r1, lo:hi].copy_(buf[r, :, : hi - lo])
+        if self.cuda:
+            src.record_stream(self.comm)
+            buf.record_stream(self.comm)
+
+    def finish(self) -> torch.Tensor:
+        if self.cuda:
+            torch.cuda.current_stream().wait_stream(self.comm)
+            self.out.record_stream(torch.cuda.current_stream())
+        return self.out
+
+
 class ShardedInt8Linear(torch.nn.Module):
     """LLM.int8() linear layer with W split along its output dimension.
 
@@ -79,7 +145,24 @@ class ShardedInt8Linear(torch.nn.Module):
         """This rank's column block Y[:, lo:hi] (no communication)."""
         return self.local(x, _timer=_timer)
 
-    def forward(self, x: torch.Tensor, _timer=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, _timer=None, chunks: int | None = None) -> torch.Tensor:
+        """Y = x @ W over all ranks. ``chunks`` row ranges pipeline the
+        all-gather behind the GEMM (default 4 when world > 1, else 1)."""
         lead = x.shape[:-1]
-        y = self.forward_local(x.reshape(-1, x.shape[-1]), _timer)
-        return gather_columns(y, self.n_total, self.group).reshape(*lead, self.n_total)
+        x2 = x.reshape(-1, x.shape[-1])
+        if chunks is None:
+            chunks = 4 if self.world > 1 else 1
+        if chunks <= 1 or _timer is not None:
+            y = self.forward_local(x2, _timer)
+            return gather_columns(y, self.n_total, self.group).reshape(*lead, self.n_total)
+        return self.forward_pipelined(x2, chunks).reshape(*lead, self.n_total)
+
+    def forward_pipelined(self, x2: torch.Tensor, chunks: int) -> torch.Tensor:
+        m = x2.shape[0]
+        width = -(-self.n_total // self.world)
+        dt = self.local.out_dtype
+        y_pad = torch.zeros((m, width), dtype=dt, device=x2.device)
+        pipe = _GatherPipeline(m, self.n_total, width, dt, x2.device, self.group)
+        self.local.matmul_rows(as_f16_matrix(x2, "x"), row_ranges(m, chunks), pipe.push,
+                               y=y_pad, ldy=width)
+        return pipe.finish()

@@ -602,3 +602,61 @@ def test_qt8_roundtrip_through_device_pipeline(p, oracle_mod, tmp_path):
     qt8.write_tensor(tmp_path / "y.qt8", tr["y_exact"])
     assert np.array_equal(_np(qt8.read_tensor(tmp_path / "c.qt8")), ref.c)
     assert np.array_equal(_np(qt8.read_tensor(tmp_path / "y.qt8")), ref.output)
+
+
+def test_row_range_gemm_and_pipelined_gather_single_rank(p, oracle_mod):
+    """i8mm_linear_gemm_rows (one prologue, GEMM per row range) is bitwise the
+    single-call result; the pipelined NCCL all-gather path of
+    ShardedInt8Linear (world size 1 here: one GPU per box) runs its streams
+    and placement and returns the same bits."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2208_07339_b200.sharded import ShardedInt8Linear
+
+    x, w = oracle_mod.planted_pair(1000, 768, 520, 6, 20.0, 2)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+    y_ref = lin(x16)
+    seen = []
+    y_rows = lin.matmul_rows(x16, [(0, 256), (256, 300), (300, 1000)],
+                             on_rows=lambda r0, r1, y: seen.append((r0, r1)))
+    assert seen == [(0, 256), (256, 300), (300, 1000)]
+    assert torch.equal(y_rows, y_ref)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sh = ShardedInt8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+        assert torch.equal(sh(x16, chunks=4), y_ref)
+        assert torch.equal(sh(x16, chunks=1), y_ref)
+        assert torch.equal(sh(x16[:7], chunks=4), lin(x16[:7]))  # decode rows: one launch
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_io_pipeline_matches_device_calls(p, oracle_mod):
+    """HostIOPipeline (overlapped H2D / row-range GEMM / D2H streams) returns
+    bitwise the device-path outputs, for prefill and decode-sized calls."""
+    mods, xs, refs = [], [], []
+    for i, (m, k, n) in enumerate([(1000, 512, 300), (600, 300, 520), (5, 512, 130)]):
+        x, w = oracle_mod.planted_pair(m, k, n, 4, 20.0, 30 + i)
+        mod = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+        x16 = torch.from_numpy(x.astype(np.float16))
+        mods.append(mod)
+        xs.append(x16.pin_memory())
+        refs.append(mod(x16.cuda()).cpu())
+    ys = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in refs]
+    pipe = p.HostIOPipeline(chunks=3)
+    for _ in range(2):
+        for y in ys:
+            y.zero_()
+        pipe.run(list(zip(mods, xs, ys)))
+        torch.cuda.synchronize()
+        for y, r in zip(ys, refs):
+            assert torch.equal(y, r)

@@ -140,7 +140,23 @@ def _gloo_worker(rank, world, port, result_q):
         local = orc.c_llm_int8_matmul(x, w[:, lo:hi], 6.0).output
         y = gather_columns(torch.from_numpy(local), n)
         full = orc.c_llm_int8_matmul(x, w, 6.0).output
-        result_q.put((rank, bool(np.array_equal(y.numpy(), full))))
+        ok = bool(np.array_equal(y.numpy(), full))
+        # the pipelined gather: row ranges of the padded local block pushed as
+        # they would be produced (one prologue over all rows, then per range)
+        from paper_2208_07339_b200.sharded import _GatherPipeline, row_ranges
+
+        width = -(-n // world)
+        y_pad = torch.zeros((m, width), dtype=torch.float32)
+        y_pad[:, : hi - lo] = torch.from_numpy(local)
+        pipe = _GatherPipeline(m, n, width, torch.float32, torch.device("cpu"), None)
+        for r0, r1 in [(0, 5), (5, 13), (13, 24)]:
+            pipe.push(r0, r1, y_pad)
+        ok = ok and bool(np.array_equal(pipe.finish().numpy(), full))
+        ok = ok and row_ranges(1000, 4) == [(0, 250), (250, 500), (500, 750), (750, 1000)]
+        ok = ok and row_ranges(16384, 4) == [(0, 4096), (4096, 8192), (8192, 12288), (12288, 16384)]
+        ok = ok and row_ranges(300, 4) == [(0, 150), (150, 300)]
+        ok = ok and row_ranges(100, 4) == [(0, 100)]
+        result_q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
