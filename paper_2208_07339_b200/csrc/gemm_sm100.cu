@@ -43,9 +43,12 @@ constexpr int A_BYTES = BM * BK;
 
 // CG = CTAs per MMA (cta_group), MC = CTA pairs per cluster sharing each WqT
 // tile through TMA multicast (cluster = CG * MC CTAs along M).
-template <int CG, int MC = 1>
+// TS: fp16 output through per-warp shared-memory staging tiles and TMA bulk
+// stores (full 64-byte row segments per box row instead of 32 scattered
+// 16-byte stores per warp instruction); costs one operand stage of smem.
+template <int CG, int MC = 1, bool TS = false>
 struct Cfg {
-    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int STAGES = CG == 1 ? 4 : (TS ? 5 : 6);
     static constexpr int B_ROWS = BN / CG;        // WqT rows resident in each CTA
     static constexpr int B_LOAD_ROWS = B_ROWS / MC;  // rows each CTA fetches (then multicasts)
     static constexpr int B_BYTES = B_ROWS * BK;
@@ -73,9 +76,12 @@ struct __align__(8) Barriers {
 
 constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(float);
 constexpr size_t SMEM_COLS = static_cast<size_t>(BN) * sizeof(double);
-template <int CG, int MC>
+constexpr int STG_BYTES = 32 * 32 * 2;  // one 32 x 32 fp16 staging tile
+constexpr size_t SMEM_STG = static_cast<size_t>(EPI_WARPS) * 2 * STG_BYTES;  // double-buffered per warp
+template <int CG, int MC, bool TS = false>
 constexpr size_t smem_total() {
-    return 1024 /*align slack*/ + Cfg<CG, MC>::SMEM_OPERANDS + SMEM_WO + SMEM_COLS + sizeof(Barriers) + 64;
+    return 1024 /*align slack*/ + Cfg<CG, MC, TS>::SMEM_OPERANDS + (TS ? SMEM_STG : 0) + SMEM_WO +
+           SMEM_COLS + sizeof(Barriers) + 64;
 }
 
 struct Params {
@@ -105,6 +111,8 @@ struct Params {
     const float* patch_amax;
     const uint32_t* patch_mask;  // bit j: Y column j is written by a patch tile instead
     int vec_store;  // 1: y rows 16-byte aligned and row pitch a multiple of 16 B
+    int dbg_epi;    // A/B knob (I8MM_DBG_EPI): bit 0 skips the outlier FMAs, bit 1 the stores
+    int tma_y;      // tmap_y is valid (fp16 Y, 16-byte aligned rows)
 };
 
 struct TileSpace {
@@ -151,20 +159,24 @@ template <int EPI, int CG, int MC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b,
-                   const __grid_constant__ CUtensorMap tmap_p, const Params p) {
-    using C = Cfg<CG, MC>;
+                   const __grid_constant__ CUtensorMap tmap_p,
+                   const __grid_constant__ CUtensorMap tmap_y, const Params p) {
+    constexpr bool TS = EPI == EPI_F16 && CG == 2;
+    using C = Cfg<CG, MC, TS>;
     constexpr int STAGES = C::STAGES;
     constexpr int B_BYTES = C::B_BYTES;
     constexpr size_t SMEM_OPERANDS = C::SMEM_OPERANDS;
+    constexpr size_t SMEM_STAGE_OUT = TS ? SMEM_STG : 0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B, by offsetting within the shared
     // array (pointer arithmetic keeps the shared address space -> LDS, not LD)
     uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + static_cast<size_t>(STAGES) * A_BYTES;
-    float* smem_wo = reinterpret_cast<float*>(smem + SMEM_OPERANDS);
-    double* smem_col = reinterpret_cast<double*>(smem + SMEM_OPERANDS + SMEM_WO);
-    Barriers* bars = reinterpret_cast<Barriers*>(smem + SMEM_OPERANDS + SMEM_WO + SMEM_COLS);
+    uint8_t* smem_stg = smem + SMEM_OPERANDS;  // TS: per-warp output staging tiles
+    float* smem_wo = reinterpret_cast<float*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT);
+    double* smem_col = reinterpret_cast<double*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT + SMEM_WO);
+    Barriers* bars = reinterpret_cast<Barriers*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT + SMEM_WO + SMEM_COLS);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -303,6 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool wo_fast = n_out <= WO_CAP && p.wo != nullptr && n_out <= p.wo_cap;
         const bool xo_fast = n_out <= WO_CAP && p.xo != nullptr && n_out <= p.o_cap;
         const bool stage_wo = n_out > 0 && n_out <= WO_CAP;
+        uint32_t stg_cnt = 0;  // TS: output boxes issued by this warp
         int it = 0;
         for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
             int m_blk, n_blk;
@@ -387,9 +400,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tmem_ld_32x32b_x32(t_row + ch * 32, r);
                 tmem_ld_wait();
                 const int64_t cbase = col0 + ch * 32;
-                if (!row_ok || cbase >= n_live) continue;
+                if (cbase >= n_live) continue;  // warp-uniform
                 // columns owned by a patch tile are skipped by the main tile (same launch)
                 const uint32_t pm = (!mapped && p.patch_mask != nullptr) ? p.patch_mask[cbase >> 5] : 0u;
+                // TS: whole 32 x 32 box through smem + TMA (rows >= M, cols >= N clipped by TMA)
+                const bool tma_chunk = TS && !mapped && pm == 0u && p.tma_y;
+                if (!tma_chunk && !row_ok) continue;
                 const bool full_chunk = !mapped && pm == 0u && p.vec_store && cbase + 32 <= n_live;
                 if constexpr (EPI == EPI_I32) {
                     int32_t* yr = reinterpret_cast<int32_t*>(p.y) + row * p.ldy;
@@ -446,7 +462,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             v2[2 * u] = __fmul2_rn(__fmul2_rn(c01, rf2), make_float2(f.x, f.y));
                             v2[2 * u + 1] = __fmul2_rn(__fmul2_rn(c23, rf2), make_float2(f.z, f.w));
                         }
-                        if (n_out > 0) {
+                        if (n_out > 0 && !(p.dbg_epi & 1)) {
                             if (stage_wo) {
 #pragma unroll
                                 for (int o = 0; o < WO_CAP; ++o) {
@@ -477,7 +493,38 @@ __global__ void __launch_bounds__(THREADS, 1)
                             }
                         }
                     }
-                    if constexpr (EPI == EPI_F16) {
+                    if (p.dbg_epi & 2) {
+                        if (v[0] == 1234.5f) reinterpret_cast<float*>(p.y)[0] = v[1];  // keep v live
+                    } else if (tma_chunk) {
+                        // stage this row's 32 outputs (64 B) in the warp's tile, then one
+                        // elected lane stores the 32 x 32 box; two tiles alternate so
+                        // the next chunk's writes overlap the previous store
+                        const int ew = warp - EPI_WARP0;
+                        uint8_t* tile = smem_stg + (ew * 2 + (stg_cnt & 1)) * STG_BYTES;
+                        if (stg_cnt >= 2) {
+                            if (lane == 0) tma_store_wait_read<1>();
+                            __syncwarp();
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(tile + lane * 64);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            uint32_t pk[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                __half2 h2 = __floats2half2_rn(v[8 * u + 2 * e], v[8 * u + 2 * e + 1]);
+                                pk[e] = *reinterpret_cast<uint32_t*>(&h2);
+                            }
+                            dst[u ^ ((lane >> 1) & 3)] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        }
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmap_y, tile, static_cast<int32_t>(cbase),
+                                         static_cast<int32_t>(row - lane));
+                            tma_store_commit();
+                        }
+                        ++stg_cnt;
+                    } else if constexpr (EPI == EPI_F16) {
                         __half* yr = reinterpret_cast<__half*>(p.y) + row * p.ldy;
                         if (full_chunk) {
 #pragma unroll
@@ -521,6 +568,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 else mbar_arrive(&bars->tmem_empty[acc]);
             }
         }
+        if (TS && lane == 0) tma_store_wait<0>();  // staged outputs fully written
     }
 
     __syncthreads();
@@ -568,13 +616,29 @@ bool make_tmap_i8(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t K,
     return r == CUDA_SUCCESS;
 }
 
+// fp16 output Y [rows x cols], row pitch ld elements; box = 32 x 32, the
+// staging tile's 16-byte chunks XOR-swizzled by (row >> 1) & 3 (SWIZZLE_64B)
+static bool make_tmap_f16_out(CUtensorMap* map, void* base, int64_t rows, int64_t cols, int64_t ld) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <int EPI, int CG, int MC>
 static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tp,
-                              const Params& p, int64_t max_tiles, cudaStream_t st) {
+                              const CUtensorMap& ty, const Params& p, int64_t max_tiles,
+                              cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
-    constexpr size_t smem = smem_total<CG, MC>();
+    constexpr size_t smem = smem_total<CG, MC, EPI == EPI_F16 && CG == 2>();
     constexpr int CL = CG * MC;
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(THREADS);
@@ -605,7 +669,7 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
     if (attr_err != cudaSuccess) return attr_err;
     const int64_t clusters = max_tiles < max_clusters ? max_tiles : max_clusters;
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, tp, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, tp, ty, p);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -613,10 +677,11 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
 
 template <int EPI>
 static cudaError_t launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tp,
-                             const Params& p, int64_t max_tiles, int cg, int mc, cudaStream_t st) {
-    if (cg == 2 && mc == 2) return launch_epi<EPI, 2, 2>(ta, tb, tp, p, max_tiles, st);
-    if (cg == 2) return launch_epi<EPI, 2, 1>(ta, tb, tp, p, max_tiles, st);
-    return launch_epi<EPI, 1, 1>(ta, tb, tp, p, max_tiles, st);
+                             const CUtensorMap& ty, const Params& p, int64_t max_tiles, int cg,
+                             int mc, cudaStream_t st) {
+    if (cg == 2 && mc == 2) return launch_epi<EPI, 2, 2>(ta, tb, tp, ty, p, max_tiles, st);
+    if (cg == 2) return launch_epi<EPI, 2, 1>(ta, tb, tp, ty, p, max_tiles, st);
+    return launch_epi<EPI, 1, 1>(ta, tb, tp, ty, p, max_tiles, st);
 }
 
 }  // namespace gemm
@@ -699,11 +764,16 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     p.patch_mask = a.patch_mask;
     const int elt = (epi == EPI_F16) ? 2 : 4;
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
+    p.dbg_epi = env_int("I8MM_DBG_EPI");
+    CUtensorMap ty = ta;
+    p.tma_y = 0;
+    if (epi == EPI_F16 && p.vec_store && env_int("I8MM_NO_TMA_STORE") != 1)
+        p.tma_y = make_tmap_f16_out(&ty, a.y, a.M, a.N, a.ldy) ? 1 : 0;
     switch (epi) {
-        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, tp, p, max_tiles, cg, mc, st);
-        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, tp, p, max_tiles, cg, mc, st);
-        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, tp, p, max_tiles, cg, mc, st);
-        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, tp, p, max_tiles, cg, mc, st);
+        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
+        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
+        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
+        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
         default: return cudaErrorInvalidValue;
     }
 }
