@@ -242,12 +242,10 @@ struct Workspace {
     uint32_t* part;
     uint32_t* ramax_bits;
     int32_t* patch_pos;
-    int32_t* pc;
     int32_t* c32;
     int64_t c32_words;
     int32_t* tile_cnt;
     int64_t n_tiles;
-    int32_t* pc_cnt;
     uint32_t* thr_word;  // alpha threshold bits, written by the prologue entry
     int64_t ldq, o_cap;
     size_t bytes;
@@ -307,13 +305,11 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
             w.part = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * grid * M));
             w.ramax_bits = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * M));
             w.patch_pos = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
-            w.pc = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(N * M)));
             // split-tile partials: two [M x 128] int32 slots per CTA
             w.c32_words = 2 * grid * M * 128;
             w.c32 = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(w.c32_words)));
             w.n_tiles = (N + 127) / 128;
             w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (w.n_tiles + 2)));
-            w.pc_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
             w.thr_word = reinterpret_cast<uint32_t*>(w.tile_cnt + w.n_tiles + 1);
         } else {
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
@@ -492,14 +488,11 @@ static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __h
     d.p_idx = ws.p_idx;
     d.p_amax = ws.p_amax;
     d.patch_pos = ws.patch_pos;
-    d.pc = ws.pc;
-    d.p_src = ws.p_src;
     d.q2 = b.q2;
     d.c32 = ws.c32;
     d.c32_words = ws.c32_words;
     d.tile_cnt = ws.tile_cnt;
     d.n_tiles = ws.n_tiles;
-    d.pc_cnt = ws.pc_cnt;
     d.y = y;
     d.ldy = ldy;
     return d;

@@ -68,6 +68,7 @@ constexpr int MAX_STAGES = 12;
 constexpr int A_BYTES = TILE_N * BK;
 constexpr uint32_t TMEM_COLS = 512;  // two accumulators at column 0 and 256
 constexpr int MAX_M = 256;
+constexpr int LOCAL_CAP = 512;  // fixup columns per CTA (N <= LOCAL_CAP * grid)
 
 __device__ __forceinline__ bool bit_of(const uint32_t* m, int64_t k) {
     return (m[k >> 5] >> (k & 31)) & 1u;
@@ -155,6 +156,11 @@ struct __align__(8) Bars {
     int32_t finisher;
     int32_t n_out;
     int32_t n_patch;
+    int32_t n_local;                // patched columns found in this CTA's fixup range:
+    int32_t local_j[LOCAL_CAP];     //   column,
+    float local_a[LOCAL_CAP];       //   amax over keep rows,
+    int32_t local_src[LOCAL_CAP];   //   1 = its codes are the cached q2 row
+    int32_t red[16 * NWARPS];       // per-warp partial dot products (patched columns)
     int32_t warp_sums[NWARPS];
 };
 
@@ -283,6 +289,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&bars->tmem_empty[q], 4);
         }
         fence_mbarrier_init();
+        bars->n_local = 0;
         const uint64_t pol_w = l2_policy_evict_normal();
         for (int i = 0; i < n_pre; ++i) {
             const int64_t u = u_begin + i;
@@ -436,13 +443,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int32_t pidx = atomicAdd(a.p_count, 1);
             a.p_idx[pidx] = static_cast<int32_t>(j);
             a.p_amax[pidx] = a_new;
-            a.p_src[pidx] = src;
             a.patch_pos[j] = pidx + 1;
-            for (int64_t m = 0; m < M; ++m) a.pc[pidx * M + m] = 0;
-            a.pc_cnt[pidx] = 0;
-            if (src)  // warm L2 with the q2 row the dot products will read
-                for (int64_t k = 0; k < a.ldq; k += 128)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.q2 + j * a.ldq + k));
+            const int li = atomicAdd(&bars->n_local, 1);
+            bars->local_j[li] = static_cast<int32_t>(j);
+            bars->local_a[li] = a_new;
+            bars->local_src[li] = src;
         }
     }
     // Xq is read back by TMA (async proxy) after the grid barrier
@@ -456,7 +461,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
     const int n_out = bars->n_out;
-    const int n_patch = bars->n_patch;
     // per-token factors (rows of X) staged once
     for (int64_t m = threadIdx.x; m < M; m += THREADS) srow[m] = amax_or_127(hbits_to_float(sram[m]));
     if (n_out > 0 && n_out <= WO_CAP) {
@@ -465,12 +469,98 @@ __global__ void __launch_bounds__(THREADS, 1)
             sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + __ldcg(a.o_idx + o)]);
         }
     }
+    __syncthreads();
+    // ---------------- this CTA's patched columns, complete, before its weight
+    // stream resumes (memory is quiet; nothing downstream waits on them): exact
+    // int32 dots of the re-derived codes (q2 row, or W's column in the rare
+    // multi-outlier case) with Xq, then the same epilogue math
+    if (threadIdx.x == 0 && p.dbg != nullptr) {
+        p.dbg[blockIdx.x * 16 + 12] = static_cast<unsigned long long>(bars->n_local);
+        p.dbg[blockIdx.x * 16 + 13] = static_cast<unsigned long long>(bars->n_local ? bars->local_src[0] : 9);
+    }
+    for (int li = 0; li < bars->n_local; ++li) {
+        const int64_t j = bars->local_j[li];
+        const float aw = bars->local_a[li];
+        const bool src = bars->local_src[li] != 0;
+        const double s = scale_of(aw);
+        const float s32 = static_cast<float>(s);
+        const int64_t nk16 = a.ldq / 16;
+        for (int64_t m0 = 0; m0 < M; m0 += 16) {
+            int acc[16];
+#pragma unroll
+            for (int mm = 0; mm < 16; ++mm) acc[mm] = 0;
+            for (int64_t kv = threadIdx.x; kv < nk16; kv += THREADS) {
+                uint4 cw;
+                if (src) {
+                    cw = __ldcs(reinterpret_cast<const uint4*>(a.q2 + j * a.ldq + kv * 16));
+                } else {  // rare: re-derive 16 codes from the strided W column
+                    uint32_t b[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int64_t k = kv * 16 + e;
+                        const int c = (k < K && !bit_of(a.mask, k))
+                                          ? code_fast(__half2float(a.w[k * a.ldw + j]), s32, s) : 0;
+                        b[e] = static_cast<uint32_t>(c) & 0xFFu;
+                    }
+                    cw = make_uint4(b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24,
+                                    b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24,
+                                    b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24,
+                                    b[12] | b[13] << 8 | b[14] << 16 | b[15] << 24);
+                }
+                // predicated (branch-free) loads: all rows' bytes in flight at once
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint4 xv[8];
+#pragma unroll
+                    for (int mm = 0; mm < 8; ++mm) {
+                        const int64_t m = m0 + h * 8 + mm;
+                        xv[mm] = m < M ? __ldcg(reinterpret_cast<const uint4*>(a.xq + m * a.ldq + kv * 16))
+                                       : make_uint4(0u, 0u, 0u, 0u);
+                    }
+#pragma unroll
+                    for (int mm = 0; mm < 8; ++mm) {
+                        int& ac = acc[h * 8 + mm];
+                        ac = __dp4a(static_cast<int>(xv[mm].x), static_cast<int>(cw.x), ac);
+                        ac = __dp4a(static_cast<int>(xv[mm].y), static_cast<int>(cw.y), ac);
+                        ac = __dp4a(static_cast<int>(xv[mm].z), static_cast<int>(cw.z), ac);
+                        ac = __dp4a(static_cast<int>(xv[mm].w), static_cast<int>(cw.w), ac);
+                    }
+                }
+            }
+            if (threadIdx.x == 0 && li == 0 && m0 == 0) DSTAMP(p.dbg, 10);
+#pragma unroll
+            for (int mm = 0; mm < 16; ++mm) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[mm] += __shfl_xor_sync(0xffffffffu, acc[mm], o);
+                if (lane == 0) bars->red[mm * NWARPS + warp] = acc[mm];
+            }
+            __syncthreads();
+            if (threadIdx.x < 16 && m0 + threadIdx.x < M) {
+                const int64_t m = m0 + threadIdx.x;
+                int32_t c = 0;
+#pragma unroll
+                for (int w = 0; w < NWARPS; ++w) c += bars->red[threadIdx.x * NWARPS + w];
+                const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
+                float wr[WO_CAP];
+#pragma unroll
+                for (int o = 0; o < WO_CAP; ++o)
+                    wr[o] = (EPI != EPI_F32_EXACT && o < n_out && n_out <= WO_CAP)
+                                ? __half2float(a.w[static_cast<int64_t>(__ldcg(a.o_idx + o)) * a.ldw + j])
+                                : 0.0f;
+                store_out<EPI>(a, m, j, epi_value<EPI>(a, c, m, j, srow[m], colf, aw, n_out, sxo, wr));
+            }
+            __syncthreads();
+        }
+    }
+    // patched columns read L2/HBM with a few dependent round trips: keep the
+    // weight streams of all CTAs paused until they are done (one more grid
+    // barrier, only when the call has patched columns at all)
+    if (bars->n_patch > 0) grid.sync();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (threadIdx.x == 0) DSTAMP(p.dbg, 9);
     const uint32_t tmem_base = bars->tmem_slot;
-    const int64_t nkc = (K + 255) / 256;
-    const int64_t patch_items = static_cast<int64_t>(n_patch) * nkc;
 
     if (warp == 0) {
         // ---------------- TMA producer
@@ -538,78 +628,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (lane == 0) DSTAMP(p.dbg, 6);
     } else {
-        // ---------------- warps 2-7: patched columns (exact int32 dot products with Xq)
-        for (int64_t it = blockIdx.x * (NWARPS - 2) + (warp - 2); it < patch_items;
-             it += G * (NWARPS - 2)) {
-            const int64_t pi = it / nkc, kc = it % nkc;
-            const int64_t j = a.p_idx[pi];
-            const double s = scale_of(a.p_amax[pi]);
-            const float s32 = static_cast<float>(s);
-            const int64_t k0 = kc * 256 + lane * 8;
-            uint32_t cw0 = 0, cw1 = 0;
-            if (k0 < K && __ldcg(a.p_src + pi)) {  // cached second-candidate codes
-                const uint2 cw = *reinterpret_cast<const uint2*>(a.q2 + j * a.ldq + k0);
-                cw0 = cw.x;
-                cw1 = cw.y;
-            } else if (k0 < K) {  // rare: re-derive from the strided W column
-                __half h[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    h[e] = k0 + e < K ? a.w[(k0 + e) * a.ldw + j] : __float2half(0.0f);
-                const uint32_t mb = (__ldcg(a.mask + (k0 >> 5)) >> (k0 & 31)) & 0xFFu;
-                uint32_t b[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int c = ((mb >> e) & 1u) ? 0 : code_fast(__half2float(h[e]), s32, s);
-                    b[e] = static_cast<uint32_t>(c) & 0xFFu;
-                }
-                cw0 = b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24;
-                cw1 = b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24;
-            }
-            for (int64_t m0 = 0; m0 < M; m0 += 8) {  // 8 token rows per step
-                int d[8];
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int64_t m = m0 + jj;
-                    uint2 xv = make_uint2(0u, 0u);
-                    if (k0 < K && m < M) xv = __ldcg(reinterpret_cast<const uint2*>(a.xq + m * a.ldq + k0));
-                    d[jj] = __dp4a(static_cast<int>(xv.x), static_cast<int>(cw0), 0);
-                    d[jj] = __dp4a(static_cast<int>(xv.y), static_cast<int>(cw1), d[jj]);
-                }
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) d[jj] += __shfl_xor_sync(0xffffffffu, d[jj], o);
-                if (lane == 0) {
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj)
-                        if (m0 + jj < M && d[jj] != 0) atomicAdd(a.pc + pi * M + m0 + jj, d[jj]);
-                }
-            }
-            // the warp completing a patched column's last K-chunk writes its
-            // outputs (the main epilogue skips patched columns): nobody waits
-            __threadfence();
-            __syncwarp();
-            int last = 0;
-            if (lane == 0) last = atomicAdd(a.pc_cnt + pi, 1) == nkc - 1;
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-                __threadfence();
-                const float aw = __ldcg(a.p_amax + pi);
-                const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
-                float wr[WO_CAP];
-#pragma unroll
-                for (int o = 0; o < WO_CAP; ++o)
-                    wr[o] = (EPI != EPI_F32_EXACT && o < n_out && n_out <= WO_CAP)
-                                ? __half2float(a.w[static_cast<int64_t>(__ldcg(a.o_idx + o)) * a.ldw + j])
-                                : 0.0f;
-                for (int64_t m = lane; m < M; m += 32)
-                    store_out<EPI>(a, m, j, epi_value<EPI>(a, __ldcg(a.pc + pi * M + m), m, j, srow[m],
-                                                          colf, aw, n_out, sxo, wr));
-            }
-        }
-        if (warp == 2 && lane == 0) DSTAMP(p.dbg, 9);
-
         if (warp >= 4) {
             // ---------------- epilogue: thread = weight row n of the tile
             const int quad = warp & 3;
@@ -741,7 +759,8 @@ bool decode_fits(int64_t M, int64_t K, int64_t N) {
     const int64_t G = decode_grid(K, N);
     const int64_t nwords = (K + 31) / 32;
     const int64_t wpc = (nwords + G - 1) / G;  // owned words per CTA (max)
-    return M * wpc * 32 * 2 <= static_cast<int64_t>(dec::SMEM_UNION) && wpc <= 64;
+    return M * wpc * 32 * 2 <= static_cast<int64_t>(dec::SMEM_UNION) && wpc <= 64 &&
+           (N + G - 1) / G <= dec::LOCAL_CAP;
 }
 
 __global__ void set_word_kernel(uint32_t* dst, uint32_t value) { *dst = value; }

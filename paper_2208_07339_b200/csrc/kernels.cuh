@@ -137,14 +137,11 @@ struct DecodeArgs {
     int32_t* p_idx;
     float* p_amax;
     int32_t* patch_pos;   // [N]: 1 + patch index, 0 = not patched
-    int32_t* pc;          // [N x M] exact int32 sums of the patched columns
-    int32_t* p_src;       // [N] 1: patch codes are the cached q2 row
     const int8_t* q2;     // N x ldq second-candidate codes (weight buffer)
     int32_t* c32;         // [2 x grid] x [M x 128] split-tile partial slots
     int64_t c32_words;
     int32_t* tile_cnt;    // [n_tiles]
     int64_t n_tiles;
-    int32_t* pc_cnt;      // [N] K-chunks of each patched column completed
     void* y;
     int64_t ldy;
 };

@@ -44,8 +44,12 @@ def col(i):
 
 
 labels = {0: "start", 1: "P1 done", 3: "P2 done", 4: "sync2 out",
-          5: "first MMA", 9: "patches", 6: "MMA done", 7: "epi done", 8: "end"}
+          10: "1st dots", 9: "patched", 5: "first MMA", 6: "MMA done", 7: "epi done", 8: "end"}
 for i, lab in labels.items():
     v = G[:, i]
     arg = int(torch.argmax(v)) if (v > 0).any() else -1
     print(f"{lab:10s} {col(i)}  (max at CTA {arg})")
+
+nl = G[:, 12]
+print("patched columns per CTA: max", int(nl.max()), "sum", int(nl.sum()), "CTAs with any", int((nl > 0).sum()),
+      "src of first:", sorted(set(int(v) for v in G[:, 13].tolist())))
