@@ -113,6 +113,7 @@ struct Params {
     int vec_store;  // 1: y rows 16-byte aligned and row pitch a multiple of 16 B
     int dbg_epi;    // A/B knob (I8MM_DBG_EPI): bit 0 skips the outlier FMAs, bit 1 the stores
     int tma_y;      // tmap_y is valid (fp16 Y, 16-byte aligned rows)
+    int group_m;    // raster: m-tiles per group sharing each B panel in L2
 };
 
 struct TileSpace {
@@ -133,9 +134,9 @@ __device__ __forceinline__ TileSpace tile_space(const Params& p) {
     return ts;
 }
 
-template <int GROUP_M>
 __device__ __forceinline__ bool tile_coords(const Params& p, const TileSpace& ts, int t,
                                             int& m_blk, int& n_blk) {
+    const int GROUP_M = p.group_m;
     if (t >= ts.main_total) {  // patch tiles (weight-stationary fixup), m fastest
         const int local = t - ts.main_total;
         m_blk = local % p.m_tiles;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t phase = 0;
             for (int t = cluster_id; t < ts.total; t += n_clusters) {
                 int m_blk, n_blk;
-                const bool is_patch = tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
+                const bool is_patch = tile_coords(p, ts, t, m_blk, n_blk);
                 const CUtensorMap* map_b = is_patch ? &tmap_p : &tmap_b;
                 const int a_row = m_blk * C::TILE_M + static_cast<int>(pair) * (BM * CG) +
                                   static_cast<int>(crank) * BM;
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int it = 0;
         for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
             int m_blk, n_blk;
-            const bool is_patch = tile_coords<C::GROUP_M>(p, ts, t, m_blk, n_blk);
+            const bool is_patch = tile_coords(p, ts, t, m_blk, n_blk);
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int64_t n_live = is_patch ? ts.patch_n : p.N;
@@ -765,6 +766,26 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     const int elt = (epi == EPI_F16) ? 2 : 4;
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
     p.dbg_epi = env_int("I8MM_DBG_EPI");
+    {
+        // Raster (measured, scripts/ab_raster.sh): when one wave of concurrent
+        // tiles covers >= 2 full rows of N-tiles, B panels are reused within the
+        // wave -> row-major (group 1); otherwise group GROUP_M m-tiles so their
+        // A panels (GROUP_M x TILE_M x K bytes) stay within ~32 MB of L2 while
+        // the B panels stream past them.
+        const int gm_env = env_int("I8MM_GROUP_M");
+        const int64_t n_tiles = (a.N + BN - 1) / BN;
+        const int64_t wave = num_sms() / (cg * mc);
+        int gm;
+        if (n_tiles * 2 <= wave) {
+            gm = 1;
+        } else {
+            const int64_t panel = static_cast<int64_t>(BM) * cg * mc * (a.K > 0 ? a.K : 1);
+            int64_t g = (32LL << 20) / panel;
+            gm = 1;
+            while (gm * 2 <= g && gm < 32) gm *= 2;
+        }
+        p.group_m = gm_env > 0 ? gm_env : gm;
+    }
     CUtensorMap ty = ta;
     p.tma_y = 0;
     if (epi == EPI_F16 && p.vec_store && env_int("I8MM_NO_TMA_STORE") != 1)
