@@ -311,6 +311,7 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
             w.n_tiles = (N + 127) / 128;
             w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (w.n_tiles + 2)));
             w.thr_word = reinterpret_cast<uint32_t*>(w.tile_cnt + w.n_tiles + 1);
+            w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(128 * w.ldq)));  // patch tile rows
         } else {
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
         }
@@ -489,6 +490,7 @@ static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __h
     d.p_amax = ws.p_amax;
     d.patch_pos = ws.patch_pos;
     d.q2 = b.q2;
+    d.pq = ws.wq_p;
     d.c32 = ws.c32;
     d.c32_words = ws.c32_words;
     d.tile_cnt = ws.tile_cnt;

@@ -69,6 +69,7 @@ constexpr int A_BYTES = TILE_N * BK;
 constexpr uint32_t TMEM_COLS = 512;  // two accumulators at column 0 and 256
 constexpr int MAX_M = 256;
 constexpr int LOCAL_CAP = 512;  // fixup columns per CTA (N <= LOCAL_CAP * grid)
+constexpr int PATCH_ROWS = 128; // patched columns handled by the extra tile of the stream
 
 __device__ __forceinline__ bool bit_of(const uint32_t* m, int64_t k) {
     return (m[k >> 5] >> (k & 31)) & 1u;
@@ -158,6 +159,7 @@ struct __align__(8) Bars {
     int32_t n_patch;
     int32_t n_local;                // patched columns found in this CTA's fixup range:
     int32_t local_j[LOCAL_CAP];     //   column,
+    int32_t local_p[LOCAL_CAP];     //   patch index (row of the patch tile),
     float local_a[LOCAL_CAP];       //   amax over keep rows,
     int32_t local_src[LOCAL_CAP];   //   1 = its codes are the cached q2 row
     int32_t red[16 * NWARPS];       // per-warp partial dot products (patched columns)
@@ -252,7 +254,8 @@ __host__ __device__ __forceinline__ void owned_words(int64_t nwords, int64_t G, 
 template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
-                        const __grid_constant__ CUtensorMap tmap_x, const Params p) {
+                        const __grid_constant__ CUtensorMap tmap_x,
+                        const __grid_constant__ CUtensorMap tmap_p, const Params p) {
     cg::grid_group grid = cg::this_grid();
     const DecodeArgs& a = p.a;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -273,13 +276,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int64_t u_begin = T * blockIdx.x / G;
     const int64_t u_end = T * (blockIdx.x + 1) / G;
     const int num_kb = p.num_kb;
-    const int n_pre = static_cast<int>(min(static_cast<int64_t>(p.prefetch), u_end - u_begin));
+    // the last tile (index n_tiles) is the patch tile: its A rows are the q2 rows
+    // of this call's patched columns, written in P2, so it is never prefetched
+    const int64_t main_units = static_cast<int64_t>(p.n_tiles) * num_kb;
+    const int n_pre = static_cast<int>(
+        max(static_cast<int64_t>(0), min(static_cast<int64_t>(p.prefetch), min(u_end, main_units) - u_begin)));
 
     if (threadIdx.x == 0) DSTAMP(p.dbg, 0);
     // ================= W0: setup + weight prefetch (independent of X)
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmap_w);
         tma_prefetch_desc(&tmap_x);
+        tma_prefetch_desc(&tmap_p);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
@@ -324,8 +332,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint4 q = load8(a.x + m * a.ldx, c0 + v8 * 8, K, a.x_vec);
             *reinterpret_cast<uint4*>(xs + m * xs_ld + v8 * 8) = q;
         }
-        for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i < a.n_tiles; i += G * PT)
-            a.tile_cnt[i] = 0;
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i <= a.n_tiles; i += G * PT)
+            a.tile_cnt[i] = 0;  // main tiles + the patch tile
         for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i < N; i += G * PT)
             a.patch_pos[i] = 0;
         if (blockIdx.x == 0 && pt == 0) *a.p_count = 0;
@@ -446,11 +454,33 @@ __global__ void __launch_bounds__(THREADS, 1)
             a.patch_pos[j] = pidx + 1;
             const int li = atomicAdd(&bars->n_local, 1);
             bars->local_j[li] = static_cast<int32_t>(j);
+            bars->local_p[li] = pidx;
             bars->local_a[li] = a_new;
             bars->local_src[li] = src;
         }
     }
-    // Xq is read back by TMA (async proxy) after the grid barrier
+    __syncthreads();
+    // patch-tile rows: the re-derived codes of this CTA's patched columns (the
+    // cached q2 row; W's strided column in the rare deeper case), read by TMA
+    // as the A operand of the extra tile
+    for (int li = 0; li < bars->n_local; ++li) {
+        const int pidx = bars->local_p[li];
+        if (pidx >= PATCH_ROWS) continue;  // overflow: CUDA-core path after the barrier
+        const int64_t j = bars->local_j[li];
+        int8_t* dst = a.pq + static_cast<int64_t>(pidx) * a.ldq;
+        if (bars->local_src[li]) {
+            const uint4* srcq = reinterpret_cast<const uint4*>(a.q2 + j * a.ldq);
+            for (int64_t v = threadIdx.x; v < a.ldq / 16; v += THREADS)
+                reinterpret_cast<uint4*>(dst)[v] = __ldcs(srcq + v);
+        } else {
+            const double s = scale_of(bars->local_a[li]);
+            const float s32 = static_cast<float>(s);
+            for (int64_t k = threadIdx.x; k < a.ldq; k += THREADS)
+                dst[k] = (k < K && !bit_of(a.mask, k))
+                             ? static_cast<int8_t>(code_fast(__half2float(a.w[k * a.ldw + j]), s32, s)) : int8_t(0);
+        }
+    }
+    // Xq and the patch rows are read back by TMA (async proxy) after the barrier
     asm volatile("fence.proxy.async.global;" ::: "memory");
     if (threadIdx.x == 32) DSTAMP(p.dbg, 3);
     grid.sync();
@@ -461,6 +491,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
     const int n_out = bars->n_out;
+    const int np_all = bars->n_patch;
     // per-token factors (rows of X) staged once
     for (int64_t m = threadIdx.x; m < M; m += THREADS) srow[m] = amax_or_127(hbits_to_float(sram[m]));
     if (n_out > 0 && n_out <= WO_CAP) {
@@ -479,6 +510,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         p.dbg[blockIdx.x * 16 + 13] = static_cast<unsigned long long>(bars->n_local ? bars->local_src[0] : 9);
     }
     for (int li = 0; li < bars->n_local; ++li) {
+        if (bars->local_p[li] < PATCH_ROWS) continue;  // handled by the patch tile
         const int64_t j = bars->local_j[li];
         const float aw = bars->local_a[li];
         const bool src = bars->local_src[li] != 0;
@@ -555,7 +587,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // patched columns read L2/HBM with a few dependent round trips: keep the
     // weight streams of all CTAs paused until they are done (one more grid
     // barrier, only when the call has patched columns at all)
-    if (bars->n_patch > 0) grid.sync();
+    if (bars->n_patch > PATCH_ROWS) grid.sync();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -580,7 +612,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(&bars->empty[stage], phase ^ 1u);
                 mbar_arrive_expect_tx(&bars->full[stage], stage_bytes);
                 uint8_t* dst = ring + static_cast<size_t>(stage) * stage_bytes;
-                tma_load_2d(&tmap_w, &bars->full[stage], dst, kb * BK, tile * TILE_N, pol_w);
+                if (tile < p.n_tiles)
+                    tma_load_2d(&tmap_w, &bars->full[stage], dst, kb * BK, tile * TILE_N, pol_w);
+                else  // the patch tile: q2 rows of the patched columns
+                    tma_load_2d(&tmap_p, &bars->full[stage], dst, kb * BK, 0, pol_x);
                 tma_load_2d(&tmap_x, &bars->full[stage], dst + A_BYTES, kb * BK, 0, pol_x);
                 if (++stage == p.stages) {
                     stage = 0;
@@ -641,10 +676,21 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const bool full = len == num_kb;
                 u = seg_end;
                 const int acc = seg & 1;
-                const int64_t n = tile * TILE_N + n_local;
-                const bool n_ok = n < N;
-                const int32_t pp = n_ok ? __ldcg(a.patch_pos + n) : 0;
-                const float aw = n_ok ? (pp ? __ldcg(a.p_amax + pp - 1) : a.amax_full[n]) : 127.0f;
+                int64_t n;
+                bool n_ok;
+                int32_t pp;
+                float aw;
+                if (tile < p.n_tiles) {
+                    n = tile * TILE_N + n_local;
+                    n_ok = n < N;
+                    pp = n_ok ? __ldcg(a.patch_pos + n) : 0;  // patched: written by the patch tile
+                    aw = n_ok ? a.amax_full[n] : 127.0f;
+                } else {  // patch tile: row n_local is patched column p_idx[n_local]
+                    n_ok = n_local < min(np_all, PATCH_ROWS);
+                    n = n_ok ? __ldcg(a.p_idx + n_local) : 0;
+                    pp = 0;
+                    aw = n_ok ? __ldcg(a.p_amax + n_local) : 127.0f;
+                }
                 const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
                 float wr[WO_CAP];
 #pragma unroll
@@ -750,7 +796,7 @@ int decode_stages(int64_t M) {
 }
 
 int decode_grid(int64_t K, int64_t N) {
-    const int64_t units = ((N + dec::TILE_N - 1) / dec::TILE_N) * ((K + dec::BK - 1) / dec::BK);
+    const int64_t units = ((N + dec::TILE_N - 1) / dec::TILE_N + 1) * ((K + dec::BK - 1) / dec::BK);
     return static_cast<int>(units < num_sms() ? units : num_sms());
 }
 
@@ -787,8 +833,8 @@ static unsigned long long* g_dbg = nullptr;
 void set_decode_timeline(unsigned long long* stamps) { g_dbg = stamps; }
 
 template <int EPI>
-static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, const dec::Params& prm,
-                                size_t smem, int grid, cudaStream_t st) {
+static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tp,
+                                const dec::Params& prm, size_t smem, int grid, cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
@@ -806,7 +852,7 @@ static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, co
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, dec::decode_fused_kernel<EPI>, tw, tx, prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dec::decode_fused_kernel<EPI>, tw, tx, tp, prm);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -820,23 +866,24 @@ cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st) {
     prm.mpad = static_cast<int>((a.M + 15) / 16 * 16);
     prm.num_kb = static_cast<int>((a.K + BK - 1) / BK);
     prm.n_tiles = static_cast<int>((a.N + TILE_N - 1) / TILE_N);
-    prm.total_units = static_cast<int64_t>(prm.n_tiles) * prm.num_kb;
+    prm.total_units = static_cast<int64_t>(prm.n_tiles + 1) * prm.num_kb;  // + the patch tile
     prm.stages = decode_stages(a.M);
     prm.b_bytes = static_cast<uint32_t>(prm.mpad * BK);
     prm.n_acc = prm.mpad <= 64 ? 4 : (prm.mpad <= 128 ? 2 : 1);
     const int pf = decode_prefetch() < 0 ? 3 : decode_prefetch();
     prm.prefetch = pf < prm.stages ? pf : prm.stages;
     prm.dbg = g_dbg;
-    CUtensorMap tw, tx;
+    CUtensorMap tw, tx, tp;
     if (!make_tmap_i8_rows(&tw, a.wq_t, a.N, a.K, a.ldq, TILE_N)) return cudaErrorInvalidValue;
     if (!make_tmap_i8_rows(&tx, a.xq, a.M, a.K, a.ldq, prm.mpad)) return cudaErrorInvalidValue;
+    if (!make_tmap_i8_rows(&tp, a.pq, PATCH_ROWS, a.K, a.ldq, TILE_N)) return cudaErrorInvalidValue;
     const size_t smem =
         1024 + static_cast<size_t>(prm.stages) * (A_BYTES + prm.b_bytes) + smem_extra();
     const int grid = decode_grid(a.K, a.N);
     switch (epi) {
-        case EPI_F16: return launch_fused<EPI_F16>(tw, tx, prm, smem, grid, st);
-        case EPI_F32: return launch_fused<EPI_F32>(tw, tx, prm, smem, grid, st);
-        case EPI_F32_EXACT: return launch_fused<EPI_F32_EXACT>(tw, tx, prm, smem, grid, st);
+        case EPI_F16: return launch_fused<EPI_F16>(tw, tx, tp, prm, smem, grid, st);
+        case EPI_F32: return launch_fused<EPI_F32>(tw, tx, tp, prm, smem, grid, st);
+        case EPI_F32_EXACT: return launch_fused<EPI_F32_EXACT>(tw, tx, tp, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }

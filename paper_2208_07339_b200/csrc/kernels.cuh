@@ -138,9 +138,10 @@ struct DecodeArgs {
     float* p_amax;
     int32_t* patch_pos;   // [N]: 1 + patch index, 0 = not patched
     const int8_t* q2;     // N x ldq second-candidate codes (weight buffer)
+    int8_t* pq;           // [128 x ldq] A rows of the patch tile (codes of patched columns)
     int32_t* c32;         // [2 x grid] x [M x 128] split-tile partial slots
     int64_t c32_words;
-    int32_t* tile_cnt;    // [n_tiles]
+    int32_t* tile_cnt;    // [n_tiles + 1] (+ the patch tile)
     int64_t n_tiles;
     void* y;
     int64_t ldy;
