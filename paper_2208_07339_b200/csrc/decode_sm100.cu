@@ -148,6 +148,46 @@ __device__ void compact_block(const uint32_t* __restrict__ mask, int64_t nwords,
     if (threadIdx.x == blockDim.x - 1) *o_count = pos;
 }
 
+// same scan, but only the first WO_CAP indices (to shared memory) and the count
+__device__ void compact_block_smem(const uint32_t* __restrict__ mask, int64_t nwords, int32_t* o_s,
+                                   int32_t* n_s, int32_t* warp_sums) {
+    const int64_t per = (nwords + blockDim.x - 1) / blockDim.x;
+    const int64_t w0 = threadIdx.x * per;
+    const int64_t w1 = w0 + per < nwords ? w0 + per : nwords;
+    int32_t local = 0;
+    for (int64_t w = w0; w < w1; ++w) local += __popc(__ldcg(mask + w));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t incl = local;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        int32_t s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t t = __shfl_up_sync(0xffffffffu, s, d);
+            if (lane >= d) s += t;
+        }
+        if (lane < nw) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    int32_t pos = incl - local + (wid > 0 ? warp_sums[wid - 1] : 0);
+    for (int64_t w = w0; w < w1 && pos < WO_CAP; ++w) {
+        uint32_t m = __ldcg(mask + w);
+        while (m && pos < WO_CAP) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            o_s[pos++] = static_cast<int32_t>((w << 5) + b);
+        }
+    }
+    if (threadIdx.x == blockDim.x - 1) *n_s = incl + (wid > 0 ? warp_sums[wid - 1] : 0);
+}
+
 struct __align__(8) Bars {
     uint64_t full[MAX_STAGES];
     uint64_t empty[MAX_STAGES];
@@ -156,7 +196,7 @@ struct __align__(8) Bars {
     uint32_t tmem_slot;
     int32_t finisher;
     int32_t n_out;
-    int32_t n_patch;
+    int32_t o_s[WO_CAP];            // first outlier columns (this CTA's compaction)
     int32_t n_local;                // patched columns found in this CTA's fixup range:
     int32_t local_j[LOCAL_CAP];     //   column,
     int32_t local_p[LOCAL_CAP];     //   patch index (row of the patch tile),
@@ -324,6 +364,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int64_t xs_ld = (w1 - w0) * 32;          // halves per smem row
     const uint32_t thr_bits = a.thr_bits_dev != nullptr ? *a.thr_bits_dev : a.thr_bits;
 
+    // fixup candidates of this CTA's column range (weight-side data: fetched now,
+    // consumed after barrier 1)
+    const int64_t j0 = N * blockIdx.x / G, j1 = N * (blockIdx.x + 1) / G;
+    int32_t crA[kTopT], crB[kTopT];
+#pragma unroll
+    for (int i = 0; i < kTopT; ++i) {
+        const int64_t ja = j0 + threadIdx.x, jb = ja + THREADS;
+        crA[i] = ja < j1 ? a.cand_r[i * N + ja] : -1;
+        crB[i] = jb < j1 ? a.cand_r[i * N + jb] : -1;
+    }
+
     // ---------------- P1: load this CTA's column slice of X (all M rows) into
     // smem; its outlier bits (final) and per-row partial absmax over keep columns
     if (pro) {
@@ -384,7 +435,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     if (blockIdx.x == 0) compact_block(a.mask, nwords, a.o_idx, a.o_count, bars->warp_sums);
+    else compact_block_smem(a.mask, nwords, bars->o_s, &bars->n_out, bars->warp_sums);
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) bars->n_out = *a.o_count;
+    if (blockIdx.x == 0 && threadIdx.x < WO_CAP && threadIdx.x < K) bars->o_s[threadIdx.x] = a.o_idx[threadIdx.x];
+    __syncthreads();
+    const int n_out = bars->n_out;
     // codes: 8 consecutive columns per thread item, stored as 8 bytes
     {
         for (int64_t i = threadIdx.x; i < M * nvec; i += THREADS) {
@@ -416,13 +472,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                 a.ramax_bits[m] = sram[m];
             }
     }
+    __syncthreads();  // the X slice (xs) is consumed: its bytes become sxo
+    // x[:, O] factors for the epilogue (X is read-only: no need to wait for anyone)
+    if (n_out > 0 && n_out <= WO_CAP) {
+        for (int64_t i = threadIdx.x; i < M * n_out; i += THREADS) {
+            const int64_t m = i / n_out, o = i % n_out;
+            sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
+        }
+    }
     // weight-stationary fixup (weights.cu fixup_kernel semantics) over this
-    // CTA's column range; all four candidates are fetched up front
-    const int64_t j0 = N * blockIdx.x / G, j1 = N * (blockIdx.x + 1) / G;
-    for (int64_t j = j0 + threadIdx.x; j < j1; j += THREADS) {
+    // CTA's column range; the four candidates were fetched during P1
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int64_t j = j0 + threadIdx.x + h * THREADS;
+        if (j >= j1) continue;
         int32_t cr[kTopT];
 #pragma unroll
-        for (int i = 0; i < kTopT; ++i) cr[i] = a.cand_r[i * N + j];
+        for (int i = 0; i < kTopT; ++i) cr[i] = h ? crB[i] : crA[i];
         if (cr[0] < 0 || !bit_of(a.mask, cr[0])) continue;
         float a_new = -1.0f;
         bool exhausted = true;
@@ -484,22 +550,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("fence.proxy.async.global;" ::: "memory");
     if (threadIdx.x == 32) DSTAMP(p.dbg, 3);
     grid.sync();
-    if (threadIdx.x == 0) {
-        DSTAMP(p.dbg, 4);
-        bars->n_out = *reinterpret_cast<volatile int32_t*>(a.o_count);
-        bars->n_patch = *reinterpret_cast<volatile int32_t*>(a.p_count);
-    }
-    __syncthreads();
-    const int n_out = bars->n_out;
-    const int np_all = bars->n_patch;
-    // per-token factors (rows of X) staged once
+    if (threadIdx.x == 0) DSTAMP(p.dbg, 4);
+    // per-token factors (rows of X) staged once; x[:, O] was staged in P2
     for (int64_t m = threadIdx.x; m < M; m += THREADS) srow[m] = amax_or_127(hbits_to_float(sram[m]));
-    if (n_out > 0 && n_out <= WO_CAP) {
-        for (int64_t i = threadIdx.x; i < M * n_out; i += THREADS) {
-            const int64_t m = i / n_out, o = i % n_out;
-            sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + __ldcg(a.o_idx + o)]);
-        }
-    }
     __syncthreads();
     // ---------------- this CTA's patched columns, complete, before its weight
     // stream resumes (memory is quiet; nothing downstream waits on them): exact
@@ -577,7 +630,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int o = 0; o < WO_CAP; ++o)
                     wr[o] = (EPI != EPI_F32_EXACT && o < n_out && n_out <= WO_CAP)
-                                ? __half2float(a.w[static_cast<int64_t>(__ldcg(a.o_idx + o)) * a.ldw + j])
+                                ? __half2float(a.w[static_cast<int64_t>(bars->o_s[o]) * a.ldw + j])
                                 : 0.0f;
                 store_out<EPI>(a, m, j, epi_value<EPI>(a, c, m, j, srow[m], colf, aw, n_out, sxo, wr));
             }
@@ -587,7 +640,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // patched columns read L2/HBM with a few dependent round trips: keep the
     // weight streams of all CTAs paused until they are done (one more grid
     // barrier, only when the call has patched columns at all)
-    if (bars->n_patch > PATCH_ROWS) grid.sync();
+
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -665,6 +718,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else {
         if (warp >= 4) {
             // ---------------- epilogue: thread = weight row n of the tile
+            const int np_all = __ldcg(a.p_count);  // final after barrier 2
             const int quad = warp & 3;
             const int n_local = quad * 32 + lane;
             const int chunks = p.mpad / 16;
@@ -697,7 +751,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int o = 0; o < WO_CAP; ++o) {
                     float wv = 0.0f;
                     if (EPI != EPI_F32_EXACT && o < n_out && n_out <= WO_CAP && n_ok)
-                        wv = __half2float(a.w[static_cast<int64_t>(__ldcg(a.o_idx + o)) * a.ldw + n]);
+                        wv = __half2float(a.w[static_cast<int64_t>(bars->o_s[o]) * a.ldw + n]);
                     wr[o] = wv;
                 }
                 mbar_wait(&bars->tmem_full[acc], (seg >> 1) & 1);
