@@ -247,6 +247,7 @@ struct Workspace {
     int32_t* tile_cnt;
     int64_t n_tiles;
     uint32_t* thr_word;  // alpha threshold bits, written by the prologue entry
+    void* rp_scratch;    // prefill: per-row group maxima + f64 row scales (launch_row_prologue)
     int64_t ldq, o_cap;
     size_t bytes;
 };
@@ -316,6 +317,7 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
         }
     }
+    if (!w.decode) w.rp_scratch = reinterpret_cast<void*>(take(row_prologue_scratch_bytes(M > 0 ? M : 1, K)));
     w.bytes = p - p0;
     return w;
 }
@@ -375,11 +377,9 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
     const __half* wh = static_cast<const __half*>(w);
     cudaError_t e;
     // gemm.py:225 extract_outlier_columns
-    if ((e = launch_outlier_scan(xh, M, K, ldx, alpha, ws.mask, nullptr, st))) return I8MM_ERR_CUDA;
-    if ((e = launch_outlier_compact(ws.mask, K, ws.o_idx, ws.o_count, st))) return I8MM_ERR_CUDA;
-    // gemm.py:242 rowwise over keep columns + gather of x[:, O] (gemm.py:238)
-    if ((e = launch_quantize_rows(xh, M, K, ldx, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
-                                  ws.row_amax, ws.xo, ws.o_cap, st)))
+    // + gemm.py:242 rowwise over keep columns + gather of x[:, O] (gemm.py:238)
+    if ((e = launch_row_prologue(xh, M, K, ldx, alpha, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
+                                 ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st)))
         return I8MM_ERR_CUDA;
     // gemm.py:243 colwise over keep rows, stored K-major
     if ((e = launch_quantize_cols_t(wh, K, N, ldw, ws.mask, ws.wq_t, ws.ldq, ws.col_amax, st)))
@@ -519,10 +519,8 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
     // prologue entry only records the threshold for it (i8mm_linear_forward
     // passes it directly and skips this launch)
     if (ws.decode) return cuda_status(launch_set_word(ws.thr_word, alpha_threshold_bits(alpha), st));
-    if (launch_outlier_scan(xh, M, K, ldx, alpha, ws.mask, nullptr, st)) return I8MM_ERR_CUDA;
-    if (launch_outlier_compact(ws.mask, K, ws.o_idx, ws.o_count, st)) return I8MM_ERR_CUDA;
-    if (launch_quantize_rows(xh, M, K, ldx, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
-                             ws.row_amax, ws.xo, ws.o_cap, st))
+    if (launch_row_prologue(xh, M, K, ldx, alpha, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
+                            ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st))
         return I8MM_ERR_CUDA;
     if (launch_gather_rows(wh, ldw, N, ws.o_idx, ws.o_count, ws.o_cap, ws.wo, round_up(N, 8), st))
         return I8MM_ERR_CUDA;

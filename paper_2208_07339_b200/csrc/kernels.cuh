@@ -18,6 +18,14 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
                                  const uint32_t* mask, const int32_t* o_idx,
                                  const int32_t* o_count, int8_t* xq, int64_t ldq, float* amax,
                                  __half* xo, int64_t o_cap, cudaStream_t st);
+// Row side of the prologue in one call: scan (+ per-row 64-column group maxima),
+// compact, row scales (+ x[:, O]), streaming codes. `scratch` holds
+// row_prologue_scratch_bytes(M, K); nullptr (or unaligned X) = scan, compact, quantize_rows.
+size_t row_prologue_scratch_bytes(int64_t M, int64_t K);
+cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
+                                uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
+                                int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
+                                void* scratch, cudaStream_t st);
 cudaError_t launch_quantize_cols_t(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                    const uint32_t* row_mask, int8_t* wq_t, int64_t ldq,
                                    float* col_amax, cudaStream_t st);

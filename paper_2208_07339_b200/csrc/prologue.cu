@@ -13,9 +13,11 @@
 // __dmul_rn / __dadd_rn / IEEE division so nvcc cannot contract into FMA.
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "quant_common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace i8mm {
 
@@ -30,22 +32,39 @@ namespace i8mm {
 // unsigned max (two halves per 32-bit word); the column is an outlier iff that
 // max >= bits(a_h). NaN/Inf patterns are >= 0x7C00, so they surface both as
 // outliers and through the nonfinite flag.
+template <bool GM>
 __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M, int64_t K,
                                         int64_t ldx, uint32_t thr_bits, int64_t rows_per_block,
                                         uint32_t* __restrict__ col_mask,
-                                        int32_t* __restrict__ nonfinite) {
+                                        int32_t* __restrict__ nonfinite,
+                                        uint16_t* __restrict__ gmax, int64_t ng) {
     const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // vector col
     const int64_t nvec = K >> 3;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
     const int64_t r1 = min(M, r0 + rows_per_block);
+    const uint32_t lane = threadIdx.x & 31u;
+    const bool live = v < nvec;
     uint32_t m[4] = {0, 0, 0, 0};
-    if (v < nvec) {
-        const __half* p = x + r0 * ldx + (v << 3);
+    // GM: per row, the max |x| bits over each 64-column group (8 adjacent
+    // lanes), so the row quantizer needs no second amax pass over X. The
+    // row loop is warp-uniform (dead lanes load nothing and feed zeros).
+    auto group_max = [&](const uint4& q, int64_t r) {
+        if (!GM) return;
+        const uint32_t w = __vmaxu2(__vmaxu2(q.x & 0x7FFF7FFFu, q.y & 0x7FFF7FFFu),
+                                    __vmaxu2(q.z & 0x7FFF7FFFu, q.w & 0x7FFF7FFFu));
+        uint32_t h = max(w & 0xFFFFu, w >> 16);
+        h = max(h, __shfl_xor_sync(0xffffffffu, h, 1));
+        h = max(h, __shfl_xor_sync(0xffffffffu, h, 2));
+        h = max(h, __shfl_xor_sync(0xffffffffu, h, 4));
+        if ((lane & 7u) == 0 && live) gmax[r * ng + (v >> 3)] = static_cast<uint16_t>(h);
+    };
+    if (live || GM) {
+        const __half* p = x + r0 * ldx + (live ? (v << 3) : 0);
         int64_t r = r0;
         for (; r + 8 <= r1; r += 8) {
             uint4 q[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) q[u] = ld_stream_u4(p + u * ldx);
+            for (int u = 0; u < 8; ++u) q[u] = live ? ld_stream_u4(p + u * ldx) : make_uint4(0, 0, 0, 0);
             p += 8 * ldx;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -53,14 +72,16 @@ __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M,
                 m[1] = __vmaxu2(m[1], q[u].y & 0x7FFF7FFFu);
                 m[2] = __vmaxu2(m[2], q[u].z & 0x7FFF7FFFu);
                 m[3] = __vmaxu2(m[3], q[u].w & 0x7FFF7FFFu);
+                group_max(q[u], r + u);
             }
         }
         for (; r < r1; ++r, p += ldx) {
-            const uint4 q = ld_stream_u4(p);
+            const uint4 q = live ? ld_stream_u4(p) : make_uint4(0, 0, 0, 0);
             m[0] = __vmaxu2(m[0], q.x & 0x7FFF7FFFu);
             m[1] = __vmaxu2(m[1], q.y & 0x7FFF7FFFu);
             m[2] = __vmaxu2(m[2], q.z & 0x7FFF7FFFu);
             m[3] = __vmaxu2(m[3], q.w & 0x7FFF7FFFu);
+            group_max(q, r);
         }
     }
     uint32_t bits = 0, bad = 0;
@@ -71,11 +92,10 @@ __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M,
         bits |= (hi >= thr_bits ? 1u : 0u) << (2 * i + 1);
         bad |= (lo >= 0x7C00u || hi >= 0x7C00u) ? 1u : 0u;
     }
-    const uint32_t lane = threadIdx.x & 31u;
     uint32_t word = bits << (8u * (lane & 3u));
     word |= __shfl_xor_sync(0xffffffffu, word, 1);
     word |= __shfl_xor_sync(0xffffffffu, word, 2);
-    if ((lane & 3u) == 0 && word != 0 && v < nvec) atomicOr(col_mask + (v >> 2), word);
+    if ((lane & 3u) == 0 && word != 0 && live) atomicOr(col_mask + (v >> 2), word);
     if (nonfinite != nullptr && __any_sync(0xffffffffu, bad != 0) && lane == 0)
         atomicExch(nonfinite, 1);
 }
@@ -110,9 +130,14 @@ __global__ void zero_u32_kernel(uint32_t* p, int64_t n) {
 
 // ------------------------------------------------------------------ compact
 // One block: prefix popcount over the mask words, scatter sorted indices.
+// dgrp (optional, K <= 65536): [count, 32 bitmap words of 64-column groups
+// holding an outlier column, then the list of those groups] for row_scale.
 __global__ void outlier_compact_kernel(const uint32_t* __restrict__ col_mask, int64_t K,
-                                       int32_t* __restrict__ o_idx, int32_t* __restrict__ o_count) {
+                                       int32_t* __restrict__ o_idx, int32_t* __restrict__ o_count,
+                                       int32_t* __restrict__ dgrp) {
     __shared__ int32_t warp_sums[32];
+    __shared__ uint32_t gbits[32];
+    __shared__ int32_t n_dg;
     const int64_t nwords = (K + 31) >> 5;
     const int64_t per = (nwords + blockDim.x - 1) / blockDim.x;
     const int64_t w0 = threadIdx.x * per;
@@ -150,6 +175,21 @@ __global__ void outlier_compact_kernel(const uint32_t* __restrict__ col_mask, in
         }
     }
     if (threadIdx.x == blockDim.x - 1) *o_count = pos;
+    if (dgrp == nullptr) return;
+    if (threadIdx.x < 32) gbits[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) n_dg = 0;
+    __syncthreads();
+    const int64_t ng = (K + 63) >> 6;
+    for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+        const uint32_t m1 = (2 * g + 1 < nwords) ? col_mask[2 * g + 1] : 0u;
+        if ((col_mask[2 * g] | m1) != 0u) {
+            atomicOr(&gbits[g >> 5], 1u << (g & 31));
+            dgrp[33 + atomicAdd(&n_dg, 1)] = static_cast<int32_t>(g);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) dgrp[1 + threadIdx.x] = static_cast<int32_t>(gbits[threadIdx.x]);
+    if (threadIdx.x == 0) dgrp[0] = n_dg;
 }
 
 // ------------------------------------------------------------------ K2 rows
@@ -386,6 +426,193 @@ __global__ void __launch_bounds__(256) quantize_rows_smem_kernel(
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------- K2 split form
+// With the scan's per-row 64-column group maxima (gmax), the row quantizer
+// splits into a tiny scale pass and a pure streaming code pass:
+//   row_scale    -- amax over keep columns = max of gmax over groups without an
+//                   outlier column, plus a direct re-read of the (few) groups that
+//                   hold one; writes row_amax, the f64 scale and x[:, O]
+//   quantize_bulk -- codes from a cp.async.bulk-fed shared-memory ring
+//                   (one 16-byte vector column per consumer thread).
+// Same bits as quantize_rows_* (amax on fp16 bit patterns, quant8 codes).
+// One warp per row, one memory round trip: the loads of the row's group
+// maxima, of the vectors of the dirty groups and of x[row, O] are all issued
+// before any is consumed. Dirty groups (64-column groups holding an outlier
+// column) come from outlier_compact's dgrp list; K <= 65536 (ng <= 1024).
+constexpr int RS_GM = 8;  // group maxima per lane per pass (256 groups = 16384 columns)
+__global__ void __launch_bounds__(256) row_scale_kernel(
+    const __half* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
+    const uint32_t* __restrict__ col_mask, const int32_t* __restrict__ o_idx,
+    const int32_t* __restrict__ o_count, const uint16_t* __restrict__ gmax, int64_t ng,
+    const int32_t* __restrict__ dgrp, float* __restrict__ row_amax, double* __restrict__ row_s,
+    __half* __restrict__ xo, int64_t o_cap) {
+    __shared__ uint32_t sgb[32];
+    __shared__ int32_t sdg[1024];
+    __shared__ int32_t so[64];
+    const int nd = __ldg(dgrp);
+    const int n_o = xo != nullptr ? static_cast<int>(min(static_cast<int64_t>(__ldg(o_count)), min(o_cap, static_cast<int64_t>(64)))) : 0;
+    if (threadIdx.x < 32) sgb[threadIdx.x] = static_cast<uint32_t>(__ldg(dgrp + 1 + threadIdx.x));
+    for (int k = threadIdx.x; k < nd; k += blockDim.x) sdg[k] = __ldg(dgrp + 33 + k);
+    for (int k = threadIdx.x; k < n_o; k += blockDim.x) so[k] = __ldg(o_idx + k);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nvec = K >> 3;
+    const int nd8 = nd * 8;
+    const int64_t nwarps = blockDim.x >> 5;
+    for (int64_t row = blockIdx.x * nwarps + (threadIdx.x >> 5); row < M;
+         row += static_cast<int64_t>(gridDim.x) * nwarps) {
+        const __half* xr = x + row * ldx;
+        const uint16_t* gr = gmax + row * ng;
+        // issue: first dirty pair chunk + x[row, O]
+        uint4 dq[2];
+        uint32_t dmb[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int pidx = lane + 32 * j;
+            const int64_t v = pidx < nd8 ? (static_cast<int64_t>(sdg[pidx >> 3]) << 3) + (pidx & 7) : nvec;
+            dq[j] = make_uint4(0, 0, 0, 0);
+            dmb[j] = 0xFFu;
+            if (v < nvec) {
+                dq[j] = *reinterpret_cast<const uint4*>(xr + (v << 3));
+                dmb[j] = mask_byte(col_mask, v);
+            }
+        }
+        __half ov[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int t = lane + 32 * j;
+            if (t < n_o) ov[j] = xr[so[t]];
+        }
+        uint32_t am = 0;
+        for (int64_t g0 = 0; g0 < ng; g0 += 32 * RS_GM) {
+            uint32_t gm[RS_GM];
+#pragma unroll
+            for (int j = 0; j < RS_GM; ++j) {
+                const int64_t g = g0 + lane + 32 * j;
+                gm[j] = g < ng ? static_cast<uint32_t>(gr[g]) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < RS_GM; ++j) {
+                const int64_t g = g0 + lane + 32 * j;
+                if (g < ng && !((sgb[g >> 5] >> (g & 31)) & 1u)) am = max(am, gm[j]);
+            }
+        }
+        auto keep_max = [&](const uint4& q, uint32_t mb) {
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+            uint32_t am2 = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) am2 = __vmaxu2(am2, (w4[i] & 0x7FFF7FFFu) & keep_word(mb, i));
+            am = max(am, max(am2 & 0xFFFFu, am2 >> 16));
+        };
+        keep_max(dq[0], dmb[0]);
+        keep_max(dq[1], dmb[1]);
+        for (int pidx = lane + 64; pidx < nd8; pidx += 32) {  // > 8 dirty groups
+            const int64_t v = (static_cast<int64_t>(sdg[pidx >> 3]) << 3) + (pidx & 7);
+            if (v < nvec) keep_max(*reinterpret_cast<const uint4*>(xr + (v << 3)), mask_byte(col_mask, v));
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int t = lane + 32 * j;
+            if (t < n_o) xo[row * o_cap + t] = ov[j];
+        }
+        for (int t = lane + 64; t < min(static_cast<int64_t>(__ldg(o_count)), o_cap) && xo != nullptr; t += 32)
+            xo[row * o_cap + t] = xr[o_idx[t]];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) am = max(am, __shfl_xor_sync(0xffffffffu, am, d));
+        if (lane == 0) {
+            const float amax = __half2float(__ushort_as_half(static_cast<unsigned short>(am)));
+            row_amax[row] = amax;
+            row_s[row] = scale_of(amax);
+        }
+    }
+}
+
+// Bulk-copy fed code pass: persistent CTAs (2 per SM), a producer lane streams
+// 8-row x 2048-column tiles of X into a QS_STAGES-deep shared-memory ring with
+// cp.async.bulk (the copy engine keeps up to QS_STAGES x 32 KB per CTA in
+// flight, independent of the register file); 8 consumer warps quantize one
+// 16-byte vector column per thread and store the codes (8 bytes, coalesced).
+constexpr int QS_ROWS = 8, QS_VECS = 256, QS_STAGES = 3;
+constexpr int QS_STAGE_BYTES = QS_ROWS * QS_VECS * 16;
+
+__global__ void __launch_bounds__(288) quantize_bulk_kernel(
+    const __half* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
+    const uint32_t* __restrict__ col_mask, const double* __restrict__ row_s,
+    int8_t* __restrict__ xq, int64_t ldq) {
+    extern __shared__ __align__(128) uint8_t qb_sm[];
+    __shared__ __align__(8) uint64_t full[QS_STAGES], empty[QS_STAGES];
+    const int64_t nvec = K >> 3;
+    const int64_t ncb = (nvec + QS_VECS - 1) / QS_VECS;
+    const int64_t ntiles = ((M + QS_ROWS - 1) / QS_ROWS) * ncb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < QS_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 8);
+        }
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+    if (warp == 8) {  // producer
+        if (lane == 0) {
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+                const int s = i % QS_STAGES;
+                if (i >= QS_STAGES) mbar_wait(&empty[s], ((i / QS_STAGES) - 1) & 1);
+                const int64_t r0 = (t / ncb) * QS_ROWS, v0 = (t % ncb) * QS_VECS;
+                const int rows = static_cast<int>(min(static_cast<int64_t>(QS_ROWS), M - r0));
+                const uint32_t seg = static_cast<uint32_t>(min(static_cast<int64_t>(QS_VECS), nvec - v0)) * 16u;
+                mbar_arrive_expect_tx(&full[s], seg * rows);
+                uint8_t* dst = qb_sm + s * QS_STAGE_BYTES;
+                for (int u = 0; u < rows; ++u)
+                    bulk_load_1d(dst + u * QS_VECS * 16, x + (r0 + u) * ldx + (v0 << 3), seg, &full[s]);
+            }
+        }
+        return;
+    }
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int s = i % QS_STAGES;
+        const int64_t r0 = (t / ncb) * QS_ROWS, v = (t % ncb) * QS_VECS + threadIdx.x;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(QS_ROWS), M - r0));
+        double sc[QS_ROWS];
+        if (rows == QS_ROWS) {
+#pragma unroll
+            for (int u = 0; u < QS_ROWS; ++u) sc[u] = __ldg(row_s + r0 + u);
+        }
+        const uint32_t mb = v < nvec ? mask_byte(col_mask, v) : 0u;
+        mbar_wait(&full[s], (i / QS_STAGES) & 1);
+        if (v < nvec) {
+            const uint4* src = reinterpret_cast<const uint4*>(qb_sm + s * QS_STAGE_BYTES) + threadIdx.x;
+            int8_t* o = xq + r0 * ldq + (v << 3);
+            if (rows == QS_ROWS) {
+                uint4 q[QS_ROWS];
+#pragma unroll
+                for (int u = 0; u < QS_ROWS; ++u) q[u] = src[u * QS_VECS];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+                for (int u = 0; u < QS_ROWS; ++u)
+                    *reinterpret_cast<uint2*>(o + u * ldq) = quant8(q[u], mb, static_cast<float>(sc[u]), sc[u]);
+            } else {
+                for (int u = 0; u < rows; ++u) {
+                    const double su = __ldg(row_s + r0 + u);
+                    *reinterpret_cast<uint2*>(o + u * ldq) =
+                        quant8(src[u * QS_VECS], mb, static_cast<float>(su), su);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            if (v == nvec - 1 && ldq > K)
+                for (int u = 0; u < rows; ++u)
+                    for (int64_t k = K; k < ldq; ++k) xq[(r0 + u) * ldq + k] = 0;
+        } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+}
+
 // Generic path (any K / alignment): two passes over the row from global.
 __global__ void quantize_rows_scalar_kernel(const __half* __restrict__ x, int64_t K, int64_t ldx,
                                             const uint32_t* __restrict__ col_mask,
@@ -473,8 +700,8 @@ cudaError_t launch_outlier_scan(const __half* x, int64_t M, int64_t K, int64_t l
         const int64_t nvec = K >> 3;
         const int64_t cb = (nvec + 255) / 256;
         const int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
-        outlier_scan_vec_kernel<<<dim3(static_cast<unsigned>(cb), rb), 256, 0, st>>>(
-            x, M, K, ldx, alpha_threshold_bits(alpha), rpb, col_mask, nonfinite);
+        outlier_scan_vec_kernel<false><<<dim3(static_cast<unsigned>(cb), rb), 256, 0, st>>>(
+            x, M, K, ldx, alpha_threshold_bits(alpha), rpb, col_mask, nonfinite, nullptr, 0);
     } else {
         const int64_t cb = (K + 255) / 256;
         const int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
@@ -487,7 +714,7 @@ cudaError_t launch_outlier_scan(const __half* x, int64_t M, int64_t K, int64_t l
 
 cudaError_t launch_outlier_compact(const uint32_t* col_mask, int64_t K, int32_t* o_idx,
                                    int32_t* o_count, cudaStream_t st) {
-    outlier_compact_kernel<<<1, 1024, 0, st>>>(col_mask, K, o_idx, o_count);
+    outlier_compact_kernel<<<1, 1024, 0, st>>>(col_mask, K, o_idx, o_count, nullptr);
     count_launch();
     return cudaGetLastError();
 }
@@ -551,6 +778,63 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
         case 8: launch_qrows<8>(t, x, M, K, ldx, mask, o_idx, o_count, xq, ldq, amax, xo, o_cap, st); break;
         default: launch_qrows<16>(t, x, M, K, ldx, mask, o_idx, o_count, xq, ldq, amax, xo, o_cap, st); break;
     }
+    count_launch();
+    return cudaGetLastError();
+}
+
+bool row_prologue_split_ok(int64_t K, int64_t ldx, int64_t ldq, const void* x, const void* xq) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("I8MM_QUANT_SPLIT");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    return env == 1 && K % 8 == 0 && ldx % 8 == 0 && ldq % 8 == 0 && K <= 65536 &&
+           (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (reinterpret_cast<uintptr_t>(xq) & 7u) == 0;
+}
+
+size_t row_prologue_scratch_bytes(int64_t M, int64_t K) {
+    const int64_t ng = (K + 63) >> 6;
+    return static_cast<size_t>(((M * ng * 2 + 255) / 256) * 256 + M * 8 + (33 + ng) * 4);
+}
+
+cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
+                                uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
+                                int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
+                                void* scratch, cudaStream_t st) {
+    cudaError_t e;
+    if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq)) {
+        if ((e = launch_outlier_scan(x, M, K, ldx, alpha, mask, nullptr, st))) return e;
+        if ((e = launch_outlier_compact(mask, K, o_idx, o_count, st))) return e;
+        return launch_quantize_rows(x, M, K, ldx, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, st);
+    }
+    const int64_t nwords = (K + 31) >> 5, nvec = K >> 3, ng = (K + 63) >> 6;
+    uint16_t* gmax = static_cast<uint16_t*>(scratch);
+    double* row_s = reinterpret_cast<double*>(static_cast<char*>(scratch) + ((M * ng * 2 + 255) / 256) * 256);
+    int32_t* dgrp = reinterpret_cast<int32_t*>(row_s + M);
+    const int sms = num_sms();
+    zero_u32_kernel<<<static_cast<unsigned>(imin64((nwords + 255) / 256, 1024)), 256, 0, st>>>(mask, nwords);
+    count_launch();
+    const int64_t cb = (nvec + 255) / 256;
+    int64_t rpb;
+    int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
+    outlier_scan_vec_kernel<true><<<dim3(static_cast<unsigned>(cb), rb), 256, 0, st>>>(
+        x, M, K, ldx, alpha_threshold_bits(alpha), rpb, mask, nullptr, gmax, ng);
+    count_launch();
+    outlier_compact_kernel<<<1, 1024, 0, st>>>(mask, K, o_idx, o_count, dgrp);
+    count_launch();
+    const int64_t rs_grid = imin64((M + 7) / 8, static_cast<int64_t>(sms) * 8);
+    row_scale_kernel<<<static_cast<unsigned>(rs_grid), 256, 0, st>>>(
+        x, M, K, ldx, mask, o_idx, o_count, gmax, ng, dgrp, row_amax, row_s, xo, o_cap);
+    count_launch();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(quantize_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             QS_STAGES * QS_STAGE_BYTES);
+        configured = true;
+    }
+    const int64_t ntiles = ((M + QS_ROWS - 1) / QS_ROWS) * ((nvec + QS_VECS - 1) / QS_VECS);
+    const unsigned g = static_cast<unsigned>(imin64(ntiles, static_cast<int64_t>(sms) * 2));
+    quantize_bulk_kernel<<<g, 288, QS_STAGES * QS_STAGE_BYTES, st>>>(x, M, K, ldx, mask, row_s, xq, ldq);
     count_launch();
     return cudaGetLastError();
 }

@@ -48,7 +48,8 @@ def test_library_exports_every_declared_symbol():
 
 def test_library_is_sm100a_tcgen05():
     """The shipped code is sm_100a SASS with tcgen05 MMA (incl. CTA pairs), TMEM
-    loads, TMA loads and TMA stores (the fp16 epilogue)."""
+    loads, TMA loads and TMA stores (the fp16 epilogue), and the bulk-copy (UBLKCP)
+    ring that feeds the row quantizer."""
     from paper_2208_07339_b200 import _native
 
     r = subprocess.run(["cuobjdump", "-sass", str(_native.LIB_PATH)], capture_output=True, text=True)
@@ -56,7 +57,7 @@ def test_library_is_sm100a_tcgen05():
         pytest.skip("cuobjdump unavailable")
     sass = r.stdout
     assert "sm_100a" in sass
-    for mnemonic in ("UTCIMMA", "LDTM", "UTMALDG", "UTMASTG", "UTCIMMA.2CTA"):
+    for mnemonic in ("UTCIMMA", "LDTM", "UTMALDG", "UTMASTG", "UTCIMMA.2CTA", "UBLKCP"):
         assert mnemonic in sass, mnemonic
 
 
