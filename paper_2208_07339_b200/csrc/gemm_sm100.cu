@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if constexpr (C::CLUSTER > 1) cluster_sync_all();  // peer barriers initialised + TMEM allocated
     tc_fence_after();
     const uint32_t tmem_base = bars->tmem_slot;
+    pdl_wait();  // setup above overlaps the predecessor's tail (programmatic dependent launch)
+    pdl_trigger();
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -645,11 +647,13 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     std::call_once(once, [&] {
@@ -670,6 +674,7 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
     if (attr_err != cudaSuccess) return attr_err;
     const int64_t clusters = max_tiles < max_clusters ? max_tiles : max_clusters;
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, tp, ty, p);
     count_launch();
     if (e != cudaSuccess) return e;

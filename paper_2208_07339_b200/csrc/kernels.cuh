@@ -9,6 +9,25 @@ namespace i8mm {
 // launch accounting + device properties (capi.cu)
 void count_launch();
 int num_sms();
+bool pdl_enabled();  // I8MM_PDL (default 1)
+
+// Launch with programmatic dependent launch allowed (see pdl_wait in
+// sm100_ptx.cuh); the kernel must call pdl_wait() before touching memory.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 cudaError_t launch_outlier_scan(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                                 uint32_t* col_mask, int32_t* nonfinite, cudaStream_t st);

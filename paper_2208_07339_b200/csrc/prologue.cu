@@ -38,6 +38,8 @@ __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M,
                                         uint32_t* __restrict__ col_mask,
                                         int32_t* __restrict__ nonfinite,
                                         uint16_t* __restrict__ gmax, int64_t ng) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // vector col
     const int64_t nvec = K >> 3;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_block;
@@ -123,6 +125,8 @@ __global__ void outlier_scan_scalar_kernel(const __half* __restrict__ x, int64_t
 }
 
 __global__ void zero_u32_kernel(uint32_t* p, int64_t n) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         p[i] = 0u;
@@ -138,6 +142,8 @@ __global__ void outlier_compact_kernel(const uint32_t* __restrict__ col_mask, in
     __shared__ int32_t warp_sums[32];
     __shared__ uint32_t gbits[32];
     __shared__ int32_t n_dg;
+    pdl_wait();
+    pdl_trigger();
     const int64_t nwords = (K + 31) >> 5;
     const int64_t per = (nwords + blockDim.x - 1) / blockDim.x;
     const int64_t w0 = threadIdx.x * per;
@@ -449,6 +455,8 @@ __global__ void __launch_bounds__(256) row_scale_kernel(
     __shared__ uint32_t sgb[32];
     __shared__ int32_t sdg[1024];
     __shared__ int32_t so[64];
+    pdl_wait();
+    pdl_trigger();
     const int nd = __ldg(dgrp);
     const int n_o = xo != nullptr ? static_cast<int>(min(static_cast<int64_t>(__ldg(o_count)), min(o_cap, static_cast<int64_t>(64)))) : 0;
     if (threadIdx.x < 32) sgb[threadIdx.x] = static_cast<uint32_t>(__ldg(dgrp + 1 + threadIdx.x));
@@ -553,6 +561,8 @@ __global__ void __launch_bounds__(288) quantize_bulk_kernel(
         fence_mbarrier_init();
     }
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
     if (warp == 8) {  // producer
         if (lane == 0) {
             int i = 0;
@@ -812,19 +822,28 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     double* row_s = reinterpret_cast<double*>(static_cast<char*>(scratch) + ((M * ng * 2 + 255) / 256) * 256);
     int32_t* dgrp = reinterpret_cast<int32_t*>(row_s + M);
     const int sms = num_sms();
-    zero_u32_kernel<<<static_cast<unsigned>(imin64((nwords + 255) / 256, 1024)), 256, 0, st>>>(mask, nwords);
+    if ((e = launch_pdl(zero_u32_kernel, dim3(static_cast<unsigned>(imin64((nwords + 255) / 256, 1024))),
+                        dim3(256), 0, st, mask, nwords)))
+        return e;
     count_launch();
     const int64_t cb = (nvec + 255) / 256;
     int64_t rpb;
     int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
-    outlier_scan_vec_kernel<true><<<dim3(static_cast<unsigned>(cb), rb), 256, 0, st>>>(
-        x, M, K, ldx, alpha_threshold_bits(alpha), rpb, mask, nullptr, gmax, ng);
+    if ((e = launch_pdl(outlier_scan_vec_kernel<true>, dim3(static_cast<unsigned>(cb), rb), dim3(256), 0, st,
+                        x, M, K, ldx, alpha_threshold_bits(alpha), rpb, mask,
+                        static_cast<int32_t*>(nullptr), gmax, ng)))
+        return e;
     count_launch();
-    outlier_compact_kernel<<<1, 1024, 0, st>>>(mask, K, o_idx, o_count, dgrp);
+    if ((e = launch_pdl(outlier_compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const uint32_t*>(mask),
+                        K, o_idx, o_count, dgrp)))
+        return e;
     count_launch();
     const int64_t rs_grid = imin64((M + 7) / 8, static_cast<int64_t>(sms) * 8);
-    row_scale_kernel<<<static_cast<unsigned>(rs_grid), 256, 0, st>>>(
-        x, M, K, ldx, mask, o_idx, o_count, gmax, ng, dgrp, row_amax, row_s, xo, o_cap);
+    if ((e = launch_pdl(row_scale_kernel, dim3(static_cast<unsigned>(rs_grid)), dim3(256), 0, st, x, M, K,
+                        ldx, static_cast<const uint32_t*>(mask), static_cast<const int32_t*>(o_idx),
+                        static_cast<const int32_t*>(o_count), static_cast<const uint16_t*>(gmax), ng,
+                        static_cast<const int32_t*>(dgrp), row_amax, row_s, xo, o_cap)))
+        return e;
     count_launch();
     static bool configured = false;
     if (!configured) {
@@ -834,7 +853,9 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     }
     const int64_t ntiles = ((M + QS_ROWS - 1) / QS_ROWS) * ((nvec + QS_VECS - 1) / QS_VECS);
     const unsigned g = static_cast<unsigned>(imin64(ntiles, static_cast<int64_t>(sms) * 2));
-    quantize_bulk_kernel<<<g, 288, QS_STAGES * QS_STAGE_BYTES, st>>>(x, M, K, ldx, mask, row_s, xq, ldq);
+    if ((e = launch_pdl(quantize_bulk_kernel, dim3(g), dim3(288), QS_STAGES * QS_STAGE_BYTES, st, x, M, K, ldx,
+                        static_cast<const uint32_t*>(mask), static_cast<const double*>(row_s), xq, ldq)))
+        return e;
     count_launch();
     return cudaGetLastError();
 }

@@ -22,6 +22,7 @@
 
 #include "kernels.cuh"
 #include "quant_common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace i8mm {
 
@@ -88,6 +89,8 @@ __global__ void amax_bits_to_float_kernel(uint32_t* a, int64_t n) {
 }
 
 __global__ void zero_words_kernel(uint32_t* p, int64_t n) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         p[i] = 0u;
@@ -179,6 +182,8 @@ __global__ void __launch_bounds__(256) quantize_cols_t_kernel(
 __global__ void gather_rows_kernel(const __half* __restrict__ w, int64_t ldw, int64_t N,
                                    const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
                                    int64_t cap, __half* __restrict__ out, int64_t ldo, int vec) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t t = blockIdx.y;
     const int64_t n = imin64(static_cast<int64_t>(*count), cap);
     if (t >= n) return;
@@ -295,6 +300,8 @@ __global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N,
                              const uint16_t* __restrict__ cand_v, const int32_t* __restrict__ cand_r,
                              int32_t* __restrict__ p_count, int32_t* __restrict__ p_idx,
                              float* __restrict__ p_amax, int32_t* __restrict__ p_src) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= N) return;
     const int32_t r0 = cand_r[j];
@@ -342,6 +349,8 @@ __global__ void __launch_bounds__(256) patch_quantize_kernel(
     const int32_t* __restrict__ p_count, const int32_t* __restrict__ p_idx,
     const float* __restrict__ p_amax, const int32_t* __restrict__ p_src,
     const int8_t* __restrict__ q2, int8_t* __restrict__ wq_p, int64_t ldq) {
+    pdl_wait();
+    pdl_trigger();
     const int32_t np = *p_count;
     const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 2048 + threadIdx.x * 8;
     if (k0 >= ldq) return;
@@ -433,10 +442,10 @@ cudaError_t launch_gather_rows(const __half* w, int64_t ldw, int64_t N, const in
     const int vec = (N % 8 == 0) && (ldw % 8 == 0) && (ldo % 8 == 0) && aligned16(w) && aligned16(out);
     const int64_t per = vec ? (N >> 3) : N;
     const unsigned gx = static_cast<unsigned>(imin64((per + 255) / 256, 64));
-    gather_rows_kernel<<<dim3(gx, static_cast<unsigned>(cap)), 256, 0, st>>>(w, ldw, N, idx, count,
-                                                                              cap, out, ldo, vec);
+    cudaError_t e = launch_pdl(gather_rows_kernel, dim3(gx, static_cast<unsigned>(cap)), dim3(256), 0, st,
+                               w, ldw, N, idx, count, cap, out, ldo, vec);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 int64_t topt_chunk_rows(int64_t K) { return K < 512 ? (K > 0 ? K : 1) : 512; }
@@ -474,15 +483,20 @@ cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t l
                                 int32_t* p_count, int32_t* p_idx, float* p_amax, int32_t* p_src,
                                 int8_t* wq_p, int64_t ldq, cudaStream_t st) {
     const int64_t zw = 4 + (N + 31) / 32;  // count + patched-column mask
-    zero_words_kernel<<<static_cast<unsigned>(imin64((zw + 255) / 256, 64)), 256, 0, st>>>(
-        reinterpret_cast<uint32_t*>(p_count), zw);
+    cudaError_t e;
+    if ((e = launch_pdl(zero_words_kernel, dim3(static_cast<unsigned>(imin64((zw + 255) / 256, 64))), dim3(256),
+                        0, st, reinterpret_cast<uint32_t*>(p_count), zw)))
+        return e;
     count_launch();
-    fixup_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(
-        w, K, N, ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax, p_src);
+    if ((e = launch_pdl(fixup_kernel, dim3(static_cast<unsigned>((N + 255) / 256)), dim3(256), 0, st, w, K, N,
+                        ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax, p_src)))
+        return e;
     count_launch();
     const dim3 pgrid(static_cast<unsigned>((ldq + 2047) / 2048), static_cast<unsigned>(imin64(N, 256)));
-    patch_quantize_kernel<<<pgrid, 256, 0, st>>>(w, K, ldw, mask, p_count, p_idx, p_amax, p_src, q2,
-                                                 wq_p, ldq);
+    if ((e = launch_pdl(patch_quantize_kernel, pgrid, dim3(256), 0, st, w, K, ldw, mask,
+                        static_cast<const int32_t*>(p_count), static_cast<const int32_t*>(p_idx),
+                        static_cast<const float*>(p_amax), static_cast<const int32_t*>(p_src), q2, wq_p, ldq)))
+        return e;
     count_launch();
     return cudaGetLastError();
 }
