@@ -310,7 +310,11 @@ def run_ours(args, layers, wl) -> None:
     ops = sum(2.0 * m * n * k for m, k, n in layers)
     timer = EventTimer()
 
-    def step():
+    def step():  # the timed step: no events inside (kernels chain with PDL)
+        for mod, x in zip(mods, xs):
+            mod(x)
+
+    def step_gemm_marked():  # separate pass: events around each GEMM for its share
         for mod, x in zip(mods, xs):
             mod(x, _timer=timer)
 
@@ -318,7 +322,7 @@ def run_ours(args, layers, wl) -> None:
 
     def step_e2e():
         if hostio is not None:  # copies overlapped with compute (and with each other)
-            hostio.run(list(zip(mods, xs_host, ys_host)))
+            hostio.run(list(zip(mods, xs_host, ys_host)), inputs_ready=True)
             return
         for mod, xh, yh in zip(mods, xs_host, ys_host):
             x = xh.to(dev, non_blocking=True)
@@ -349,12 +353,16 @@ def run_ours(args, layers, wl) -> None:
         step()
     torch.cuda.synchronize()
     launches0 = _native.launch_count()
-    timer.enabled = True
     with ClockSampler(local_rank) as clk:
         ms = timed(step, args.steps)
-    timer.enabled = False
     launches = _native.launch_count() - launches0
-    gemm_ms = timer.total_ms() / args.steps  # per step, this rank
+    g_steps = max(1, min(args.steps, 20))
+    timer.enabled = True
+    for _ in range(g_steps):
+        step_gemm_marked()
+    torch.cuda.synchronize()
+    timer.enabled = False
+    gemm_ms = timer.total_ms() / g_steps  # per step, this rank
     ms_step = ms / args.steps
     value = ops / (ms_step * 1e-3) / 1e12
 
@@ -382,6 +390,8 @@ def run_ours(args, layers, wl) -> None:
         # + X + Y + fp16 outlier rows (6 planted) + column amax, over the decode kernels' time
         hbm = peaks.get("hbm_gbs", 6543.7)
         byts = sum(k * n + 2 * m * k + 2 * m * n + 2 * 6 * n + 4 * n for m, k, n in layers)
+        # the decode kernel IS the layer (one launch): time it from the unmarked step
+        gemm_ms = ms_step
         ach = byts / (gemm_ms * 1e-3) / 1e9
         roofline = {
             "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
@@ -489,7 +499,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--cpu-sample-rows", type=int, default=0, help="0 = auto-size the sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparators", action="store_true")

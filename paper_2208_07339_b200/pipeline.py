@@ -39,9 +39,17 @@ class HostIOPipeline:
         self.h2d = torch.cuda.Stream(device=self.device)
         self.d2h = torch.cuda.Stream(device=self.device)
 
-    def run(self, calls: list[tuple[Int8Linear, torch.Tensor, torch.Tensor]]) -> None:
+    def run(self, calls: list[tuple[Int8Linear, torch.Tensor, torch.Tensor]],
+            inputs_ready: bool = False) -> None:
+        """Enqueue the calls. By default the input copies wait for the caller's
+        current stream (it may still be producing the host inputs, e.g. a D2H
+        into ``x_host``). ``inputs_ready=True`` asserts the host inputs are
+        already final, so this batch's input copies start at once and overlap
+        the previous batch's compute and output copies (a serving loop over
+        independent batches)."""
         compute = torch.cuda.current_stream(self.device)
-        self.h2d.wait_stream(compute)  # host buffers may be rewritten after the last sync
+        if not inputs_ready:
+            self.h2d.wait_stream(compute)
         staged = []
         with torch.cuda.stream(self.h2d):
             for _, xh, _ in calls:

@@ -660,3 +660,32 @@ def test_host_io_pipeline_matches_device_calls(p, oracle_mod):
         torch.cuda.synchronize()
         for y, r in zip(ys, refs):
             assert torch.equal(y, r)
+
+
+def test_host_io_pipeline_back_to_back_batches(p, oracle_mod):
+    """inputs_ready=True: consecutive batches overlap (batch b+1's input copies
+    start while batch b computes and copies out); every batch's outputs still
+    equal the device path bitwise."""
+    shapes = [(700, 512, 300), (700, 300, 512)]
+    mods = []
+    for i, (m, k, n) in enumerate(shapes):
+        _, w = oracle_mod.planted_pair(m, k, n, 4, 20.0, 50 + i)
+        mods.append(p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda()))
+    batches = []
+    for b in range(3):
+        xs, ys, refs = [], [], []
+        for i, ((m, k, n), mod) in enumerate(zip(shapes, mods)):
+            x, _ = oracle_mod.planted_pair(m, k, n, 4, 20.0, 60 + 10 * b + i)
+            x16 = torch.from_numpy(x.astype(np.float16))
+            xs.append(x16.pin_memory())
+            refs.append(mod(x16.cuda()).cpu())
+            ys.append(torch.zeros(refs[-1].shape, dtype=refs[-1].dtype).pin_memory())
+        batches.append((xs, ys, refs))
+    torch.cuda.synchronize()
+    pipe = p.HostIOPipeline(chunks=2)
+    for xs, ys, _ in batches:
+        pipe.run(list(zip(mods, xs, ys)), inputs_ready=True)
+    torch.cuda.synchronize()
+    for _, ys, refs in batches:
+        for y, r in zip(ys, refs):
+            assert torch.equal(y, r)
