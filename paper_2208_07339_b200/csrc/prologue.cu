@@ -792,6 +792,309 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------- K1+K2 one-read form
+// One HBM read of X (SURVEY 8(d) "1-read"): persistent CTAs stream blocks of
+// RB whole rows into a shared-memory ring (cp.async.bulk, one copy per row);
+// per block the consumer warps
+//   1. scan the block's columns (|x| >= alpha on fp16 bits) and publish new
+//      outlier columns to the running global mask F (atomicOr only for bits
+//      not yet set),
+//   2. snapshot F (S_b: it holds every column flagged so far, including the
+//      block's own) and store S_b with its popcount,
+//   3. quantize the rows against S_b: amax over keep columns, codes (quant8),
+//      all from shared memory.
+// S_b is a subset of the final mask F, so rows of a block quantized before some
+// column was flagged elsewhere are corrected exactly by rp1_finalize_kernel:
+// codes at the late columns are zeroed, and a row whose amax may have sat in a
+// late column is re-quantized from X. When outlier features show up in most
+// row blocks (they do in LLM activations and in planted_pair) S_b == F for
+// nearly every block and the finalize pass only gathers x[:, O].
+constexpr int RP1_THREADS = 544;  // 16 consumer warps + 1 producer warp
+constexpr int RP1_CONSUMERS = 512;
+constexpr int RP1_MAX_STAGES = 4;
+constexpr int RP1_BLOCK_VECS = 4096;       // 16-byte vectors per block (64 KB)
+constexpr int RP1_VPT = RP1_BLOCK_VECS / RP1_CONSUMERS;  // vectors per consumer thread (registers)
+constexpr int RP1_SMEM_RING = 200 * 1024;  // ring bytes (row blocks + their mask views)
+
+struct Rp1Geom {
+    int rb;          // rows per block (power of two, <= 16)
+    int tpr;         // consumer threads per row = RP1_CONSUMERS / rb
+    int view_bytes;  // mask view per stage (nwords rounded up to 16 bytes)
+    int stage_bytes; // rb rows + view
+    int stages;
+    int64_t nblk;
+};
+
+__host__ __device__ inline Rp1Geom rp1_geom(int64_t M, int64_t K) {
+    Rp1Geom g{};
+    const int64_t nv = K >> 3;
+    int64_t p2 = 1;
+    while (p2 < nv) p2 <<= 1;
+    int64_t rb = RP1_BLOCK_VECS / p2;
+    if (rb < 1) rb = 1;
+    if (rb > 16) rb = 16;
+    g.rb = static_cast<int>(rb);
+    g.tpr = RP1_CONSUMERS / g.rb;
+    const int64_t nwords = (K + 31) >> 5;
+    g.view_bytes = static_cast<int>(((nwords * 4 + 15) / 16) * 16);
+    const int64_t row_part = ((rb * K * 2 + 127) / 128) * 128;
+    g.stage_bytes = static_cast<int>(row_part + ((g.view_bytes + 127) / 128) * 128);
+    int64_t st = RP1_SMEM_RING / g.stage_bytes;
+    if (st > RP1_MAX_STAGES) st = RP1_MAX_STAGES;
+    g.stages = static_cast<int>(st);
+    g.nblk = (M + rb - 1) / rb;
+    return g;
+}
+
+// Per block: the producer lands RB rows (one bulk copy each) plus a copy of
+// the running mask F (the block's snapshot S_b, taken when the copy is
+// issued). Consumers (256 / RB threads per row):
+//   pass A: keep amax of the row against S_b; elements >= alpha in a column
+//           outside S_b publish that column to F (atomicOr; rare once F holds
+//           the layer's outlier features) -- such rows are then corrected by
+//           rp1_finalize_kernel, like every row of a block whose S_b missed a
+//           column of the final F;
+//   pass B: codes (quant8) from shared memory, 8-byte stores.
+// S_b and its popcount are stored for the finalize pass.
+template <int RB>
+__global__ void __launch_bounds__(RP1_THREADS, 1) rp1_stream_kernel(
+    const __half* __restrict__ x, int64_t M, int64_t K, int64_t ldx, uint32_t thr_bits,
+    uint32_t* __restrict__ fmask, uint32_t* __restrict__ snap, int32_t* __restrict__ snap_cnt,
+    int8_t* __restrict__ xq, int64_t ldq, float* __restrict__ row_amax) {
+    extern __shared__ __align__(128) uint8_t rp_sm[];
+    __shared__ __align__(8) uint64_t full[RP1_MAX_STAGES], empty[RP1_MAX_STAGES];
+    __shared__ uint32_t ram[3][16];  // block i uses slot i % 3 (reset two blocks ahead)
+    static_assert(RP1_CONSUMERS / 32 <= 16 * 32, "");
+    __shared__ int32_t scnt[3];
+    constexpr int TPR = RP1_CONSUMERS / RB;  // threads per row (>= 32: whole warps)
+    const Rp1Geom g = rp1_geom(M, K);
+    const int nwords = static_cast<int>((K + 31) >> 5);
+    const int nv = static_cast<int>(K >> 3);
+    const int row_part = g.stage_bytes - ((g.view_bytes + 127) / 128) * 128;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < g.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], RP1_CONSUMERS / 32);
+        }
+        fence_mbarrier_init();
+    }
+    if (threadIdx.x < 48) ram[threadIdx.x >> 4][threadIdx.x & 15] = 0u;
+    if (threadIdx.x < 3) scnt[threadIdx.x] = 0;
+    __syncthreads();
+    pdl_wait();
+    pdl_trigger();
+    if (warp == RP1_CONSUMERS / 32) {  // producer
+        if (lane == 0) {
+            int i = 0;
+            for (int64_t b = blockIdx.x; b < g.nblk; b += gridDim.x, ++i) {
+                const int s = i % g.stages;
+                if (i >= g.stages)  // back off between polls: the spin would steal issue slots
+                    while (!mbar_try_wait(&empty[s], ((i / g.stages) - 1) & 1)) __nanosleep(64);
+                const int64_t r0 = b * RB;
+                const int rows = static_cast<int>(min(static_cast<int64_t>(RB), M - r0));
+                mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows * K * 2 + g.view_bytes));
+                uint8_t* dst = rp_sm + static_cast<size_t>(s) * g.stage_bytes;
+                bulk_load_1d(dst + row_part, fmask, static_cast<uint32_t>(g.view_bytes), &full[s]);
+                for (int u = 0; u < rows; ++u)
+                    bulk_load_1d(dst + u * K * 2, x + (r0 + u) * ldx, static_cast<uint32_t>(K * 2), &full[s]);
+            }
+        }
+        return;
+    }
+    const int tid = threadIdx.x;
+    const int rl = tid / TPR, tr = tid % TPR;  // row within the block, thread within the row
+    const uint32_t thr2 = thr_bits | (thr_bits << 16);
+    int i = 0;
+    for (int64_t b = blockIdx.x; b < g.nblk; b += gridDim.x, ++i) {
+        // slot (i+1)%3 was last read by block i-2, before block i-1's barrier
+        const int s = i % g.stages, par = i % 3, nxt = (i + 1) % 3;
+        const int64_t r0 = b * RB;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(RB), M - r0));
+        if (tid < 16) ram[nxt][tid] = 0u;
+        if (tid == 0) scnt[nxt] = 0;
+        mbar_wait(&full[s], (i / g.stages) & 1);
+        const uint8_t* base = rp_sm + static_cast<size_t>(s) * g.stage_bytes;
+        const uint32_t* view = reinterpret_cast<const uint32_t*>(base + row_part);
+        const uint4* rowv = reinterpret_cast<const uint4*>(base) + static_cast<int64_t>(rl) * nv;
+        const bool live = rl < rows;
+        // snapshot S_b -> global (for the finalize pass)
+        int32_t pc = 0;
+        for (int w = tid; w < nwords; w += RP1_CONSUMERS) {
+            const uint32_t f = view[w];
+            snap[b * nwords + w] = f;
+            pc += __popc(f);
+        }
+        if (pc) atomicAdd(&scnt[par], pc);
+        // the thread's (at most 8) vectors of its row and their mask bytes -> registers
+        uint4 q[RP1_VPT];
+        uint32_t mbv[RP1_VPT];
+#pragma unroll
+        for (int j = 0; j < RP1_VPT; ++j) {
+            const int v = tr + j * TPR;
+            const bool ok = live && v < nv;
+            q[j] = ok ? rowv[v] : make_uint4(0, 0, 0, 0);
+            mbv[j] = ok ? (view[v >> 2] >> (8 * (v & 3))) & 0xFFu : 0xFFu;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // stage consumed: the producer may refill it
+        // keep amax + detection of columns outside S_b
+        uint32_t am2 = 0;
+#pragma unroll
+        for (int j = 0; j < RP1_VPT; ++j) {
+            const uint32_t w4[4] = {q[j].x & 0x7FFF7FFFu, q[j].y & 0x7FFF7FFFu, q[j].z & 0x7FFF7FFFu,
+                                    q[j].w & 0x7FFF7FFFu};
+            const uint32_t m = __vmaxu2(__vmaxu2(w4[0], w4[1]), __vmaxu2(w4[2], w4[3]));
+            const uint32_t mb = mbv[j];
+            uint32_t mk = m;
+            if (mb != 0u)
+                mk = __vmaxu2(__vmaxu2(w4[0] & keep_word(mb, 0), w4[1] & keep_word(mb, 1)),
+                              __vmaxu2(w4[2] & keep_word(mb, 2), w4[3] & keep_word(mb, 3)));
+            am2 = __vmaxu2(am2, mk);
+            if (max(m & 0xFFFFu, m >> 16) >= thr_bits) {  // an element >= alpha
+                uint32_t hit = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t c = __vcmpgeu2(w4[e], thr2);
+                    hit |= ((c & 1u) << (2 * e)) | (((c >> 16) & 1u) << (2 * e + 1));
+                }
+                hit &= ~mb;
+                const int v = tr + j * TPR;
+                if (hit) atomicOr(fmask + (v >> 2), hit << (8 * (v & 3)));
+            }
+        }
+        uint32_t am = max(am2 & 0xFFFFu, am2 >> 16);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) am = max(am, __shfl_xor_sync(0xffffffffu, am, d));
+        if (live && lane == 0 && am) atomicMax(&ram[par][rl], am);
+        named_bar_sync(1, RP1_CONSUMERS);
+        if (tid == 0) snap_cnt[b] = scnt[par];
+        // codes from registers
+        if (live) {
+            const float amax = __half2float(__ushort_as_half(static_cast<unsigned short>(ram[par][rl])));
+            const double sc = scale_of(amax);
+            const float s32 = static_cast<float>(sc);
+            int8_t* qr = xq + (r0 + rl) * ldq;
+#pragma unroll
+            for (int j = 0; j < RP1_VPT; ++j) {
+                const int v = tr + j * TPR;
+                if (v < nv) *reinterpret_cast<uint2*>(qr + 8 * v) = quant8(q[j], mbv[j], s32, sc);
+            }
+            if (tr == 0) {
+                row_amax[r0 + rl] = amax;
+                for (int64_t k = K; k < ldq; ++k) qr[k] = 0;
+            }
+        }
+    }
+}
+
+// Final mask F -> sorted o_idx / o_count (block 0), x[:, O] for every row, and
+// the exact correction of blocks whose snapshot S_b missed columns of F.
+__global__ void __launch_bounds__(256) rp1_finalize_kernel(
+    const __half* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
+    const uint32_t* __restrict__ fmask, const uint32_t* __restrict__ snap,
+    const int32_t* __restrict__ snap_cnt, int rb, int32_t* __restrict__ o_idx,
+    int32_t* __restrict__ o_count, int8_t* __restrict__ xq, int64_t ldq,
+    float* __restrict__ row_amax, __half* __restrict__ xo, int64_t o_cap) {
+    extern __shared__ __align__(16) uint32_t fz_sm[];
+    __shared__ int32_t warp_sums[32];
+    __shared__ int32_t n_f;
+    pdl_wait();
+    pdl_trigger();
+    const int nwords = static_cast<int>((K + 31) >> 5);
+    uint32_t* sf = fz_sm;                                     // F
+    int32_t* scol = reinterpret_cast<int32_t*>(fz_sm + nwords);  // sorted columns of F (cap K)
+    const int per = (nwords + blockDim.x - 1) / blockDim.x;
+    const int w0 = threadIdx.x * per, w1 = min(nwords, w0 + per);
+    int32_t local = 0;
+    for (int w = w0; w < w1; ++w) {
+        const uint32_t f = fmask[w];
+        sf[w] = f;
+        local += __popc(f);
+    }
+    // block exclusive scan of the popcounts -> sorted column list
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t incl = local;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        int32_t sum = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t t = __shfl_up_sync(0xffffffffu, sum, d);
+            if (lane >= d) sum += t;
+        }
+        if (lane < nw) warp_sums[lane] = sum;
+        if (lane == nw - 1) n_f = sum;
+    }
+    __syncthreads();
+    int32_t pos = incl - local + (wid > 0 ? warp_sums[wid - 1] : 0);
+    for (int w = w0; w < w1; ++w)
+        for (uint32_t m = sf[w]; m; m &= m - 1) {
+            const int32_t c = (w << 5) + __ffs(m) - 1;
+            scol[pos] = c;
+            if (blockIdx.x == 0) o_idx[pos] = c;
+            ++pos;
+        }
+    __syncthreads();
+    const int nf = n_f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *o_count = nf;
+    const int n_xo = xo != nullptr ? static_cast<int>(min(static_cast<int64_t>(nf), o_cap)) : 0;
+    const int64_t nwarps = blockDim.x >> 5;
+    for (int64_t row = blockIdx.x * nwarps + wid; row < M; row += static_cast<int64_t>(gridDim.x) * nwarps) {
+        const __half* xr = x + row * ldx;
+        for (int t = lane; t < n_xo; t += 32) xo[row * o_cap + t] = xr[scol[t]];
+        const int64_t b = row / rb;
+        if (snap_cnt[b] == nf) continue;  // S_b == F (S_b is a subset of F)
+        // late columns: in F, not in S_b
+        const uint32_t* sb = snap + b * nwords;
+        const uint32_t am_bits = __half_as_ushort(__float2half_rn(row_amax[row]));
+        bool requant = false;
+        for (int t = lane; t < nf; t += 32) {
+            const int32_t c = scol[t];
+            if ((sb[c >> 5] >> (c & 31)) & 1u) continue;
+            if ((__half_as_ushort(xr[c]) & 0x7FFFu) == am_bits) requant = true;
+        }
+        requant = __any_sync(0xffffffffu, requant);
+        if (!requant) {
+            for (int t = lane; t < nf; t += 32) {
+                const int32_t c = scol[t];
+                if (!((sb[c >> 5] >> (c & 31)) & 1u)) xq[row * ldq + c] = 0;
+            }
+            continue;
+        }
+        // the row max may have been in a late column: redo the row against F
+        // (K % 8 == 0 and 16-byte aligned rows on this path)
+        const int nvr = static_cast<int>(K >> 3);
+        uint32_t am2 = 0;
+        for (int v = lane; v < nvr; v += 32) {
+            const uint4 q = *reinterpret_cast<const uint4*>(xr + 8 * v);
+            const uint32_t mb = (sf[v >> 2] >> (8 * (v & 3))) & 0xFFu;
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) am2 = __vmaxu2(am2, (w4[e] & 0x7FFF7FFFu) & keep_word(mb, e));
+        }
+        uint32_t am = max(am2 & 0xFFFFu, am2 >> 16);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) am = max(am, __shfl_xor_sync(0xffffffffu, am, d));
+        const float amax = __half2float(__ushort_as_half(static_cast<unsigned short>(am)));
+        const double sc = scale_of(amax);
+        const float s32 = static_cast<float>(sc);
+        for (int v = lane; v < nvr; v += 32) {
+            const uint4 q = *reinterpret_cast<const uint4*>(xr + 8 * v);
+            const uint32_t mb = (sf[v >> 2] >> (8 * (v & 3))) & 0xFFu;
+            *reinterpret_cast<uint2*>(xq + row * ldq + 8 * v) = quant8(q, mb, s32, sc);
+        }
+        if (lane == 0) row_amax[row] = amax;
+    }
+}
+
 bool row_prologue_split_ok(int64_t K, int64_t ldx, int64_t ldq, const void* x, const void* xq) {
     static int env = -1;
     if (env < 0) {
@@ -802,9 +1105,93 @@ bool row_prologue_split_ok(int64_t K, int64_t ldx, int64_t ldq, const void* x, c
            (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (reinterpret_cast<uintptr_t>(xq) & 7u) == 0;
 }
 
+
+// 1-read row prologue (rp1_*): scratch = row_prologue_scratch_bytes(M, K).
+// Returns cudaErrorNotSupported when the shape is outside its envelope (the
+// caller then runs the 2-read form).
+static bool rp1_ok(int64_t M, int64_t K, int64_t ldx, int64_t ldq, const void* x, const void* xq) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("I8MM_PROLOGUE_1READ");  // opt-in: measured slower
+        env = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (env != 1 || M <= 0 || K % 8 != 0 || ldx % 8 != 0 || ldq % 8 != 0) return false;
+    if ((reinterpret_cast<uintptr_t>(x) & 15u) || (reinterpret_cast<uintptr_t>(xq) & 7u)) return false;
+    const Rp1Geom g = rp1_geom(M, K);
+    // a row fits the consumers' registers (K <= 32768), >= 2 ring stages
+    return (K >> 3) <= RP1_BLOCK_VECS && g.stages >= 2;
+}
+
+static size_t rp1_scratch_bytes(int64_t M, int64_t K) {
+    const Rp1Geom g = rp1_geom(M > 0 ? M : 1, K);
+    const int64_t nwords = (K + 31) >> 5;
+    return static_cast<size_t>(((g.nblk * nwords * 4 + 255) / 256) * 256 + g.nblk * 4);
+}
+
+static cudaError_t launch_rp1(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
+                              uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
+                              int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
+                              void* scratch, cudaStream_t st) {
+    const Rp1Geom g = rp1_geom(M, K);
+    const int64_t nwords = (K + 31) >> 5;
+    uint32_t* snap = static_cast<uint32_t*>(scratch);
+    int32_t* snap_cnt = reinterpret_cast<int32_t*>(static_cast<char*>(scratch) +
+                                                   ((g.nblk * nwords * 4 + 255) / 256) * 256);
+    const int sms = num_sms();
+    cudaError_t e;
+    if ((e = launch_pdl(zero_u32_kernel, dim3(static_cast<unsigned>(imin64((nwords + 255) / 256, 1024))),
+                        dim3(256), 0, st, mask, nwords)))
+        return e;
+    count_launch();
+    // seed F with the first rows (systematic outlier features show up at once),
+    // so few blocks are quantized against an incomplete snapshot
+    {
+        const int64_t seed_rows = imin64(M, 64);
+        const int64_t nvec = K >> 3, cb = (nvec + 255) / 256;
+        const int64_t rpb = 4, rbs = (seed_rows + rpb - 1) / rpb;
+        if ((e = launch_pdl(outlier_scan_vec_kernel<false>, dim3(static_cast<unsigned>(cb), static_cast<unsigned>(rbs)),
+                            dim3(256), 0, st, x, seed_rows, K, ldx, alpha_threshold_bits(alpha), rpb, mask,
+                            static_cast<int32_t*>(nullptr), static_cast<uint16_t*>(nullptr), int64_t(0))))
+            return e;
+        count_launch();
+    }
+    const size_t smem = static_cast<size_t>(g.stages) * g.stage_bytes;
+    const unsigned grid = static_cast<unsigned>(imin64(g.nblk, sms));
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RP1_SMEM_RING);
+        return launch_pdl(kern, dim3(grid), dim3(RP1_THREADS), smem, st, x, M, K, ldx,
+                          alpha_threshold_bits(alpha), mask, snap, snap_cnt, xq, ldq, row_amax);
+    };
+    switch (g.rb) {
+        case 1: e = go(rp1_stream_kernel<1>); break;
+        case 2: e = go(rp1_stream_kernel<2>); break;
+        case 4: e = go(rp1_stream_kernel<4>); break;
+        case 8: e = go(rp1_stream_kernel<8>); break;
+        default: e = go(rp1_stream_kernel<16>); break;
+    }
+    if (e) return e;
+    count_launch();
+    const size_t fsmem = static_cast<size_t>(nwords) * 4 + static_cast<size_t>(K) * 4;
+    static size_t fconfigured = 0;
+    if (fsmem > 48 * 1024 && fsmem > fconfigured) {
+        cudaFuncSetAttribute(rp1_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(fsmem));
+        fconfigured = fsmem;
+    }
+    const int64_t fgrid = imin64((M + 7) / 8, static_cast<int64_t>(sms) * 4);
+    if ((e = launch_pdl(rp1_finalize_kernel, dim3(static_cast<unsigned>(fgrid)), dim3(256), fsmem, st, x, M,
+                        K, ldx, static_cast<const uint32_t*>(mask), static_cast<const uint32_t*>(snap),
+                        static_cast<const int32_t*>(snap_cnt), g.rb, o_idx, o_count, xq, ldq, row_amax,
+                        xo, o_cap)))
+        return e;
+    count_launch();
+    return cudaGetLastError();
+}
 size_t row_prologue_scratch_bytes(int64_t M, int64_t K) {
     const int64_t ng = (K + 63) >> 6;
-    return static_cast<size_t>(((M * ng * 2 + 255) / 256) * 256 + M * 8 + (33 + ng) * 4);
+    const size_t two = static_cast<size_t>(((M * ng * 2 + 255) / 256) * 256 + M * 8 + (33 + ng) * 4);
+    const size_t one = rp1_scratch_bytes(M, K);
+    return one > two ? one : two;
 }
 
 cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
@@ -817,6 +1204,8 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
         if ((e = launch_outlier_compact(mask, K, o_idx, o_count, st))) return e;
         return launch_quantize_rows(x, M, K, ldx, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, st);
     }
+    if (rp1_ok(M, K, ldx, ldq, x, xq))
+        return launch_rp1(x, M, K, ldx, alpha, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, scratch, st);
     const int64_t nwords = (K + 31) >> 5, nvec = K >> 3, ng = (K + 63) >> 6;
     uint16_t* gmax = static_cast<uint16_t*>(scratch);
     double* row_s = reinterpret_cast<double*>(static_cast<char*>(scratch) + ((M * ng * 2 + 255) / 256) * 256);

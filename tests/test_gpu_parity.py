@@ -381,12 +381,13 @@ print("VARIANT OK")
 """
 
 
-@pytest.mark.parametrize("variant", [{"I8MM_FORCE_CG1": "1"}, {"I8MM_GEMM_MC": "2"}],
-                         ids=["cta_group1", "pair_multicast_cluster4"])
+@pytest.mark.parametrize("variant", [{"I8MM_FORCE_CG1": "1"}, {"I8MM_GEMM_MC": "2"},
+                                     {"I8MM_PROLOGUE_1READ": "1"}],
+                         ids=["cta_group1", "pair_multicast_cluster4", "prologue_one_read"])
 def test_gemm_kernel_variants(p, variant):
-    """The 1-CTA (cta_group::1) GEMM and the 4-CTA-cluster GEMM multicasting
-    WqT between two CTA pairs, pinned via environment overrides (the default
-    CTA-pair path is covered above)."""
+    """The 1-CTA (cta_group::1) GEMM, the 4-CTA-cluster GEMM multicasting WqT
+    between two CTA pairs, and the opt-in 1-read row prologue, pinned via
+    environment overrides (the defaults are covered above)."""
     import os
     import subprocess
     import sys
@@ -689,3 +690,53 @@ def test_host_io_pipeline_back_to_back_batches(p, oracle_mod):
     for _, ys, refs in batches:
         for y, r in zip(ys, refs):
             assert torch.equal(y, r)
+
+
+_LATE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2208_07339_b200 as p
+from oracle import oracle as orc
+for k in (1024, 4096, 16384):
+    rng = np.random.Generator(np.random.PCG64(k))
+    m, n = 600, 256
+    x = (0.5 * rng.standard_normal((m, k))).astype(np.float32)
+    c1, c2, c3 = 5, k // 2 + 3, k - 7
+    x[:, c1] = 5.5          # the row maximum everywhere, outlier only in the last row
+    x[:, c2] = 0.25         # outlier only in the last row, never a row maximum
+    x[-1, c1] = 10.0
+    x[-1, c2] = -12.0
+    x[::3, c3] = 30.0       # a regular outlier column
+    w = rng.standard_normal((k, n)).astype(np.float32)
+    x = x.astype(np.float16).astype(np.float32)
+    w = w.astype(np.float16).astype(np.float32)
+    ref = orc.c_llm_int8_matmul(x, w, 6.0)
+    assert tuple(ref.dims) == tuple(sorted((c1, c2, c3))), ref.dims
+    r = p.llm_int8_matmul(x, w, 6.0, exact=True)
+    assert r.decomposed_cols == 3
+    assert np.array_equal(r.output.cpu().numpy(), ref.output), k
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    assert np.array_equal(lin.matmul(x16, exact=True).cpu().numpy(), ref.output), k
+    assert lin.last_stats()["decomposed_cols"] == 3
+print("LATE OK")
+"""
+
+
+@pytest.mark.parametrize("one_read", ["0", "1"], ids=["two_read", "one_read"])
+def test_prologue_late_outlier_columns(p, one_read):
+    """Columns that turn outlier only in the last row. c1 holds the row maximum
+    (5.5 < alpha) in every row, c2 never does, c3 is a regular planted column.
+    In the 1-read form every block quantized before c1/c2 were flagged is
+    corrected exactly by the finalize pass (rows re-quantized for c1, codes
+    zeroed for c2)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    env = dict(os.environ, I8MM_PROLOGUE_1READ=one_read)
+    r = subprocess.run([sys.executable, "-c", _LATE_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "LATE OK" in r.stdout, r.stdout + r.stderr
