@@ -156,6 +156,23 @@ __device__ __forceinline__ bool tile_coords(const Params& p, const TileSpace& ts
 
 __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0f : a; }
 
+// v[0..31] += sum_o xo[o] * wo[o][0..31] over NO staged (zero-padded) outlier rows,
+// packed f32x2 FMAs, no per-row guards.
+template <int NO>
+__device__ __forceinline__ void outlier_fma(float2* v2, const float* xo_r, const float* wrow) {
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+        const float2 xv2 = make_float2(xo_r[o], xo_r[o]);
+        const float4* wr = reinterpret_cast<const float4*>(wrow + o * BN);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float4 f = wr[u];
+            v2[2 * u] = __ffma2_rn(xv2, make_float2(f.x, f.y), v2[2 * u]);
+            v2[2 * u + 1] = __ffma2_rn(xv2, make_float2(f.z, f.w), v2[2 * u + 1]);
+        }
+    }
+}
+
 template <int EPI, int CG, int MC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -318,6 +335,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool wo_fast = n_out <= WO_CAP && p.wo != nullptr && n_out <= p.wo_cap;
         const bool xo_fast = n_out <= WO_CAP && p.xo != nullptr && n_out <= p.o_cap;
         const bool stage_wo = n_out > 0 && n_out <= WO_CAP;
+        // staged outlier rows are padded with zeros to a class of 4 / 8 / 16 so the
+        // FMA loop is straight-line code (per-outlier guards made the compiler
+        // shuffle the 32 accumulators between registers at every join)
+        const int n_cls = n_out <= 4 ? 4 : (n_out <= 8 ? 8 : WO_CAP);
         uint32_t stg_cnt = 0;  // TS: output boxes issued by this warp
         int it = 0;
         for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
@@ -351,10 +372,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (stage_wo) {
                     if (wo_fast && !mapped && col0 + BN <= n_live && (p.ldwo % 8) == 0) {
                         // 16-byte vector loads of the compact outlier rows
-                        for (int i = et; i < n_out * (BN / 8); i += EPI_THREADS) {
+                        for (int i = et; i < n_cls * (BN / 8); i += EPI_THREADS) {
                             const int o = i / (BN / 8), v = i % (BN / 8);
-                            const uint4 q = *reinterpret_cast<const uint4*>(
-                                p.wo + static_cast<int64_t>(o) * p.ldwo + col0 + v * 8);
+                            const uint4 q = o < n_out ? *reinterpret_cast<const uint4*>(
+                                p.wo + static_cast<int64_t>(o) * p.ldwo + col0 + v * 8) : make_uint4(0, 0, 0, 0);
                             const __half2* h2 = reinterpret_cast<const __half2*>(&q);
                             float4* dst = reinterpret_cast<float4*>(smem_wo + o * BN + v * 8);
                             const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]);
@@ -363,11 +384,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                             dst[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
                         }
                     } else {
-                        for (int i = et; i < n_out * BN; i += EPI_THREADS) {
+                        for (int i = et; i < n_cls * BN; i += EPI_THREADS) {
                             const int o = i / BN, j = i % BN;
                             const int64_t c = col0 + j;
                             float v = 0.0f;
-                            if (c < n_live) {
+                            if (c < n_live && o < n_out) {
                                 const int64_t gc = mapped ? cmap[c] : c;
                                 v = wo_fast ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + gc])
                                             : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + gc]);
@@ -467,20 +488,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                         if (n_out > 0 && !(p.dbg_epi & 1)) {
                             if (stage_wo) {
-#pragma unroll
-                                for (int o = 0; o < WO_CAP; ++o) {
-                                    if (o < n_out) {
-                                        const float2 xv2 = make_float2(xo_r[o], xo_r[o]);
-                                        const float4* wr = reinterpret_cast<const float4*>(
-                                            smem_wo + o * BN + ch * 32);
-#pragma unroll
-                                        for (int u = 0; u < 8; ++u) {
-                                            const float4 f = wr[u];
-                                            v2[2 * u] = __ffma2_rn(xv2, make_float2(f.x, f.y), v2[2 * u]);
-                                            v2[2 * u + 1] = __ffma2_rn(xv2, make_float2(f.z, f.w), v2[2 * u + 1]);
-                                        }
-                                    }
-                                }
+                                const float* wrow = smem_wo + ch * 32;
+                                if (n_cls == 4) outlier_fma<4>(v2, xo_r, wrow);
+                                else if (n_cls == 8) outlier_fma<8>(v2, xo_r, wrow);
+                                else outlier_fma<WO_CAP>(v2, xo_r, wrow);
                             } else {
                                 for (int o = 0; o < n_out; ++o) {
                                     const int64_t k = p.o_idx[o];

@@ -6,6 +6,7 @@ bytes = K*N (int8 WqT) + 2*M*K (X) + 2*M*N (Y) + 2*|O|*N (fp16 outlier rows)
 + 4*N (column amax), against MEASURED_PEAKS.json hbm_gbs.
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -40,6 +41,8 @@ def t_ev(fn, iters=50, warm=5):
 
 def main():
     projs, ms_list, iters = dict(PROJ), MS, 50
+    if os.environ.get("DECODE_MS"):  # e.g. DECODE_MS=1,8,16 for a short A/B
+        ms_list = [int(v) for v in os.environ["DECODE_MS"].split(",")]
     if len(sys.argv) > 2:  # e.g. "fc1 16" for a short run under ncu
         projs = {sys.argv[1]: PROJ[sys.argv[1]]}
         ms_list, iters = [int(sys.argv[2])], 3
