@@ -41,10 +41,13 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
 // compact, row scales (+ x[:, O]), streaming codes. `scratch` holds
 // row_prologue_scratch_bytes(M, K); nullptr (or unaligned X) = scan, compact, quantize_rows.
 size_t row_prologue_scratch_bytes(int64_t M, int64_t K);
+// zero2 / zero2_n: an extra range of words zeroed in the same launch (the
+// weight-stationary fixup counters), or nullptr.
 cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                                 uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
                                 int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
-                                void* scratch, cudaStream_t st);
+                                void* scratch, cudaStream_t st, uint32_t* zero2 = nullptr,
+                                int64_t zero2_n = 0);
 cudaError_t launch_quantize_cols_t(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                    const uint32_t* row_mask, int8_t* wq_t, int64_t ldq,
                                    float* col_amax, cudaStream_t st);
@@ -71,6 +74,19 @@ cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t l
                                 const uint16_t* cand_v, const int32_t* cand_r, const int8_t* q2,
                                 int32_t* p_count, int32_t* p_idx, float* p_amax, int32_t* p_src,
                                 int8_t* wq_p, int64_t ldq, cudaStream_t st);
+// Weight-stationary per-call work after the row prologue, in two launches:
+// W[O, :] gather + column fixup (one grid, p_count region already zeroed by
+// the row prologue), then the patched columns' codes.
+cudaError_t launch_gather_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
+                                const uint32_t* mask, const int32_t* o_idx, const int32_t* o_count,
+                                int64_t o_cap, __half* wo, int64_t ldwo, const float* amax_full,
+                                const uint16_t* cand_v, const int32_t* cand_r, int32_t* p_count,
+                                int32_t* p_idx, float* p_amax, int32_t* p_src, cudaStream_t st);
+cudaError_t launch_patch_quantize(const __half* w, int64_t K, int64_t N, int64_t ldw,
+                                  const uint32_t* mask, const int8_t* q2, const int32_t* p_count,
+                                  const int32_t* p_idx, const float* p_amax, const int32_t* p_src,
+                                  int8_t* wq_p, int64_t ldq, cudaStream_t st);
+int64_t fixup_zero_words(int64_t N);  // size of the p_count region
 cudaError_t launch_transpose_i8(const int8_t* src, int64_t rows, int64_t cols, int64_t lds,
                                 int8_t* dst, int64_t ldd, cudaStream_t st);
 

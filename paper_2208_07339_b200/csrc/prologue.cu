@@ -132,6 +132,17 @@ __global__ void zero_u32_kernel(uint32_t* p, int64_t n) {
         p[i] = 0u;
 }
 
+// two ranges in one launch (the mask and the caller's per-call counters)
+__global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n2) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n + n2; i += stride) {
+        if (i < n) p[i] = 0u;
+        else p2[i - n] = 0u;
+    }
+}
+
 // ------------------------------------------------------------------ compact
 // One block: prefix popcount over the mask words, scatter sorted indices.
 // dgrp (optional, K <= 65536): [count, 32 bitmap words of 64-column groups
@@ -1197,8 +1208,17 @@ size_t row_prologue_scratch_bytes(int64_t M, int64_t K) {
 cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                                 uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
                                 int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
-                                void* scratch, cudaStream_t st) {
+                                void* scratch, cudaStream_t st, uint32_t* zero2, int64_t zero2_n) {
     cudaError_t e;
+    if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq) ||
+        rp1_ok(M, K, ldx, ldq, x, xq)) {
+        if (zero2 != nullptr && zero2_n > 0) {
+            if ((e = launch_pdl(zero_u32_kernel, dim3(static_cast<unsigned>(imin64((zero2_n + 255) / 256, 64))),
+                                dim3(256), 0, st, zero2, zero2_n)))
+                return e;
+            count_launch();
+        }
+    }
     if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq)) {
         if ((e = launch_outlier_scan(x, M, K, ldx, alpha, mask, nullptr, st))) return e;
         if ((e = launch_outlier_compact(mask, K, o_idx, o_count, st))) return e;
@@ -1211,10 +1231,13 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     double* row_s = reinterpret_cast<double*>(static_cast<char*>(scratch) + ((M * ng * 2 + 255) / 256) * 256);
     int32_t* dgrp = reinterpret_cast<int32_t*>(row_s + M);
     const int sms = num_sms();
-    if ((e = launch_pdl(zero_u32_kernel, dim3(static_cast<unsigned>(imin64((nwords + 255) / 256, 1024))),
-                        dim3(256), 0, st, mask, nwords)))
-        return e;
-    count_launch();
+    {
+        const int64_t n2 = zero2 != nullptr ? zero2_n : 0;
+        if ((e = launch_pdl(zero2_u32_kernel, dim3(static_cast<unsigned>(imin64((nwords + n2 + 255) / 256, 1024))),
+                            dim3(256), 0, st, mask, nwords, zero2, n2)))
+            return e;
+        count_launch();
+    }
     const int64_t cb = (nvec + 255) / 256;
     int64_t rpb;
     int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);

@@ -179,25 +179,30 @@ __global__ void __launch_bounds__(256) quantize_cols_t_kernel(
 
 // ------------------------------------------------------------------ gather
 // out[t, :] = w[idx[t], :] for t < min(*count, cap) (compact outlier rows).
-__global__ void gather_rows_kernel(const __half* __restrict__ w, int64_t ldw, int64_t N,
-                                   const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
-                                   int64_t cap, __half* __restrict__ out, int64_t ldo, int vec) {
-    pdl_wait();
-    pdl_trigger();
-    const int64_t t = blockIdx.y;
+// block (bx of gx) of row t
+__device__ __forceinline__ void gather_rows_block(const __half* __restrict__ w, int64_t ldw, int64_t N,
+                                                  const int32_t* __restrict__ idx,
+                                                  const int32_t* __restrict__ count, int64_t cap,
+                                                  __half* __restrict__ out, int64_t ldo, int vec,
+                                                  int64_t t, int64_t bx, int64_t gx) {
     const int64_t n = imin64(static_cast<int64_t>(*count), cap);
     if (t >= n) return;
     const __half* src = w + static_cast<int64_t>(idx[t]) * ldw;
     __half* dst = out + t * ldo;
     if (vec) {
-        for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < (N >> 3);
-             v += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        for (int64_t v = bx * blockDim.x + threadIdx.x; v < (N >> 3); v += gx * blockDim.x)
             reinterpret_cast<uint4*>(dst)[v] = ld_stream_u4(src + (v << 3));
     } else {
-        for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < N;
-             j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-            dst[j] = src[j];
+        for (int64_t j = bx * blockDim.x + threadIdx.x; j < N; j += gx * blockDim.x) dst[j] = src[j];
     }
+}
+
+__global__ void gather_rows_kernel(const __half* __restrict__ w, int64_t ldw, int64_t N,
+                                   const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
+                                   int64_t cap, __half* __restrict__ out, int64_t ldo, int vec) {
+    pdl_wait();
+    pdl_trigger();
+    gather_rows_block(w, ldw, N, idx, count, cap, out, ldo, vec, blockIdx.y, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------------ top-T
@@ -295,14 +300,14 @@ __global__ void topt_merge_kernel(int64_t N, int64_t chunks, const uint32_t* __r
 // One thread per column: the column's amax over keep rows from the cached
 // candidates (full rescan only if every candidate row is an outlier row).
 // Columns whose amax changes are appended to the patch list.
-__global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N, int64_t ldw,
-                             const uint32_t* __restrict__ mask, const float* __restrict__ amax_full,
-                             const uint16_t* __restrict__ cand_v, const int32_t* __restrict__ cand_r,
-                             int32_t* __restrict__ p_count, int32_t* __restrict__ p_idx,
-                             float* __restrict__ p_amax, int32_t* __restrict__ p_src) {
-    pdl_wait();
-    pdl_trigger();
-    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void fixup_column(const __half* __restrict__ w, int64_t K, int64_t N, int64_t ldw,
+                                             const uint32_t* __restrict__ mask,
+                                             const float* __restrict__ amax_full,
+                                             const uint16_t* __restrict__ cand_v,
+                                             const int32_t* __restrict__ cand_r,
+                                             int32_t* __restrict__ p_count, int32_t* __restrict__ p_idx,
+                                             float* __restrict__ p_amax, int32_t* __restrict__ p_src,
+                                             int64_t j) {
     if (j >= N) return;
     const int32_t r0 = cand_r[j];
     if (r0 < 0 || !row_is_out(mask, r0)) return;  // cached maximiser is a keep row
@@ -339,6 +344,39 @@ __global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N,
         p_src[p] = src;
         atomicOr(reinterpret_cast<uint32_t*>(p_count) + 4 + (j >> 5), 1u << (j & 31));
     }
+}
+
+__global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N, int64_t ldw,
+                             const uint32_t* __restrict__ mask, const float* __restrict__ amax_full,
+                             const uint16_t* __restrict__ cand_v, const int32_t* __restrict__ cand_r,
+                             int32_t* __restrict__ p_count, int32_t* __restrict__ p_idx,
+                             float* __restrict__ p_amax, int32_t* __restrict__ p_src) {
+    pdl_wait();
+    pdl_trigger();
+    fixup_column(w, K, N, ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax, p_src,
+                 static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+}
+
+// One launch for the two independent consumers of the outlier set: blocks
+// [0, cap * gx) gather W[O, :] (row t = b / gx), the rest run the column fixup.
+__global__ void gather_fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N, int64_t ldw,
+                                    const uint32_t* __restrict__ mask, const int32_t* __restrict__ o_idx,
+                                    const int32_t* __restrict__ o_count, int64_t o_cap,
+                                    __half* __restrict__ wo, int64_t ldwo, int vec, int64_t gx,
+                                    const float* __restrict__ amax_full,
+                                    const uint16_t* __restrict__ cand_v,
+                                    const int32_t* __restrict__ cand_r, int32_t* __restrict__ p_count,
+                                    int32_t* __restrict__ p_idx, float* __restrict__ p_amax,
+                                    int32_t* __restrict__ p_src) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t b = blockIdx.x, ng = o_cap * gx;
+    if (b < ng) {
+        gather_rows_block(w, ldw, N, o_idx, o_count, o_cap, wo, ldwo, vec, b / gx, b % gx, gx);
+        return;
+    }
+    fixup_column(w, K, N, ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax, p_src,
+                 (b - ng) * blockDim.x + threadIdx.x);
 }
 
 // codes of the patched columns (K-major rows of WqP), outlier rows = 0.
@@ -444,6 +482,36 @@ cudaError_t launch_gather_rows(const __half* w, int64_t ldw, int64_t N, const in
     const unsigned gx = static_cast<unsigned>(imin64((per + 255) / 256, 64));
     cudaError_t e = launch_pdl(gather_rows_kernel, dim3(gx, static_cast<unsigned>(cap)), dim3(256), 0, st,
                                w, ldw, N, idx, count, cap, out, ldo, vec);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+int64_t fixup_zero_words(int64_t N) { return 4 + (N + 31) / 32; }
+
+cudaError_t launch_gather_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
+                                const uint32_t* mask, const int32_t* o_idx, const int32_t* o_count,
+                                int64_t o_cap, __half* wo, int64_t ldwo, const float* amax_full,
+                                const uint16_t* cand_v, const int32_t* cand_r, int32_t* p_count,
+                                int32_t* p_idx, float* p_amax, int32_t* p_src, cudaStream_t st) {
+    if (N == 0) return cudaSuccess;
+    const int vec = (N % 8 == 0) && (ldw % 8 == 0) && (ldwo % 8 == 0) && aligned16(w) && aligned16(wo);
+    const int64_t per = vec ? (N >> 3) : N;
+    const int64_t gx = imin64((per + 255) / 256, 16);
+    const int64_t blocks = o_cap * gx + (N + 255) / 256;
+    cudaError_t e = launch_pdl(gather_fixup_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st,
+                               w, K, N, ldw, mask, o_idx, o_count, o_cap, wo, ldwo, vec, gx, amax_full,
+                               cand_v, cand_r, p_count, p_idx, p_amax, p_src);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_patch_quantize(const __half* w, int64_t K, int64_t N, int64_t ldw,
+                                  const uint32_t* mask, const int8_t* q2, const int32_t* p_count,
+                                  const int32_t* p_idx, const float* p_amax, const int32_t* p_src,
+                                  int8_t* wq_p, int64_t ldq, cudaStream_t st) {
+    const dim3 pgrid(static_cast<unsigned>((ldq + 2047) / 2048), static_cast<unsigned>(imin64(N, 256)));
+    cudaError_t e = launch_pdl(patch_quantize_kernel, pgrid, dim3(256), 0, st, w, K, ldw, mask, p_count,
+                               p_idx, p_amax, p_src, q2, wq_p, ldq);
     count_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
