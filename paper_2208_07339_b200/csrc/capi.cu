@@ -530,15 +530,10 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
     if (ws.decode) return cuda_status(launch_set_word(ws.thr_word, alpha_threshold_bits(alpha), st));
     // row side (+ the fixup counters zeroed in the same first launch), then
     // W[O, :] gather + column fixup in one launch, then the patched codes
+    const PerCallFix fix{wh, K, N, ldw, ws.wo, round_up(N, 8), b.col_amax, b.cand_v, b.cand_r, b.q2,
+                         ws.p_count, ws.p_idx, ws.p_amax, ws.p_src, ws.wq_p};
     if (launch_row_prologue(xh, M, K, ldx, alpha, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
-                            ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st,
-                            reinterpret_cast<uint32_t*>(ws.p_count), fixup_zero_words(N)))
-        return I8MM_ERR_CUDA;
-    if (launch_gather_fixup(wh, K, N, ldw, ws.mask, ws.o_idx, ws.o_count, ws.o_cap, ws.wo, round_up(N, 8),
-                            b.col_amax, b.cand_v, b.cand_r, ws.p_count, ws.p_idx, ws.p_amax, ws.p_src, st))
-        return I8MM_ERR_CUDA;
-    if (launch_patch_quantize(wh, K, N, ldw, ws.mask, b.q2, ws.p_count, ws.p_idx, ws.p_amax, ws.p_src,
-                              ws.wq_p, ws.ldq, st))
+                            ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st, &fix))
         return I8MM_ERR_CUDA;
     return I8MM_OK;
 }

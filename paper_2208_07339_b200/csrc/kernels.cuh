@@ -41,13 +41,31 @@ cudaError_t launch_quantize_rows(const __half* x, int64_t M, int64_t K, int64_t 
 // compact, row scales (+ x[:, O]), streaming codes. `scratch` holds
 // row_prologue_scratch_bytes(M, K); nullptr (or unaligned X) = scan, compact, quantize_rows.
 size_t row_prologue_scratch_bytes(int64_t M, int64_t K);
-// zero2 / zero2_n: an extra range of words zeroed in the same launch (the
-// weight-stationary fixup counters), or nullptr.
+// Weight-stationary per-call state that rides along with the row prologue
+// (W[O, :] gather, column fixup, patched codes; see percall_dev.cuh).
+struct PerCallFix {
+    const __half* w;
+    int64_t K, N, ldw;
+    __half* wo;
+    int64_t ldwo;
+    const float* amax_full;
+    const uint16_t* cand_v;
+    const int32_t* cand_r;
+    const int8_t* q2;
+    int32_t* p_count;  // [count, pad x3, patched-column bits]
+    int32_t* p_idx;
+    float* p_amax;
+    int32_t* p_src;
+    int8_t* wq_p;
+};
+
+// fix != nullptr: the weight-stationary per-call work is done too (its
+// counters zeroed with the mask, gather + fixup fused into the row-scale
+// grid, patched codes written by the code-pass CTAs).
 cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                                 uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
                                 int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
-                                void* scratch, cudaStream_t st, uint32_t* zero2 = nullptr,
-                                int64_t zero2_n = 0);
+                                void* scratch, cudaStream_t st, const PerCallFix* fix = nullptr);
 cudaError_t launch_quantize_cols_t(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                    const uint32_t* row_mask, int8_t* wq_t, int64_t ldq,
                                    float* col_amax, cudaStream_t st);

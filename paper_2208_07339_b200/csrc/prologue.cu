@@ -18,6 +18,7 @@
 #include "kernels.cuh"
 #include "quant_common.cuh"
 #include "sm100_ptx.cuh"
+#include "percall_dev.cuh"
 
 namespace i8mm {
 
@@ -457,17 +458,36 @@ __global__ void __launch_bounds__(256) quantize_rows_smem_kernel(
 // before any is consumed. Dirty groups (64-column groups holding an outlier
 // column) come from outlier_compact's dgrp list; K <= 65536 (ng <= 1024).
 constexpr int RS_GM = 8;  // group maxima per lane per pass (256 groups = 16384 columns)
-__global__ void __launch_bounds__(256) row_scale_kernel(
-    const __half* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
-    const uint32_t* __restrict__ col_mask, const int32_t* __restrict__ o_idx,
-    const int32_t* __restrict__ o_count, const uint16_t* __restrict__ gmax, int64_t ng,
-    const int32_t* __restrict__ dgrp, float* __restrict__ row_amax, double* __restrict__ row_s,
-    __half* __restrict__ xo, int64_t o_cap) {
+struct RowScaleArgs {
+    const __half* x;
+    int64_t M, K, ldx;
+    const uint32_t* col_mask;
+    const int32_t* o_idx;
+    const int32_t* o_count;
+    const uint16_t* gmax;
+    int64_t ng;
+    const int32_t* dgrp;
+    float* row_amax;
+    double* row_s;
+    __half* xo;
+    int64_t o_cap;
+};
+
+// block bid of nblk row-scale blocks
+__device__ __forceinline__ void row_scale_block(const RowScaleArgs& a, int64_t bid, int64_t nblk) {
+    const __half* __restrict__ x = a.x;
+    const int64_t M = a.M, K = a.K, ldx = a.ldx, ng = a.ng, o_cap = a.o_cap;
+    const uint32_t* __restrict__ col_mask = a.col_mask;
+    const int32_t* __restrict__ o_idx = a.o_idx;
+    const int32_t* __restrict__ o_count = a.o_count;
+    const uint16_t* __restrict__ gmax = a.gmax;
+    const int32_t* __restrict__ dgrp = a.dgrp;
+    float* __restrict__ row_amax = a.row_amax;
+    double* __restrict__ row_s = a.row_s;
+    __half* __restrict__ xo = a.xo;
     __shared__ uint32_t sgb[32];
     __shared__ int32_t sdg[1024];
     __shared__ int32_t so[64];
-    pdl_wait();
-    pdl_trigger();
     const int nd = __ldg(dgrp);
     const int n_o = xo != nullptr ? static_cast<int>(min(static_cast<int64_t>(__ldg(o_count)), min(o_cap, static_cast<int64_t>(64)))) : 0;
     if (threadIdx.x < 32) sgb[threadIdx.x] = static_cast<uint32_t>(__ldg(dgrp + 1 + threadIdx.x));
@@ -478,8 +498,7 @@ __global__ void __launch_bounds__(256) row_scale_kernel(
     const int64_t nvec = K >> 3;
     const int nd8 = nd * 8;
     const int64_t nwarps = blockDim.x >> 5;
-    for (int64_t row = blockIdx.x * nwarps + (threadIdx.x >> 5); row < M;
-         row += static_cast<int64_t>(gridDim.x) * nwarps) {
+    for (int64_t row = bid * nwarps + (threadIdx.x >> 5); row < M; row += nblk * nwarps) {
         const __half* xr = x + row * ldx;
         const uint16_t* gr = gmax + row * ng;
         // issue: first dirty pair chunk + x[row, O]
@@ -546,6 +565,33 @@ __global__ void __launch_bounds__(256) row_scale_kernel(
     }
 }
 
+__global__ void __launch_bounds__(256) row_scale_kernel(const RowScaleArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    row_scale_block(a, blockIdx.x, gridDim.x);
+}
+
+// Row scales + the weight-stationary W[O, :] gather and column fixup in one
+// grid (all three only need the compacted outlier set): blocks [0, rs_blocks)
+// are row-scale blocks, then o_cap * gx gather blocks, then fixup blocks.
+__global__ void __launch_bounds__(256) row_scale_fix_kernel(const RowScaleArgs a, int64_t rs_blocks,
+                                                            const PerCallFix f, int vec, int64_t gx) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t b = blockIdx.x;
+    if (b < rs_blocks) {
+        row_scale_block(a, b, rs_blocks);
+        return;
+    }
+    const int64_t g = b - rs_blocks, ngath = a.o_cap * gx;
+    if (g < ngath) {
+        gather_rows_block(f.w, f.ldw, f.N, a.o_idx, a.o_count, a.o_cap, f.wo, f.ldwo, vec, g / gx, g % gx, gx);
+        return;
+    }
+    fixup_column(f.w, f.K, f.N, f.ldw, a.col_mask, f.amax_full, f.cand_v, f.cand_r, f.p_count, f.p_idx,
+                 f.p_amax, f.p_src, (g - ngath) * blockDim.x + threadIdx.x);
+}
+
 // Bulk-copy fed code pass: persistent CTAs (2 per SM), a producer lane streams
 // 8-row x 2048-column tiles of X into a QS_STAGES-deep shared-memory ring with
 // cp.async.bulk (the copy engine keeps up to QS_STAGES x 32 KB per CTA in
@@ -557,7 +603,7 @@ constexpr int QS_STAGE_BYTES = QS_ROWS * QS_VECS * 16;
 __global__ void __launch_bounds__(288) quantize_bulk_kernel(
     const __half* __restrict__ x, int64_t M, int64_t K, int64_t ldx,
     const uint32_t* __restrict__ col_mask, const double* __restrict__ row_s,
-    int8_t* __restrict__ xq, int64_t ldq) {
+    int8_t* __restrict__ xq, int64_t ldq, const PerCallFix f) {
     extern __shared__ __align__(128) uint8_t qb_sm[];
     __shared__ __align__(8) uint64_t full[QS_STAGES], empty[QS_STAGES];
     const int64_t nvec = K >> 3;
@@ -590,6 +636,12 @@ __global__ void __launch_bounds__(288) quantize_bulk_kernel(
             }
         }
         return;
+    }
+    if (f.p_count != nullptr) {  // weight-stationary: patched columns' codes first (the ring fills meanwhile)
+        const int32_t np = *f.p_count;
+        for (int32_t p = blockIdx.x; p < np; p += gridDim.x)
+            for (int64_t k0 = threadIdx.x * 8; k0 < ldq; k0 += 256 * 8)
+                patch_chunk(f.w, f.K, f.ldw, col_mask, f.p_idx, f.p_amax, f.p_src, f.q2, f.wq_p, ldq, p, k0);
     }
     int i = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
@@ -1208,24 +1260,34 @@ size_t row_prologue_scratch_bytes(int64_t M, int64_t K) {
 cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                                 uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
                                 int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
-                                void* scratch, cudaStream_t st, uint32_t* zero2, int64_t zero2_n) {
+                                void* scratch, cudaStream_t st, const PerCallFix* fix) {
     cudaError_t e;
-    if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq) ||
-        rp1_ok(M, K, ldx, ldq, x, xq)) {
-        if (zero2 != nullptr && zero2_n > 0) {
+    uint32_t* zero2 = fix != nullptr ? reinterpret_cast<uint32_t*>(fix->p_count) : nullptr;
+    const int64_t zero2_n = fix != nullptr ? fixup_zero_words(fix->N) : 0;
+    const bool split = M > 0 && scratch != nullptr && row_prologue_split_ok(K, ldx, ldq, x, xq) &&
+                       !rp1_ok(M, K, ldx, ldq, x, xq);
+    if (!split) {  // unfused forms: the per-call weight work runs as its own launches
+        if (zero2 != nullptr) {
             if ((e = launch_pdl(zero_u32_kernel, dim3(static_cast<unsigned>(imin64((zero2_n + 255) / 256, 64))),
                                 dim3(256), 0, st, zero2, zero2_n)))
                 return e;
             count_launch();
         }
+        if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq)) {
+            if ((e = launch_outlier_scan(x, M, K, ldx, alpha, mask, nullptr, st))) return e;
+            if ((e = launch_outlier_compact(mask, K, o_idx, o_count, st))) return e;
+            e = launch_quantize_rows(x, M, K, ldx, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, st);
+        } else {
+            e = launch_rp1(x, M, K, ldx, alpha, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, scratch, st);
+        }
+        if (e || fix == nullptr) return e;
+        if ((e = launch_gather_fixup(fix->w, fix->K, fix->N, fix->ldw, mask, o_idx, o_count, o_cap, fix->wo,
+                                     fix->ldwo, fix->amax_full, fix->cand_v, fix->cand_r, fix->p_count,
+                                     fix->p_idx, fix->p_amax, fix->p_src, st)))
+            return e;
+        return launch_patch_quantize(fix->w, fix->K, fix->N, fix->ldw, mask, fix->q2, fix->p_count,
+                                     fix->p_idx, fix->p_amax, fix->p_src, fix->wq_p, ldq, st);
     }
-    if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq)) {
-        if ((e = launch_outlier_scan(x, M, K, ldx, alpha, mask, nullptr, st))) return e;
-        if ((e = launch_outlier_compact(mask, K, o_idx, o_count, st))) return e;
-        return launch_quantize_rows(x, M, K, ldx, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, st);
-    }
-    if (rp1_ok(M, K, ldx, ldq, x, xq))
-        return launch_rp1(x, M, K, ldx, alpha, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, scratch, st);
     const int64_t nwords = (K + 31) >> 5, nvec = K >> 3, ng = (K + 63) >> 6;
     uint16_t* gmax = static_cast<uint16_t*>(scratch);
     double* row_s = reinterpret_cast<double*>(static_cast<char*>(scratch) + ((M * ng * 2 + 255) / 256) * 256);
@@ -1251,11 +1313,21 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
         return e;
     count_launch();
     const int64_t rs_grid = imin64((M + 7) / 8, static_cast<int64_t>(sms) * 8);
-    if ((e = launch_pdl(row_scale_kernel, dim3(static_cast<unsigned>(rs_grid)), dim3(256), 0, st, x, M, K,
-                        ldx, static_cast<const uint32_t*>(mask), static_cast<const int32_t*>(o_idx),
-                        static_cast<const int32_t*>(o_count), static_cast<const uint16_t*>(gmax), ng,
-                        static_cast<const int32_t*>(dgrp), row_amax, row_s, xo, o_cap)))
-        return e;
+    const RowScaleArgs ra{x, M, K, ldx, mask, o_idx, o_count, gmax, ng, dgrp, row_amax, row_s, xo, o_cap};
+    if (fix == nullptr) {
+        if ((e = launch_pdl(row_scale_kernel, dim3(static_cast<unsigned>(rs_grid)), dim3(256), 0, st, ra)))
+            return e;
+    } else {
+        const int vec = (fix->N % 8 == 0) && (fix->ldw % 8 == 0) && (fix->ldwo % 8 == 0) &&
+                        (reinterpret_cast<uintptr_t>(fix->w) & 15u) == 0 &&
+                        (reinterpret_cast<uintptr_t>(fix->wo) & 15u) == 0;
+        const int64_t per = vec ? (fix->N >> 3) : fix->N;
+        const int64_t gx = imin64((per + 255) / 256, 16);
+        const int64_t blocks = rs_grid + o_cap * gx + (fix->N + 255) / 256;
+        if ((e = launch_pdl(row_scale_fix_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, ra,
+                            rs_grid, *fix, vec, gx)))
+            return e;
+    }
     count_launch();
     static bool configured = false;
     if (!configured) {
@@ -1265,8 +1337,10 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     }
     const int64_t ntiles = ((M + QS_ROWS - 1) / QS_ROWS) * ((nvec + QS_VECS - 1) / QS_VECS);
     const unsigned g = static_cast<unsigned>(imin64(ntiles, static_cast<int64_t>(sms) * 2));
+    PerCallFix pf{};
+    if (fix != nullptr) pf = *fix;
     if ((e = launch_pdl(quantize_bulk_kernel, dim3(g), dim3(288), QS_STAGES * QS_STAGE_BYTES, st, x, M, K, ldx,
-                        static_cast<const uint32_t*>(mask), static_cast<const double*>(row_s), xq, ldq)))
+                        static_cast<const uint32_t*>(mask), static_cast<const double*>(row_s), xq, ldq, pf)))
         return e;
     count_launch();
     return cudaGetLastError();
