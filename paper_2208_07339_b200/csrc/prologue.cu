@@ -22,6 +22,72 @@
 
 namespace i8mm {
 
+// ------------------------------------------------------------------ compact
+// One block (any multiple of 32 threads): prefix popcount over the mask words,
+// scatter the sorted outlier indices. Mask words are read through L2 (the
+// caller may be the scan's last CTA, whose atomics went to L2).
+// dgrp (optional, K <= 65536): [count, 32 bitmap words of 64-column groups
+// holding an outlier column, then the list of those groups] for row_scale.
+__device__ __forceinline__ void compact_block(const uint32_t* __restrict__ col_mask, int64_t K,
+                                              int32_t* __restrict__ o_idx, int32_t* __restrict__ o_count,
+                                              int32_t* __restrict__ dgrp) {
+    __shared__ int32_t warp_sums[32];
+    __shared__ uint32_t gbits[32];
+    __shared__ int32_t n_dg;
+    const int64_t nwords = (K + 31) >> 5;
+    const int64_t per = (nwords + blockDim.x - 1) / blockDim.x;
+    const int64_t w0 = threadIdx.x * per;
+    const int64_t w1 = min(nwords, w0 + per);
+    int32_t local = 0;
+    for (int64_t w = w0; w < w1; ++w) local += __popc(__ldcg(col_mask + w));
+    // block exclusive scan
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t incl = local;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        int32_t s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int32_t t = __shfl_up_sync(0xffffffffu, s, d);
+            if (lane >= d) s += t;
+        }
+        if (lane < nw) warp_sums[lane] = s;  // inclusive warp prefix
+    }
+    __syncthreads();
+    int32_t pos = incl - local + (wid > 0 ? warp_sums[wid - 1] : 0);
+    for (int64_t w = w0; w < w1; ++w) {
+        uint32_t m = __ldcg(col_mask + w);
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            o_idx[pos++] = static_cast<int32_t>((w << 5) + b);
+        }
+    }
+    if (threadIdx.x == blockDim.x - 1) *o_count = pos;
+    if (dgrp == nullptr) return;
+    if (threadIdx.x < 32) gbits[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) n_dg = 0;
+    __syncthreads();
+    const int64_t ng = (K + 63) >> 6;
+    for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+        const uint32_t m1 = (2 * g + 1 < nwords) ? __ldcg(col_mask + 2 * g + 1) : 0u;
+        if ((__ldcg(col_mask + 2 * g) | m1) != 0u) {
+            atomicOr(&gbits[g >> 5], 1u << (g & 31));
+            dgrp[33 + atomicAdd(&n_dg, 1)] = static_cast<int32_t>(g);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) dgrp[1 + threadIdx.x] = static_cast<int32_t>(gbits[threadIdx.x]);
+    if (threadIdx.x == 0) dgrp[0] = n_dg;
+}
+
 // ------------------------------------------------------------------ K1 scan
 // Vector path: each thread owns 8 consecutive columns (one 16-byte load per
 // row) for a chunk of rows; 4 adjacent lanes form one 32-bit mask word. The
@@ -38,7 +104,9 @@ __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M,
                                         int64_t ldx, uint32_t thr_bits, int64_t rows_per_block,
                                         uint32_t* __restrict__ col_mask,
                                         int32_t* __restrict__ nonfinite,
-                                        uint16_t* __restrict__ gmax, int64_t ng) {
+                                        uint16_t* __restrict__ gmax, int64_t ng,
+                                        int32_t* __restrict__ done_ctr, int32_t* __restrict__ o_idx,
+                                        int32_t* __restrict__ o_count, int32_t* __restrict__ dgrp) {
     pdl_wait();
     pdl_trigger();
     const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // vector col
@@ -101,6 +169,19 @@ __global__ void outlier_scan_vec_kernel(const __half* __restrict__ x, int64_t M,
     if ((lane & 3u) == 0 && word != 0 && live) atomicOr(col_mask + (v >> 2), word);
     if (nonfinite != nullptr && __any_sync(0xffffffffu, bad != 0) && lane == 0)
         atomicExch(nonfinite, 1);
+    if (done_ctr != nullptr) {  // the last CTA to finish compacts the final mask (saves a launch)
+        __shared__ int last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(done_ctr, 1) == static_cast<int>(gridDim.x * gridDim.y) - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            compact_block(col_mask, K, o_idx, o_count, dgrp);
+        }
+    }
 }
 
 // Scalar path for K % 8 != 0 or unaligned X: one column per thread.
@@ -134,11 +215,13 @@ __global__ void zero_u32_kernel(uint32_t* p, int64_t n) {
 }
 
 // two ranges in one launch (the mask and the caller's per-call counters)
-__global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n2) {
+__global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n2, uint32_t* one) {
     pdl_wait();
     pdl_trigger();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n + n2; i += stride) {
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i0 == 0) *one = 0u;
+    for (int64_t i = i0; i < n + n2; i += stride) {
         if (i < n) p[i] = 0u;
         else p2[i - n] = 0u;
     }
@@ -146,68 +229,12 @@ __global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n
 
 // ------------------------------------------------------------------ compact
 // One block: prefix popcount over the mask words, scatter sorted indices.
-// dgrp (optional, K <= 65536): [count, 32 bitmap words of 64-column groups
-// holding an outlier column, then the list of those groups] for row_scale.
 __global__ void outlier_compact_kernel(const uint32_t* __restrict__ col_mask, int64_t K,
                                        int32_t* __restrict__ o_idx, int32_t* __restrict__ o_count,
                                        int32_t* __restrict__ dgrp) {
-    __shared__ int32_t warp_sums[32];
-    __shared__ uint32_t gbits[32];
-    __shared__ int32_t n_dg;
     pdl_wait();
     pdl_trigger();
-    const int64_t nwords = (K + 31) >> 5;
-    const int64_t per = (nwords + blockDim.x - 1) / blockDim.x;
-    const int64_t w0 = threadIdx.x * per;
-    const int64_t w1 = min(nwords, w0 + per);
-    int32_t local = 0;
-    for (int64_t w = w0; w < w1; ++w) local += __popc(col_mask[w]);
-    // block exclusive scan
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int32_t incl = local;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += t;
-    }
-    if (lane == 31) warp_sums[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        const int nw = blockDim.x >> 5;
-        int32_t s = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            int32_t t = __shfl_up_sync(0xffffffffu, s, d);
-            if (lane >= d) s += t;
-        }
-        if (lane < nw) warp_sums[lane] = s;  // inclusive warp prefix
-    }
-    __syncthreads();
-    int32_t pos = incl - local + (wid > 0 ? warp_sums[wid - 1] : 0);
-    for (int64_t w = w0; w < w1; ++w) {
-        uint32_t m = col_mask[w];
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            o_idx[pos++] = static_cast<int32_t>((w << 5) + b);
-        }
-    }
-    if (threadIdx.x == blockDim.x - 1) *o_count = pos;
-    if (dgrp == nullptr) return;
-    if (threadIdx.x < 32) gbits[threadIdx.x] = 0u;
-    if (threadIdx.x == 0) n_dg = 0;
-    __syncthreads();
-    const int64_t ng = (K + 63) >> 6;
-    for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
-        const uint32_t m1 = (2 * g + 1 < nwords) ? col_mask[2 * g + 1] : 0u;
-        if ((col_mask[2 * g] | m1) != 0u) {
-            atomicOr(&gbits[g >> 5], 1u << (g & 31));
-            dgrp[33 + atomicAdd(&n_dg, 1)] = static_cast<int32_t>(g);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) dgrp[1 + threadIdx.x] = static_cast<int32_t>(gbits[threadIdx.x]);
-    if (threadIdx.x == 0) dgrp[0] = n_dg;
+    compact_block(col_mask, K, o_idx, o_count, dgrp);
 }
 
 // ------------------------------------------------------------------ K2 rows
@@ -774,7 +801,8 @@ cudaError_t launch_outlier_scan(const __half* x, int64_t M, int64_t K, int64_t l
         const int64_t cb = (nvec + 255) / 256;
         const int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
         outlier_scan_vec_kernel<false><<<dim3(static_cast<unsigned>(cb), rb), 256, 0, st>>>(
-            x, M, K, ldx, alpha_threshold_bits(alpha), rpb, col_mask, nonfinite, nullptr, 0);
+            x, M, K, ldx, alpha_threshold_bits(alpha), rpb, col_mask, nonfinite, nullptr, 0, nullptr,
+            nullptr, nullptr, nullptr);
     } else {
         const int64_t cb = (K + 255) / 256;
         const int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
@@ -1214,7 +1242,9 @@ static cudaError_t launch_rp1(const __half* x, int64_t M, int64_t K, int64_t ldx
         const int64_t rpb = 4, rbs = (seed_rows + rpb - 1) / rpb;
         if ((e = launch_pdl(outlier_scan_vec_kernel<false>, dim3(static_cast<unsigned>(cb), static_cast<unsigned>(rbs)),
                             dim3(256), 0, st, x, seed_rows, K, ldx, alpha_threshold_bits(alpha), rpb, mask,
-                            static_cast<int32_t*>(nullptr), static_cast<uint16_t*>(nullptr), int64_t(0))))
+                            static_cast<int32_t*>(nullptr), static_cast<uint16_t*>(nullptr), int64_t(0),
+                            static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                            static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr))))
             return e;
         count_launch();
     }
@@ -1252,7 +1282,7 @@ static cudaError_t launch_rp1(const __half* x, int64_t M, int64_t K, int64_t ldx
 }
 size_t row_prologue_scratch_bytes(int64_t M, int64_t K) {
     const int64_t ng = (K + 63) >> 6;
-    const size_t two = static_cast<size_t>(((M * ng * 2 + 255) / 256) * 256 + M * 8 + (33 + ng) * 4);
+    const size_t two = static_cast<size_t>(((M * ng * 2 + 255) / 256) * 256 + M * 8 + (34 + ng) * 4);
     const size_t one = rp1_scratch_bytes(M, K);
     return one > two ? one : two;
 }
@@ -1292,11 +1322,13 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     uint16_t* gmax = static_cast<uint16_t*>(scratch);
     double* row_s = reinterpret_cast<double*>(static_cast<char*>(scratch) + ((M * ng * 2 + 255) / 256) * 256);
     int32_t* dgrp = reinterpret_cast<int32_t*>(row_s + M);
+    int32_t* done_ctr = dgrp + 33 + ng;  // scan CTAs finished (the last one compacts)
     const int sms = num_sms();
     {
         const int64_t n2 = zero2 != nullptr ? zero2_n : 0;
-        if ((e = launch_pdl(zero2_u32_kernel, dim3(static_cast<unsigned>(imin64((nwords + n2 + 255) / 256, 1024))),
-                            dim3(256), 0, st, mask, nwords, zero2, n2)))
+        if ((e = launch_pdl(zero2_u32_kernel, dim3(static_cast<unsigned>(imin64((nwords + n2 + 256) / 256, 1024))),
+                            dim3(256), 0, st, mask, nwords, zero2, n2,
+                            reinterpret_cast<uint32_t*>(done_ctr))))
             return e;
         count_launch();
     }
@@ -1305,11 +1337,7 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
     if ((e = launch_pdl(outlier_scan_vec_kernel<true>, dim3(static_cast<unsigned>(cb), rb), dim3(256), 0, st,
                         x, M, K, ldx, alpha_threshold_bits(alpha), rpb, mask,
-                        static_cast<int32_t*>(nullptr), gmax, ng)))
-        return e;
-    count_launch();
-    if ((e = launch_pdl(outlier_compact_kernel, dim3(1), dim3(1024), 0, st, static_cast<const uint32_t*>(mask),
-                        K, o_idx, o_count, dgrp)))
+                        static_cast<int32_t*>(nullptr), gmax, ng, done_ctr, o_idx, o_count, dgrp)))
         return e;
     count_launch();
     const int64_t rs_grid = imin64((M + 7) / 8, static_cast<int64_t>(sms) * 8);
