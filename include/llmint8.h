@@ -180,6 +180,9 @@ int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, in
  * kernels. The workspace layout depends on the routing, so set max_m before
  * sizing a workspace. */
 void i8mm_debug_set_decode_max_m(int max_m);
+/* Programmatic dependent launch on the prefill path: 1 on (default), 0 off
+   (same as I8MM_PDL=0); for A/B measurements. */
+void i8mm_debug_set_pdl(int on);
 int i8mm_linear_uses_decode(int64_t M, int64_t K, int64_t N);
 /* Dev tool: per-CTA %globaltimer stamps of the decode kernel (16 u64 per CTA,
  * device buffer sized for one CTA per SM; NULL disables). */

@@ -58,6 +58,7 @@ EXPORTED_SYMBOLS = (
     "i8mm_linear_workspace_views",
     "i8mm_linear_weight_views",
     "i8mm_debug_set_decode_max_m",
+    "i8mm_debug_set_pdl",
     "i8mm_linear_uses_decode",
     "i8mm_debug_decode_timeline",
     "i8mm_tensor_stats",
@@ -89,6 +90,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_launch_count": ([], ctypes.c_uint64),
         "i8mm_debug_set_gemm_variant": ([I32, I32], None),
         "i8mm_debug_set_decode_max_m": ([I32], None),
+        "i8mm_debug_set_pdl": ([I32], None),
         "i8mm_linear_uses_decode": ([I64, I64, I64], I32),
         "i8mm_debug_decode_timeline": ([P], None),
         "i8mm_outlier_scan": ([P, I64, I64, I64, F32, P, P, P], I32),

@@ -21,13 +21,13 @@ namespace i8mm {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+static int g_pdl = -1;
 bool pdl_enabled() {
-    static int on = -1;
-    if (on < 0) {
+    if (g_pdl < 0) {
         const char* e = getenv("I8MM_PDL");
-        on = (e && e[0] == '0') ? 0 : 1;
+        g_pdl = (e && e[0] == '0') ? 0 : 1;
     }
-    return on == 1;
+    return g_pdl == 1;
 }
 
 int num_sms() {
@@ -410,6 +410,8 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
 }
 
 // ---------------------------------------------------------------- linear layer
+void i8mm_debug_set_pdl(int on) { g_pdl = on ? 1 : 0; }
+
 void i8mm_debug_set_decode_max_m(int max_m) {
     g_decode_max_m = max_m < 0 ? 0 : (max_m > kDecodeMaxM ? kDecodeMaxM : max_m);
 }

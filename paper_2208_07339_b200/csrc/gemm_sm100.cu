@@ -198,7 +198,6 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const TileSpace ts = tile_space(p);
     const uint32_t cl_rank = C::CLUSTER > 1 ? cluster_ctarank() : 0u;
     const uint32_t crank = cl_rank % CG;            // rank within the CTA pair
     const uint32_t pair = cl_rank / CG;             // which pair of the cluster
@@ -233,6 +232,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem_base = bars->tmem_slot;
     pdl_wait();  // setup above overlaps the predecessor's tail (programmatic dependent launch)
     pdl_trigger();
+    // the live tile count reads the patch counter written by the prologue:
+    // only after the dependency wait
+    const TileSpace ts = tile_space(p);
 
     if (warp == 0) {
         // ===================== TMA producer =====================

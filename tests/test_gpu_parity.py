@@ -740,3 +740,18 @@ def test_prologue_late_outlier_columns(p, one_read):
     r = subprocess.run([sys.executable, "-c", _LATE_SCRIPT.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "LATE OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_alternating_decode_prefill_calls_stable(p, oracle_mod):
+    """Decode-routed and prefill calls of one module interleaved back to back
+    (programmatic dependent launch chains the prefill kernels; workspaces are
+    recycled by the caching allocator): every call must reproduce the oracle,
+    including patched columns (heavy outlier rows in W force patches)."""
+    x, w = _ws_case(11, 64, 1024, 700, 6, 6)
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda(), alpha=6.0)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    refs = {m: torch.from_numpy(oracle_mod.c_llm_int8_matmul(x[:m], w, 6.0).output) for m in (8, 16, 32, 64)}
+    for _ in range(6):
+        for m in (16, 32, 8, 64):
+            y = lin.matmul(x16[:m].contiguous(), exact=True)
+            assert torch.equal(y.cpu(), refs[m]), m
