@@ -1,7 +1,8 @@
 """cfg3 decode sweep (dev tool): OPT-13B projections at M = 1..256 tokens.
 
 Times Int8Linear.forward (weight-stationary) per projection with CUDA events
-and reports the HBM roofline fraction of the weight stream:
+(median of 50 calls, each after a 1 GiB L2 flush) and reports the HBM roofline
+fraction of the weight stream:
 bytes = K*N (int8 WqT) + 2*M*K (X) + 2*M*N (Y) + 2*|O|*N (fp16 outlier rows)
 + 4*N (column amax), against MEASURED_PEAKS.json hbm_gbs.
 """
@@ -26,7 +27,7 @@ def t_ev(fn, iters=50, warm=5):
         fn()
     torch.cuda.synchronize()
     flush = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")  # keeps the GPU busy while the host enqueues
-    tot = 0.0
+    ts = []
     for _ in range(iters):
         flush.zero_()  # L2 flush: the weight stream must come from HBM
         s = torch.cuda.Event(enable_timing=True)
@@ -35,8 +36,10 @@ def t_ev(fn, iters=50, warm=5):
         fn()
         e.record()
         e.synchronize()
-        tot += s.elapsed_time(e)
-    return tot / iters
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    t_ev.last = ts
+    return sum(ts) / iters
 
 
 def main():
@@ -58,7 +61,12 @@ def main():
             o = lin.last_stats().get("decomposed_cols", 0)
             byts = k * n + 2 * m * k + 2 * m * n + 2 * o * n + 4 * n
             gbs = byts / (ms * 1e-3) / 1e9
+            tl = t_ev.last
+            # median per-call time: a rare host-side stall inside the timed loop (caching-allocator
+            # segment growth, tens of ms) would otherwise dominate a mean over 50 calls
+            ms = tl[len(tl) // 2]
             rows.append({"proj": name, "m": m, "k": k, "n": n, "us": ms * 1e3, "o": o,
+                         "us_mean": sum(tl) / len(tl) * 1e3, "us_max": tl[-1] * 1e3,
                          "gbs": gbs, "frac_hbm": gbs / hbm,
                          "tops": 2.0 * m * n * k / (ms * 1e-3) / 1e12})
             print(json.dumps(rows[-1]), flush=True)
