@@ -257,6 +257,8 @@ struct Workspace {
     int64_t n_tiles;
     uint32_t* thr_word;  // alpha threshold bits, written by the prologue entry
     void* rp_scratch;    // prefill: per-row group maxima + f64 row scales (launch_row_prologue)
+    int32_t* sk_c32;     // prefill M <= 128 (linear): split-K partial sums, then tile counters
+    int64_t sk_ld, sk_words;
     int64_t ldq, o_cap;
     size_t bytes;
 };
@@ -327,6 +329,11 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
         }
     }
     if (!w.decode) w.rp_scratch = reinterpret_cast<void*>(take(row_prologue_scratch_bytes(M > 0 ? M : 1, K)));
+    if (linear && !w.decode && gemm_split_factor(M, N, K) > 1) {
+        w.sk_ld = gemm_split_cols(N, true);  // column-major partials: sk_ld columns x M rows
+        w.sk_words = M * w.sk_ld + gemm_split_tiles(N, true);
+        w.sk_c32 = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(w.sk_words)));
+    }
     w.bytes = p - p0;
     return w;
 }
@@ -532,8 +539,9 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
     if (ws.decode) return cuda_status(launch_set_word(ws.thr_word, alpha_threshold_bits(alpha), st));
     // row side (+ the fixup counters zeroed in the same first launch), then
     // W[O, :] gather + column fixup in one launch, then the patched codes
-    const PerCallFix fix{wh, K, N, ldw, ws.wo, round_up(N, 8), b.col_amax, b.cand_v, b.cand_r, b.q2,
-                         ws.p_count, ws.p_idx, ws.p_amax, ws.p_src, ws.wq_p};
+    const PerCallFix fix{ws.sk_c32, ws.sk_c32 != nullptr ? ws.sk_words : 0, wh, K, N, ldw, ws.wo, round_up(N, 8),
+                         b.col_amax, b.cand_v, b.cand_r, b.q2, ws.p_count, ws.p_idx, ws.p_amax, ws.p_src,
+                         ws.wq_p};
     if (launch_row_prologue(xh, M, K, ldx, alpha, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
                             ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st, &fix))
         return I8MM_ERR_CUDA;
@@ -598,6 +606,12 @@ static int linear_gemm_rows_impl(const void* x, int64_t ldx, int64_t M, const vo
     g.patch_idx = ws.p_idx;
     g.patch_amax = ws.p_amax;
     g.patch_mask = reinterpret_cast<const uint32_t*>(ws.p_count) + 4;
+    if (ws.sk_c32 != nullptr && row0 == 0 && rows == M) {  // split-K scratch (zeroed by the prologue)
+        g.c32 = ws.sk_c32;
+        g.c32_rows = M;
+        g.c32_cnt = ws.sk_c32 + M * ws.sk_ld;
+        g.c32_tiles = gemm_split_tiles(N, true);
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (launch_gemm_sm100(g, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
     return I8MM_OK;

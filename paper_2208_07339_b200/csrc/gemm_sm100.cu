@@ -114,6 +114,13 @@ struct Params {
     int dbg_epi;    // A/B knob (I8MM_DBG_EPI): bit 0 skips the outlier FMAs, bit 1 the stores
     int tma_y;      // tmap_y is valid (fp16 Y, 16-byte aligned rows)
     int group_m;    // raster: m-tiles per group sharing each B panel in L2
+    // split-K (CG = 1 only): ksplit units per tile, each over a K-block range;
+    // partials are added into c32 (column-major, c32_rows rows: one red per
+    // lane covers 32 consecutive rows), the last unit of a tile runs the epilogue
+    int ksplit;
+    int32_t* c32;
+    int64_t c32_rows;
+    int32_t* c32_cnt;
 };
 
 struct TileSpace {
@@ -242,7 +249,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t pol = l2_policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cluster_id; t < ts.total; t += n_clusters) {
+            for (int u = cluster_id; u < ts.total * p.ksplit; u += n_clusters) {
+                const int t = u / p.ksplit, sl = u % p.ksplit;
+                const int kb0 = sl * p.num_kb / p.ksplit, kb1 = (sl + 1) * p.num_kb / p.ksplit;
                 int m_blk, n_blk;
                 const bool is_patch = tile_coords(p, ts, t, m_blk, n_blk);
                 const CUtensorMap* map_b = is_patch ? &tmap_p : &tmap_b;
@@ -254,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 uint16_t b_mask = 0;
 #pragma unroll
                 for (int q = 0; q < MC; ++q) b_mask |= static_cast<uint16_t>(1u << (q * CG + crank));
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1u);
                     if constexpr (CG == 2) {
                         // the pair leader's full barrier counts every byte landing in the pair
@@ -287,13 +296,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
+        for (int u = cluster_id; u < ts.total * p.ksplit; u += n_clusters, ++it) {
+            const int sl = u % p.ksplit;
+            const int kb0 = sl * p.num_kb / p.ksplit, kb1 = (sl + 1) * p.num_kb / p.ksplit;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1u);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-            for (int kb = 0; kb < p.num_kb; ++kb) {
+            for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&bars->full[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
@@ -303,8 +314,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int k = 0; k < BK / UMMA_K; ++k) {
                         const uint64_t ad = smem_desc_k_sw128(a0 + k * UMMA_K);
                         const uint64_t bd = smem_desc_k_sw128(b0 + k * UMMA_K);
-                        if constexpr (CG == 2) mma_i8_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-                        else mma_i8(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+                        if constexpr (CG == 2) mma_i8_pair(d_tmem, ad, bd, idesc, accum);
+                        else mma_i8(d_tmem, ad, bd, idesc, accum);
                     }
                     // frees the smem slot (in both CTAs of a pair) when the MMAs finish
                     // (with MC > 1 the slot also holds B pieces written by the other
@@ -342,8 +354,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         // shuffle the 32 accumulators between registers at every join)
         const int n_cls = n_out <= 4 ? 4 : (n_out <= 8 ? 8 : WO_CAP);
         uint32_t stg_cnt = 0;  // TS: output boxes issued by this warp
+        __shared__ int split_last;
         int it = 0;
-        for (int t = cluster_id; t < ts.total; t += n_clusters, ++it) {
+        for (int u = cluster_id; u < ts.total * p.ksplit; u += n_clusters, ++it) {
+            const int t = u / p.ksplit;
             int m_blk, n_blk;
             const bool is_patch = tile_coords(p, ts, t, m_blk, n_blk);
             const int acc = it & 1;
@@ -419,19 +433,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
-            for (int cc = 0; cc < COLS_PER_EPI_WARP / 32; ++cc) {
-                const int ch = half * (COLS_PER_EPI_WARP / 32) + cc;
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(t_row + ch * 32, r);
-                tmem_ld_wait();
+            // one 32-column chunk of this thread's row: dequant + outlier term + store
+            auto emit = [&](int ch, uint32_t (&r)[32]) {
                 const int64_t cbase = col0 + ch * 32;
-                if (cbase >= n_live) continue;  // warp-uniform
+                if (cbase >= n_live) return;  // warp-uniform
                 // columns owned by a patch tile are skipped by the main tile (same launch)
                 const uint32_t pm = (!mapped && p.patch_mask != nullptr) ? p.patch_mask[cbase >> 5] : 0u;
                 // TS: whole 32 x 32 box through smem + TMA (rows >= M, cols >= N clipped by TMA)
                 const bool tma_chunk = TS && !mapped && pm == 0u && p.tma_y;
-                if (!tma_chunk && !row_ok) continue;
+                if (!tma_chunk && !row_ok) return;
                 const bool full_chunk = !mapped && pm == 0u && p.vec_store && cbase + 32 <= n_live;
                 if constexpr (EPI == EPI_I32) {
                     int32_t* yr = reinterpret_cast<int32_t*>(p.y) + row * p.ldy;
@@ -575,6 +585,24 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                     }
                 }
+                        };
+            const bool split = CG == 1 && p.ksplit > 1;
+            // split-K: c32 column of this tile's first column (patch tiles after the main ones)
+            const int64_t c32_col = (is_patch ? static_cast<int64_t>(ts.n_tiles) * BN : 0) +
+                                    static_cast<int64_t>(n_blk) * BN;
+#pragma unroll 1
+            for (int cc = 0; cc < COLS_PER_EPI_WARP / 32; ++cc) {
+                const int ch = half * (COLS_PER_EPI_WARP / 32) + cc;
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(t_row + ch * 32, r);
+                tmem_ld_wait();
+                if (!split) {
+                    emit(ch, r);
+                } else if (row_ok) {  // add this K-range's partial sums (fire-and-forget reds)
+                    int32_t* cr = p.c32 + (c32_col + ch * 32) * p.c32_rows + row;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) red_add_s32(cr + j * p.c32_rows, static_cast<int32_t>(r[j]));
+                }
             }
             // accumulator drained: hand TMEM back to the MMA warp
             tc_fence_before();
@@ -582,6 +610,27 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lane == 0) {
                 if constexpr (CG == 2) mbar_arrive_remote(&bars->tmem_empty[acc], leader_rank);
                 else mbar_arrive(&bars->tmem_empty[acc]);
+            }
+            if constexpr (CG == 1) {
+                if (split) {  // the tile's last K-range to arrive runs the epilogue on the sums
+                    __threadfence();
+                    named_bar_sync(2, EPI_THREADS);
+                    if (et == 0) split_last = atomicAdd(p.c32_cnt + t, 1) == p.ksplit - 1;
+                    named_bar_sync(2, EPI_THREADS);
+                    if (split_last) {
+                        __threadfence();
+#pragma unroll 1
+                        for (int cc = 0; cc < COLS_PER_EPI_WARP / 32; ++cc) {
+                            const int ch = half * (COLS_PER_EPI_WARP / 32) + cc;
+                            uint32_t r[32];
+                            const int32_t* cr = p.c32 + (c32_col + ch * 32) * p.c32_rows + (row_ok ? row : 0);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                r[j] = row_ok ? static_cast<uint32_t>(__ldcg(cr + j * p.c32_rows)) : 0u;
+                            emit(ch, r);
+                        }
+                    }
+                }
             }
         }
         if (TS && lane == 0) tma_store_wait<0>();  // staged outputs fully written
@@ -685,7 +734,8 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
         cudaGetLastError();
     });
     if (attr_err != cudaSuccess) return attr_err;
-    const int64_t clusters = max_tiles < max_clusters ? max_tiles : max_clusters;
+    const int64_t units = max_tiles * p.ksplit;
+    const int64_t clusters = units < max_clusters ? units : max_clusters;
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, tp, ty, p);
@@ -729,6 +779,32 @@ static int gemm_mc_override() {
 void set_gemm_variant(int cg, int mc) {
     g_cg_override = cg;
     g_mc_override = mc;
+}
+
+int64_t gemm_split_tiles(int64_t N, bool patches) {
+    const int64_t nt = (N + gemm::BN - 1) / gemm::BN;
+    return patches ? 2 * nt : nt;
+}
+int64_t gemm_split_cols(int64_t N, bool patches) { return gemm_split_tiles(N, patches) * gemm::BN; }
+
+// K-split of the single-m-tile GEMM: units ~ one per SM, each keeping >= 16
+// K-blocks (2 KB of K), and only for K >= 8192 where the per-unit costs
+// (partial-sum reds, the last unit's read-back, zeroing the scratch) pay:
+// measured OPT-13B fc2 (K = 20480) M = 32..128: 96-102 -> 61-72 us; qkvo
+// (K = 5120) lost 4-6 us, so it is not split. 1 = no split.
+int gemm_split_factor(int64_t M, int64_t N, int64_t K) {
+    static int off = -1;
+    if (off < 0) {
+        const char* e = getenv("I8MM_NO_SPLITK");
+        off = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (off || M <= 0 || M > gemm::BM || K < 8192) return 1;
+    const int64_t num_kb = (K + gemm::BK - 1) / gemm::BK;
+    const int64_t main_tiles = (N + gemm::BN - 1) / gemm::BN;
+    int64_t sk = num_sms() / (main_tiles > 0 ? main_tiles : 1);
+    if (sk > num_kb / 16) sk = num_kb / 16;
+    if (sk > 16) sk = 16;
+    return sk >= 2 ? static_cast<int>(sk) : 1;
 }
 
 cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
@@ -784,6 +860,17 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     const int elt = (epi == EPI_F16) ? 2 : 4;
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
     p.dbg_epi = env_int("I8MM_DBG_EPI");
+    // split-K when one m-tile's N-tiles would leave most SMs idle (M <= 128)
+    p.ksplit = 1;
+    if (cg == 1 && a.c32 != nullptr && p.m_tiles == 1) {
+        const int sk = gemm_split_factor(a.M, a.N, a.K);
+        if (sk >= 2) {
+            p.ksplit = static_cast<int>(sk);
+            p.c32 = a.c32;
+            p.c32_rows = a.c32_rows;
+            p.c32_cnt = a.c32_cnt;
+        }
+    }
     {
         // Raster (measured, scripts/ab_raster.sh): when one wave of concurrent
         // tiles covers >= 2 full rows of N-tiles, B panels are reused within the

@@ -44,6 +44,8 @@ size_t row_prologue_scratch_bytes(int64_t M, int64_t K);
 // Weight-stationary per-call state that rides along with the row prologue
 // (W[O, :] gather, column fixup, patched codes; see percall_dev.cuh).
 struct PerCallFix {
+    int32_t* c32;       // split-K scratch zeroed with the mask (or nullptr)
+    int64_t c32_words;  // partial sums + counters
     const __half* w;
     int64_t K, N, ldw;
     __half* wo;
@@ -160,7 +162,20 @@ struct GemmArgs {
     const int32_t* patch_idx;
     const float* patch_amax;
     const uint32_t* patch_mask;  // bit j set: column j is patched (main tiles skip it)
+    // split-K for one m-tile (M <= 128) when few N-tiles would leave SMs idle
+    // (nullable): zeroed int32 partial sums, column-major [cols x c32_rows]
+    // (cols = gemm_split_cols: main and patch tiles), and per-tile arrival
+    // counters [c32_tiles]
+    int32_t* c32;
+    int64_t c32_rows;
+    int32_t* c32_cnt;
+    int64_t c32_tiles;
 };
+
+// split-K scratch of the single-m-tile GEMM: c32 [cols x M] + counters
+int64_t gemm_split_cols(int64_t N, bool patches);
+int gemm_split_factor(int64_t M, int64_t N, int64_t K);  // 1 = no split
+int64_t gemm_split_tiles(int64_t N, bool patches);
 
 cudaError_t launch_gemm_sm100(const GemmArgs& args, int epi, cudaStream_t st);
 

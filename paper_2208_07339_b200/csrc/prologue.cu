@@ -215,7 +215,8 @@ __global__ void zero_u32_kernel(uint32_t* p, int64_t n) {
 }
 
 // two ranges in one launch (the mask and the caller's per-call counters)
-__global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n2, uint32_t* one) {
+__global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n2, uint32_t* one,
+                                 uint32_t* p3, int64_t n3) {
     pdl_wait();
     pdl_trigger();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -225,6 +226,10 @@ __global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n
         if (i < n) p[i] = 0u;
         else p2[i - n] = 0u;
     }
+    // third range (split-K partial sums): 16-byte stores
+    uint4* q3 = reinterpret_cast<uint4*>(p3);
+    for (int64_t i = i0; i < (n3 >> 2); i += stride) q3[i] = make_uint4(0, 0, 0, 0);
+    for (int64_t i = (n3 & ~int64_t(3)) + i0; i < n3; i += stride) p3[i] = 0u;
 }
 
 // ------------------------------------------------------------------ compact
@@ -1303,6 +1308,12 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
                 return e;
             count_launch();
         }
+        if (fix != nullptr && fix->c32 != nullptr && fix->c32_words > 0) {
+            if ((e = launch_pdl(zero_u32_kernel, dim3(static_cast<unsigned>(imin64((fix->c32_words + 255) / 256, 1184))),
+                                dim3(256), 0, st, reinterpret_cast<uint32_t*>(fix->c32), fix->c32_words)))
+                return e;
+            count_launch();
+        }
         if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq)) {
             if ((e = launch_outlier_scan(x, M, K, ldx, alpha, mask, nullptr, st))) return e;
             if ((e = launch_outlier_compact(mask, K, o_idx, o_count, st))) return e;
@@ -1326,9 +1337,12 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     const int sms = num_sms();
     {
         const int64_t n2 = zero2 != nullptr ? zero2_n : 0;
-        if ((e = launch_pdl(zero2_u32_kernel, dim3(static_cast<unsigned>(imin64((nwords + n2 + 256) / 256, 1024))),
+        uint32_t* z3 = fix != nullptr ? reinterpret_cast<uint32_t*>(fix->c32) : nullptr;
+        const int64_t n3 = z3 != nullptr ? fix->c32_words : 0;
+        const int64_t work = nwords + n2 + n3 / 4 + 256;
+        if ((e = launch_pdl(zero2_u32_kernel, dim3(static_cast<unsigned>(imin64(work / 256 + 1, 1184))),
                             dim3(256), 0, st, mask, nwords, zero2, n2,
-                            reinterpret_cast<uint32_t*>(done_ctr))))
+                            reinterpret_cast<uint32_t*>(done_ctr), z3, n3)))
             return e;
         count_launch();
     }

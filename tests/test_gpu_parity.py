@@ -303,8 +303,11 @@ def _ws_case(seed, m, k, n, n_out, heavy_rows=0):
 @pytest.mark.parametrize("case", [(0, 256, 1024, 512, 6, 0), (1, 97, 1040, 328, 6, 2),
                                   (2, 130, 512, 300, 8, 8), (3, 64, 256, 1000, 3, 3),
                                   (4, 1, 512, 256, 6, 0), (5, 33, 3, 40, 2, 2),
-                                  (6, 600, 1024, 2000, 6, 6), (7, 300, 768, 1100, 5, 1)])
+                                  (6, 600, 1024, 2000, 6, 6), (7, 300, 768, 1100, 5, 1),
+                                  (8, 100, 8704, 700, 6, 6), (9, 40, 16384, 300, 4, 0)])
 def test_weight_stationary_matches_reference_semantics(p, oracle_mod, case):
+    """Cases 8-9 take the split-K GEMM (one m-tile, K >= 8192, few N-tiles),
+    case 8 with patched columns split as well."""
     seed, m, k, n, n_out, heavy = case
     x, w = _ws_case(seed, m, k, n, n_out, heavy)
     ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
