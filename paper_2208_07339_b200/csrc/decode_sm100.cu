@@ -885,6 +885,7 @@ static int decode_prefetch() {
 
 static unsigned long long* g_dbg = nullptr;
 void set_decode_timeline(unsigned long long* stamps) { g_dbg = stamps; }
+unsigned long long* debug_timeline() { return g_dbg; }
 
 template <int EPI>
 static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tp,

@@ -121,7 +121,16 @@ struct Params {
     int32_t* c32;
     int64_t c32_rows;
     int32_t* c32_cnt;
+    unsigned long long* dbg;  // per-CTA %globaltimer stamps (dev tool), nullable
 };
+
+__device__ __forceinline__ void gstamp(unsigned long long* dbg, int i) {
+    if (dbg != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        dbg[blockIdx.x * 16 + i] = t;
+    }
+}
 
 struct TileSpace {
     int n_tiles, main_total, patch_n, total;
@@ -205,6 +214,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) gstamp(p.dbg, 0);
     const uint32_t cl_rank = C::CLUSTER > 1 ? cluster_ctarank() : 0u;
     const uint32_t crank = cl_rank % CG;            // rank within the CTA pair
     const uint32_t pair = cl_rank / CG;             // which pair of the cluster
@@ -242,6 +252,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // the live tile count reads the patch counter written by the prologue:
     // only after the dependency wait
     const TileSpace ts = tile_space(p);
+    if (threadIdx.x == 0) gstamp(p.dbg, 1);
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -263,6 +274,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 uint16_t b_mask = 0;
 #pragma unroll
                 for (int q = 0; q < MC; ++q) b_mask |= static_cast<uint16_t>(1u << (q * CG + crank));
+                if (u == cluster_id) gstamp(p.dbg, 2);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&bars->empty[stage], phase ^ 1u);
                     if constexpr (CG == 2) {
@@ -307,6 +319,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&bars->full[stage], phase);
                 tc_fence_after();
+                if (lane == 0 && it == 0 && kb == kb0) gstamp(p.dbg, 3);
                 if (lane == 0) {
                     const uint32_t a0 = smem_addr(smem_a + stage * A_BYTES);
                     const uint32_t b0 = smem_addr(smem_b + stage * B_BYTES);
@@ -332,6 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     phase ^= 1u;
                 }
             }
+            if (lane == 0 && it == 0) gstamp(p.dbg, 4);
             if (lane == 0) {  // accumulator ready (both CTAs' epilogues)
                 if constexpr (CG == 2)
                     mma_commit_pair(&bars->tmem_full[acc], static_cast<uint16_t>(0x3u << leader_rank));
@@ -429,8 +443,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
 
+            if (warp == EPI_WARP0 && lane == 0 && it == 0) gstamp(p.dbg, 8);
             mbar_wait(&bars->tmem_full[acc], acc_phase);
             tc_fence_after();
+            if (warp == EPI_WARP0 && lane == 0 && it == 0) gstamp(p.dbg, 5);
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
             // one 32-column chunk of this thread's row: dequant + outlier term + store
@@ -604,6 +620,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int j = 0; j < 32; ++j) red_add_s32(cr + j * p.c32_rows, static_cast<int32_t>(r[j]));
                 }
             }
+            if (warp == EPI_WARP0 && lane == 0 && it == 0) gstamp(p.dbg, 6);
             // accumulator drained: hand TMEM back to the MMA warp
             tc_fence_before();
             __syncwarp();
@@ -637,6 +654,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     __syncthreads();
+    if (threadIdx.x == 0) gstamp(p.dbg, 7);
     if constexpr (C::CLUSTER > 1) cluster_sync_all();  // all CTAs done with TMEM and barriers
     if (warp == 2) {
         tc_fence_after();
@@ -798,6 +816,12 @@ int gemm_split_factor(int64_t M, int64_t N, int64_t K) {
         const char* e = getenv("I8MM_NO_SPLITK");
         off = (e && e[0] == '1') ? 1 : 0;
     }
+    static int force = -1;  // I8MM_SPLITK_FORCE=S: A/B measurements only
+    if (force < 0) {
+        const char* e = getenv("I8MM_SPLITK_FORCE");
+        force = (e && e[0]) ? atoi(e) : 0;
+    }
+    if (force >= 2 && M > 0 && M <= gemm::BM) return force;
     if (off || M <= 0 || M > gemm::BM || K < 8192) return 1;
     const int64_t num_kb = (K + gemm::BK - 1) / gemm::BK;
     const int64_t main_tiles = (N + gemm::BN - 1) / gemm::BN;
@@ -860,6 +884,7 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     const int elt = (epi == EPI_F16) ? 2 : 4;
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
     p.dbg_epi = env_int("I8MM_DBG_EPI");
+    p.dbg = debug_timeline();
     // split-K when one m-tile's N-tiles would leave most SMs idle (M <= 128)
     p.ksplit = 1;
     if (cg == 1 && a.c32 != nullptr && p.m_tiles == 1) {

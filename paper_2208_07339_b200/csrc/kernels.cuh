@@ -230,6 +230,7 @@ bool decode_fits(int64_t M, int64_t K, int64_t N);
 cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st);
 cudaError_t launch_set_word(uint32_t* dst, uint32_t value, cudaStream_t st);
 void set_decode_timeline(unsigned long long* stamps);
+unsigned long long* debug_timeline();  // the same buffer, also stamped by the GEMM (16 per CTA)
 void set_gemm_variant(int cg_override, int mc_override);
 
 }  // namespace i8mm
