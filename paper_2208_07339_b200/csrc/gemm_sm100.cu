@@ -74,7 +74,7 @@ struct __align__(8) Barriers {
     uint32_t tmem_slot;
 };
 
-constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(float);
+constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(__half);
 constexpr size_t SMEM_COLS = static_cast<size_t>(BN) * sizeof(double);
 constexpr int STG_BYTES = 32 * 32 * 2;  // one 32 x 32 fp16 staging tile
 constexpr size_t SMEM_STG = static_cast<size_t>(EPI_WARPS) * 2 * STG_BYTES;  // double-buffered per warp
@@ -172,22 +172,26 @@ __device__ __forceinline__ bool tile_coords(const Params& p, const TileSpace& ts
 
 __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0f : a; }
 
-// v[0..31] += sum_o xo[o] * wo[o][0..31] over NO staged (zero-padded) outlier rows,
-// packed f32x2 FMAs, no per-row guards.
+// v[0..31] += sum_o xo[o] * wo[o][0..31] over NO staged (zero-padded) outlier
+// rows: straight-line packed f32x2 FMAs, no per-row guards. The rows are staged
+// as fp16 (exact: they are fp16 values) and widened in registers, which halves
+// the epilogue's shared-memory wavefronts.
 template <int NO>
-__device__ __forceinline__ void outlier_fma(float2* v2, const float* xo_r, const float* wrow) {
+__device__ __forceinline__ void outlier_fma_h(float2* v2, const float* xo_r, const __half* wrow) {
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
         const float2 xv2 = make_float2(xo_r[o], xo_r[o]);
-        const float4* wr = reinterpret_cast<const float4*>(wrow + o * BN);
+        const uint4* wr = reinterpret_cast<const uint4*>(wrow + o * BN);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const float4 f = wr[u];
-            v2[2 * u] = __ffma2_rn(xv2, make_float2(f.x, f.y), v2[2 * u]);
-            v2[2 * u + 1] = __ffma2_rn(xv2, make_float2(f.z, f.w), v2[2 * u + 1]);
+        for (int u = 0; u < 4; ++u) {
+            const uint4 q = wr[u];
+            const __half2* h2 = reinterpret_cast<const __half2*>(&q);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v2[4 * u + e] = __ffma2_rn(xv2, __half22float2(h2[e]), v2[4 * u + e]);
         }
     }
 }
+
 
 template <int EPI, int CG, int MC>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + static_cast<size_t>(STAGES) * A_BYTES;
     uint8_t* smem_stg = smem + SMEM_OPERANDS;  // TS: per-warp output staging tiles
-    float* smem_wo = reinterpret_cast<float*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT);
+    __half* smem_wo_h = reinterpret_cast<__half*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT);
     double* smem_col = reinterpret_cast<double*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT + SMEM_WO);
     Barriers* bars = reinterpret_cast<Barriers*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT + SMEM_WO + SMEM_COLS);
 
@@ -260,6 +264,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t pol = l2_policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
+            long long w_empty = 0;
             for (int u = cluster_id; u < ts.total * p.ksplit; u += n_clusters) {
                 const int t = u / p.ksplit, sl = u % p.ksplit;
                 const int kb0 = sl * p.num_kb / p.ksplit, kb1 = (sl + 1) * p.num_kb / p.ksplit;
@@ -276,6 +281,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int q = 0; q < MC; ++q) b_mask |= static_cast<uint16_t>(1u << (q * CG + crank));
                 if (u == cluster_id) gstamp(p.dbg, 2);
                 for (int kb = kb0; kb < kb1; ++kb) {
+                    if (p.dbg != nullptr) {
+                        const long long c0 = clock64();
+                        mbar_wait(&bars->empty[stage], phase ^ 1u);
+                        w_empty += clock64() - c0;
+                    }
                     mbar_wait(&bars->empty[stage], phase ^ 1u);
                     if constexpr (CG == 2) {
                         // the pair leader's full barrier counts every byte landing in the pair
@@ -301,6 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
             }
+            if (p.dbg != nullptr) p.dbg[blockIdx.x * 16 + 14] = static_cast<unsigned long long>(w_empty);
         }
     } else if (warp == 1 && leader) {
         // ===================== MMA issuer (leader CTA) =====================
@@ -308,15 +319,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
+        long long w_full = 0, w_acc = 0;
         for (int u = cluster_id; u < ts.total * p.ksplit; u += n_clusters, ++it) {
             const int sl = u % p.ksplit;
             const int kb0 = sl * p.num_kb / p.ksplit, kb1 = (sl + 1) * p.num_kb / p.ksplit;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            if (p.dbg != nullptr) {
+                const long long c0 = clock64();
+                mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1u);
+                w_acc += clock64() - c0;
+            }
             mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1u);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
             for (int kb = kb0; kb < kb1; ++kb) {
+                if (p.dbg != nullptr) {
+                    const long long c0 = clock64();
+                    mbar_wait(&bars->full[stage], phase);
+                    w_full += clock64() - c0;
+                }
                 mbar_wait(&bars->full[stage], phase);
                 tc_fence_after();
                 if (lane == 0 && it == 0 && kb == kb0) gstamp(p.dbg, 3);
@@ -353,6 +375,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             __syncwarp();
         }
+        if (p.dbg != nullptr && lane == 0) {
+            p.dbg[blockIdx.x * 16 + 12] = static_cast<unsigned long long>(w_full);
+            p.dbg[blockIdx.x * 16 + 13] = static_cast<unsigned long long>(w_acc);
+        }
     } else if (warp >= EPI_WARP0) {
         // ===================== epilogue =====================
         const int quad = warp & 3;                       // TMEM lanes 32*quad .. +31
@@ -369,6 +395,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int n_cls = n_out <= 4 ? 4 : (n_out <= 8 ? 8 : WO_CAP);
         uint32_t stg_cnt = 0;  // TS: output boxes issued by this warp
         __shared__ int split_last;
+        long long w_tf = 0;
         int it = 0;
         for (int u = cluster_id; u < ts.total * p.ksplit; u += n_clusters, ++it) {
             const int t = u / p.ksplit;
@@ -406,12 +433,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             const int o = i / (BN / 8), v = i % (BN / 8);
                             const uint4 q = o < n_out ? *reinterpret_cast<const uint4*>(
                                 p.wo + static_cast<int64_t>(o) * p.ldwo + col0 + v * 8) : make_uint4(0, 0, 0, 0);
-                            const __half2* h2 = reinterpret_cast<const __half2*>(&q);
-                            float4* dst = reinterpret_cast<float4*>(smem_wo + o * BN + v * 8);
-                            const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]);
-                            const float2 f2 = __half22float2(h2[2]), f3 = __half22float2(h2[3]);
-                            dst[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
-                            dst[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
+                            *reinterpret_cast<uint4*>(smem_wo_h + o * BN + v * 8) = q;
                         }
                     } else {
                         for (int i = et; i < n_cls * BN; i += EPI_THREADS) {
@@ -423,7 +445,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 v = wo_fast ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + gc])
                                             : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + gc]);
                             }
-                            smem_wo[o * BN + j] = v;
+                            smem_wo_h[o * BN + j] = __float2half_rn(v);  // exact: v is an fp16 value
                         }
                     }
                 }
@@ -444,6 +466,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
 
             if (warp == EPI_WARP0 && lane == 0 && it == 0) gstamp(p.dbg, 8);
+            if (p.dbg != nullptr) {
+                const long long c0 = clock64();
+                mbar_wait(&bars->tmem_full[acc], acc_phase);
+                w_tf += clock64() - c0;
+            }
             mbar_wait(&bars->tmem_full[acc], acc_phase);
             tc_fence_after();
             if (warp == EPI_WARP0 && lane == 0 && it == 0) gstamp(p.dbg, 5);
@@ -516,10 +543,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                         if (n_out > 0 && !(p.dbg_epi & 1)) {
                             if (stage_wo) {
-                                const float* wrow = smem_wo + ch * 32;
-                                if (n_cls == 4) outlier_fma<4>(v2, xo_r, wrow);
-                                else if (n_cls == 8) outlier_fma<8>(v2, xo_r, wrow);
-                                else outlier_fma<WO_CAP>(v2, xo_r, wrow);
+                                const __half* wrow = smem_wo_h + ch * 32;
+                                if (n_cls == 4) outlier_fma_h<4>(v2, xo_r, wrow);
+                                else if (n_cls == 8) outlier_fma_h<8>(v2, xo_r, wrow);
+                                else outlier_fma_h<WO_CAP>(v2, xo_r, wrow);
                             } else {
                                 for (int o = 0; o < n_out; ++o) {
                                     const int64_t k = p.o_idx[o];
@@ -632,8 +659,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (split) {  // the tile's last K-range to arrive runs the epilogue on the sums
                     __threadfence();
                     named_bar_sync(2, EPI_THREADS);
+                    if (et == 0 && it == 0) gstamp(p.dbg, 9);
                     if (et == 0) split_last = atomicAdd(p.c32_cnt + t, 1) == p.ksplit - 1;
                     named_bar_sync(2, EPI_THREADS);
+                    if (et == 0 && it == 0) gstamp(p.dbg, 10);
                     if (split_last) {
                         __threadfence();
 #pragma unroll 1
@@ -646,11 +675,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 r[j] = row_ok ? static_cast<uint32_t>(__ldcg(cr + j * p.c32_rows)) : 0u;
                             emit(ch, r);
                         }
+                        if (et == 0) gstamp(p.dbg, 11);
                     }
                 }
             }
         }
         if (TS && lane == 0) tma_store_wait<0>();  // staged outputs fully written
+        if (p.dbg != nullptr && warp == EPI_WARP0 && lane == 0)
+            p.dbg[blockIdx.x * 16 + 15] = static_cast<unsigned long long>(w_tf);
     }
 
     __syncthreads();
