@@ -348,6 +348,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     if (warp == 2) tmem_alloc<TMEM_COLS>(&bars->tmem_slot);
+    // programmatic dependent launch: the weight prefetch above (weights are
+    // never written by the preceding kernels) overlaps the previous layer's
+    // tail; X, the threshold word and the workspace only after the wait
+    pdl_wait();
+    pdl_trigger();
 
     // ================= prologue (warps 1-7; warp 0 is issuing the prefetch)
     constexpr int PT = (NWARPS - 1) * 32;
@@ -902,11 +907,13 @@ static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, co
     cfg.blockDim = dim3(dec::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, dec::decode_fused_kernel<EPI>, tw, tx, tp, prm);
     count_launch();
     if (e != cudaSuccess) return e;
