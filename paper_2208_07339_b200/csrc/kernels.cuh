@@ -85,18 +85,13 @@ cudaError_t launch_weight_prepare(const __half* w, int64_t K, int64_t N, int64_t
                                   int8_t* q2, int64_t ldq, float* col_amax, uint16_t* cand_v,
                                   int32_t* cand_r, uint32_t* scratch_v, int32_t* scratch_r,
                                   cudaStream_t st);
-// p_count points at [count, pad x3, patched-column bit mask (ceil(N/32) words)]
+// Weight-stationary per-call work after an unfused row prologue, in two
+// launches: W[O, :] gather + column fixup (one grid; the p_count region
+// already zeroed), then the patched columns' codes.
+// p_count points at [count, pad x3, patched-column bit mask (ceil(N/32) words)];
 // q2: cached codes under each column's second-largest |w| (K-major, ldq);
 // p_src[p] = 1 when patch p's codes are q2's row (its top-1 row is the only
-// outlier among the candidates), else they are re-derived from W
-cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
-                                const uint32_t* mask, const float* amax_full,
-                                const uint16_t* cand_v, const int32_t* cand_r, const int8_t* q2,
-                                int32_t* p_count, int32_t* p_idx, float* p_amax, int32_t* p_src,
-                                int8_t* wq_p, int64_t ldq, cudaStream_t st);
-// Weight-stationary per-call work after the row prologue, in two launches:
-// W[O, :] gather + column fixup (one grid, p_count region already zeroed by
-// the row prologue), then the patched columns' codes.
+// outlier among the candidates), else they are re-derived from W.
 cudaError_t launch_gather_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                 const uint32_t* mask, const int32_t* o_idx, const int32_t* o_count,
                                 int64_t o_cap, __half* wo, int64_t ldwo, const float* amax_full,

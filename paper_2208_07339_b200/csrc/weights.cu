@@ -277,17 +277,6 @@ __global__ void topt_merge_kernel(int64_t N, int64_t chunks, const uint32_t* __r
 // candidates (full rescan only if every candidate row is an outlier row).
 // Columns whose amax changes are appended to the patch list.
 
-__global__ void fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N, int64_t ldw,
-                             const uint32_t* __restrict__ mask, const float* __restrict__ amax_full,
-                             const uint16_t* __restrict__ cand_v, const int32_t* __restrict__ cand_r,
-                             int32_t* __restrict__ p_count, int32_t* __restrict__ p_idx,
-                             float* __restrict__ p_amax, int32_t* __restrict__ p_src) {
-    pdl_wait();
-    pdl_trigger();
-    fixup_column(w, K, N, ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax, p_src,
-                 static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
-}
-
 // One launch for the two independent consumers of the outlier set: blocks
 // [0, cap * gx) gather W[O, :] (row t = b / gx), the rest run the column fixup.
 __global__ void gather_fixup_kernel(const __half* __restrict__ w, int64_t K, int64_t N, int64_t ldw,
@@ -449,28 +438,5 @@ cudaError_t launch_weight_prepare(const __half* w, int64_t K, int64_t N, int64_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_weight_fixup(const __half* w, int64_t K, int64_t N, int64_t ldw,
-                                const uint32_t* mask, const float* amax_full,
-                                const uint16_t* cand_v, const int32_t* cand_r, const int8_t* q2,
-                                int32_t* p_count, int32_t* p_idx, float* p_amax, int32_t* p_src,
-                                int8_t* wq_p, int64_t ldq, cudaStream_t st) {
-    const int64_t zw = 4 + (N + 31) / 32;  // count + patched-column mask
-    cudaError_t e;
-    if ((e = launch_pdl(zero_words_kernel, dim3(static_cast<unsigned>(imin64((zw + 255) / 256, 64))), dim3(256),
-                        0, st, reinterpret_cast<uint32_t*>(p_count), zw)))
-        return e;
-    count_launch();
-    if ((e = launch_pdl(fixup_kernel, dim3(static_cast<unsigned>((N + 255) / 256)), dim3(256), 0, st, w, K, N,
-                        ldw, mask, amax_full, cand_v, cand_r, p_count, p_idx, p_amax, p_src)))
-        return e;
-    count_launch();
-    const dim3 pgrid(static_cast<unsigned>((ldq + 2047) / 2048), static_cast<unsigned>(imin64(N, 256)));
-    if ((e = launch_pdl(patch_quantize_kernel, pgrid, dim3(256), 0, st, w, K, ldw, mask,
-                        static_cast<const int32_t*>(p_count), static_cast<const int32_t*>(p_idx),
-                        static_cast<const float*>(p_amax), static_cast<const int32_t*>(p_src), q2, wq_p, ldq)))
-        return e;
-    count_launch();
-    return cudaGetLastError();
-}
 
 }  // namespace i8mm
