@@ -299,7 +299,7 @@ def run_ours(args, layers, wl) -> None:
     for li, (m, k, n) in enumerate(layers):
         x, w, _ = planted_pair_device(m, k, n, 6, 20.0, seed=li, device=dev)
         if dist_on:
-            mods.append(ShardedInt8Linear(w, alpha=6.0))
+            mods.append(ShardedInt8Linear(w, alpha=6.0, fused_gather=False if args.nccl_gather else None))
         else:
             mods.append(pkg.Int8Linear(w, alpha=6.0))
         del w
@@ -452,7 +452,10 @@ def run_ours(args, layers, wl) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic",
             "config": {"workload": args.workload, "desc": wl["desc"], "layers_mkn": layers,
-                       "tokens": layers[0][0], "parallelism": f"N-shard x{world} + NCCL all-gather" if dist_on else "single",
+                       "tokens": layers[0][0], "parallelism": ((f"N-shard x{world} + all-gather fused into the GEMM epilogue (symmetric memory)"
+                                        if getattr(mods[0], "gather_path", None) == "fused-epilogue"
+                                        else f"N-shard x{world} + pipelined NCCL all-gather")
+                                       if dist_on else "single"),
                        "l2": ("inputs fit L2 (cfg1 is a parity config)" if args.workload == "cfg1" else
                               "weights 314 MB per step > L2 (no flush needed)" if wl.get("decode") else
                               "inputs larger than L2 (no flush needed)"),
@@ -500,6 +503,9 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--nccl-gather", action="store_true",
+                    help="under torchrun: the pipelined NCCL all-gather instead of the default "
+                         "all-gather fused into the GEMM epilogue (symmetric memory)")
     ap.add_argument("--cpu-sample-rows", type=int, default=0, help="0 = auto-size the sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparators", action="store_true")

@@ -187,6 +187,18 @@ int i8mm_linear_uses_decode(int64_t M, int64_t K, int64_t N);
 /* Dev tool: per-CTA %globaltimer stamps of the decode kernel (16 u64 per CTA,
  * device buffer sized for one CTA per SM; NULL disables). */
 void i8mm_debug_decode_timeline(void* stamps);
+/* Fused output all-gather for N-sharded layers (fp16 out): like
+ * i8mm_linear_forward, and every output element Y[i, j] is also stored, from the
+ * GEMM epilogue, to y_peers[q][i * ldy_peer + col_off + j] for q < n_peers
+ * (n_peers <= 8). y_peers are device pointers this device can store to: the
+ * other ranks' full-width Y buffers in NVLink peer memory (symmetric memory),
+ * this rank's own included. The caller orders the peers' reads after the
+ * writes (a cross-rank barrier). Decode-routed calls (M <= 16) store the block
+ * with copy-engine peer copies instead. */
+int i8mm_linear_forward_peers(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                              const void* wbuf, int64_t K, int64_t N, float alpha, void* y, int64_t ldy,
+                              void* workspace, size_t workspace_bytes, void* const* y_peers, int n_peers,
+                              int64_t ldy_peer, int64_t col_off, void* stream);
 /* introspection (tests): device pointers into the workspace / weight buffer.
  * workspace views: [o_count, o_idx, xq, row_amax, p_count, p_idx, p_amax, wq_p]
  * weight views:    [wq_t, col_amax, cand_v, cand_r(, q2)] */

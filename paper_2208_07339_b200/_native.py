@@ -55,6 +55,7 @@ EXPORTED_SYMBOLS = (
     "i8mm_linear_gemm",
     "i8mm_linear_gemm_rows",
     "i8mm_linear_forward",
+    "i8mm_linear_forward_peers",
     "i8mm_linear_workspace_views",
     "i8mm_linear_weight_views",
     "i8mm_debug_set_decode_max_m",
@@ -113,6 +114,8 @@ def _declare(lib: ctypes.CDLL) -> None:
                                    ctypes.c_size_t, I64, I64, P], I32),
         "i8mm_linear_forward": ([P, I64, I64, P, I64, P, I64, I64, F32, P, I64, I32, P,
                                  ctypes.c_size_t, P, P], I32),
+        "i8mm_linear_forward_peers": ([P, I64, I64, P, I64, P, I64, I64, F32, P, I64, P,
+                                       ctypes.c_size_t, P, I32, I64, I64, P], I32),
         "i8mm_linear_workspace_views": ([P, I64, I64, I64, P, I32], I32),
         "i8mm_linear_weight_views": ([P, I64, I64, P, I32], I32),
         "i8mm_dequantize_output": ([P, I64, I64, I64, P, P, P, I64, P], I32),

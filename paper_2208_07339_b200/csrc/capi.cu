@@ -550,10 +550,16 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
 
 // GEMM + epilogue over rows [row0, row0 + rows) of a prologue's workspace
 // (rows are independent once O and the row scales are known, gemm.py:210, 242)
+struct PeerOut {  // fused output all-gather destinations (i8mm_linear_forward_peers)
+    void* const* y;
+    int n;
+    int64_t ldy, col;
+};
+
 static int linear_gemm_rows_impl(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
                                  const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy,
                                  int out_kind, void* workspace, size_t workspace_bytes, int64_t row0,
-                                 int64_t rows, void* stream) {
+                                 int64_t rows, void* stream, const PeerOut* peers = nullptr) {
     if (int s = check_device()) return s;
     if (M <= 0 || K <= 0 || N <= 0 || ldy < N || !y || !wbuf || !workspace) return I8MM_ERR_ARGUMENT;
     if (row0 < 0 || rows < 0 || row0 + rows > M) return I8MM_ERR_ARGUMENT;
@@ -606,6 +612,14 @@ static int linear_gemm_rows_impl(const void* x, int64_t ldx, int64_t M, const vo
     g.patch_idx = ws.p_idx;
     g.patch_amax = ws.p_amax;
     g.patch_mask = reinterpret_cast<const uint32_t*>(ws.p_count) + 4;
+    if (peers != nullptr && peers->n > 0) {
+        if (peers->n > kMaxPeers || epi != EPI_F16) return I8MM_ERR_ARGUMENT;
+        g.n_peer = peers->n;
+        for (int q = 0; q < peers->n; ++q)
+            g.y_peer[q] = static_cast<char*>(peers->y[q]) + row0 * peers->ldy * 2;
+        g.peer_ldy = peers->ldy;
+        g.peer_col = peers->col;
+    }
     if (ws.sk_c32 != nullptr && row0 == 0 && rows == M) {  // split-K scratch (zeroed by the prologue)
         g.c32 = ws.sk_c32;
         g.c32_rows = M;
@@ -615,6 +629,33 @@ static int linear_gemm_rows_impl(const void* x, int64_t ldx, int64_t M, const vo
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (launch_gemm_sm100(g, epi, st) != cudaSuccess) return I8MM_ERR_CUDA;
     return I8MM_OK;
+}
+
+int i8mm_linear_forward_peers(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
+                              const void* wbuf, int64_t K, int64_t N, float alpha, void* y, int64_t ldy,
+                              void* workspace, size_t workspace_bytes, void* const* y_peers, int n_peers,
+                              int64_t ldy_peer, int64_t col_off, void* stream) {
+    if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && y_peers == nullptr) || col_off < 0 ||
+        ldy_peer < col_off + N)
+        return I8MM_ERR_ARGUMENT;
+    for (int q = 0; q < n_peers; ++q)
+        if (y_peers[q] == nullptr) return I8MM_ERR_ARGUMENT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (uses_decode(M, K, N)) {  // one decode launch, then copy-engine stores of the block to the peers
+        int s = i8mm_linear_forward(x, ldx, M, w, ldw, wbuf, K, N, alpha, y, ldy, I8MM_OUT_F16, workspace,
+                                    workspace_bytes, nullptr, stream);
+        if (s) return s;
+        for (int q = 0; q < n_peers; ++q)
+            if (cudaMemcpy2DAsync(static_cast<char*>(y_peers[q]) + col_off * 2, ldy_peer * 2, y, ldy * 2, N * 2, M,
+                                  cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return I8MM_ERR_CUDA;
+        return I8MM_OK;
+    }
+    int s = i8mm_linear_prologue(x, ldx, M, w, ldw, wbuf, K, N, alpha, workspace, workspace_bytes, stream);
+    if (s) return s;
+    const PeerOut peers{y_peers, n_peers, ldy_peer, col_off};
+    return linear_gemm_rows_impl(x, ldx, M, w, ldw, wbuf, K, N, y, ldy, I8MM_OUT_F16, workspace,
+                                 workspace_bytes, 0, M, stream, &peers);
 }
 
 int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,

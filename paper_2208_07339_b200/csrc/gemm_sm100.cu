@@ -122,6 +122,13 @@ struct Params {
     int64_t c32_rows;
     int32_t* c32_cnt;
     unsigned long long* dbg;  // per-CTA %globaltimer stamps (dev tool), nullable
+    // fused output all-gather (EPI_F16): every output row segment is also
+    // stored to n_peer peer buffers (NVLink peer memory of the other ranks'
+    // full Y, column offset peer_col); peer_vec: 16-byte aligned peer rows
+    void* y_peer[kMaxPeers];
+    int n_peer;
+    int64_t peer_ldy, peer_col;
+    int peer_vec;
 };
 
 __device__ __forceinline__ void gstamp(unsigned long long* dbg, int i) {
@@ -562,6 +569,34 @@ __global__ void __launch_bounds__(THREADS, 1)
                             }
                         }
                     }
+                    if constexpr (EPI == EPI_F16) {
+                        if (p.n_peer > 0 && row_ok) {  // fused all-gather: the same values to every peer
+                            uint4 pkv[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                uint32_t pk[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    __half2 h2 = __floats2half2_rn(v[8 * u + 2 * e], v[8 * u + 2 * e + 1]);
+                                    pk[e] = *reinterpret_cast<uint32_t*>(&h2);
+                                }
+                                pkv[u] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                            }
+                            for (int q = 0; q < p.n_peer; ++q) {
+                                __half* yq = reinterpret_cast<__half*>(p.y_peer[q]) + row * p.peer_ldy + p.peer_col;
+                                if (full_chunk && p.peer_vec) {
+#pragma unroll
+                                    for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(yq + cbase + 8 * u) = pkv[u];
+                                } else {
+                                    for (int j = 0; j < 32; ++j) {
+                                        const int64_t c = cbase + j;
+                                        if (c < n_live && !((pm >> j) & 1u))
+                                            yq[mapped ? cmap[c] : c] = __float2half_rn(v[j]);
+                                    }
+                                }
+                            }
+                        }
+                    }
                     if (p.dbg_epi & 2) {
                         if (v[0] == 1234.5f) reinterpret_cast<float*>(p.y)[0] = v[1];  // keep v live
                     } else if (tma_chunk) {
@@ -917,6 +952,17 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     p.vec_store = ((a.ldy * elt) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
     p.dbg_epi = env_int("I8MM_DBG_EPI");
     p.dbg = debug_timeline();
+    p.n_peer = 0;
+    if (epi == EPI_F16 && a.n_peer > 0) {
+        if (a.n_peer > kMaxPeers) return cudaErrorInvalidValue;
+        p.n_peer = a.n_peer;
+        for (int q = 0; q < a.n_peer; ++q) p.y_peer[q] = a.y_peer[q];
+        p.peer_ldy = a.peer_ldy;
+        p.peer_col = a.peer_col;
+        bool vec = (a.peer_ldy % 8 == 0) && (a.peer_col % 8 == 0);
+        for (int q = 0; q < a.n_peer; ++q) vec = vec && (reinterpret_cast<uintptr_t>(a.y_peer[q]) & 15u) == 0;
+        p.peer_vec = vec ? 1 : 0;
+    }
     // split-K when one m-tile's N-tiles would leave most SMs idle (M <= 128)
     p.ksplit = 1;
     if (cg == 1 && a.c32 != nullptr && p.m_tiles == 1) {

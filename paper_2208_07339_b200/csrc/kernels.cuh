@@ -165,7 +165,13 @@ struct GemmArgs {
     int64_t c32_rows;
     int32_t* c32_cnt;
     int64_t c32_tiles;
+    // fused output all-gather (fp16 out only): also store every output to
+    // n_peer buffers y_peer[q] + row * peer_ldy + peer_col + column
+    void* y_peer[8];
+    int n_peer;
+    int64_t peer_ldy, peer_col;
 };
+constexpr int kMaxPeers = 8;
 
 // split-K scratch of the single-m-tile GEMM: c32 [cols x M] + counters
 int64_t gemm_split_cols(int64_t N, bool patches);

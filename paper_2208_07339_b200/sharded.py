@@ -12,9 +12,18 @@ The all-gather is pipelined behind the GEMM: after one
 prologue over all rows, the GEMM runs per row range and each range's block is
 gathered on a communication stream while the next range computes, so the
 NVLink transfer overlaps the tensor-core work except for the last range.
+
+The default (``fused_gather=None``) removes the collective altogether when the
+process group supports symmetric memory: Y lives in symmetric memory and the
+GEMM epilogue stores each output tile into every rank's Y over NVLink
+(``forward_fused``); otherwise the NCCL pipeline runs. Validated on one GPU
+(world size 1 through symmetric memory, and peers emulated by extra buffers in
+``i8mm_linear_forward_peers``); no multi-GPU box was available to this round.
 """
 
 from __future__ import annotations
+
+import ctypes
 
 import torch
 import torch.distributed as dist
@@ -129,8 +138,12 @@ class ShardedInt8Linear(torch.nn.Module):
 
     def __init__(self, weight, n_total: int | None = None, alpha: float = 6.0,
                  group=None, local: bool = False, out_dtype: torch.dtype = torch.float16,
-                 weight_stationary: bool = True):
+                 weight_stationary: bool = True, fused_gather: bool | None = None):
         super().__init__()
+        # forward() -> forward_fused (symmetric memory) when True; None = use it
+        # when the process group supports symmetric memory, else the NCCL pipeline
+        self.fused_gather = fused_gather
+        self.gather_path = None  # "fused-epilogue" | "nccl-pipelined", set by forward()
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -140,6 +153,7 @@ class ShardedInt8Linear(torch.nn.Module):
         if not local:
             w = w[:, self.lo:self.hi].contiguous()
         self.local = Int8Linear(w, alpha, out_dtype=out_dtype, weight_stationary=weight_stationary)
+        self._symm = {}  # forward_fused: (M, device) -> symmetric Y buffer and peer handles
 
     def forward_local(self, x: torch.Tensor, _timer=None) -> torch.Tensor:
         """This rank's column block Y[:, lo:hi] (no communication)."""
@@ -150,12 +164,70 @@ class ShardedInt8Linear(torch.nn.Module):
         all-gather behind the GEMM (default 4 when world > 1, else 1)."""
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
+        if self.fused_gather is not False and _timer is None and chunks is None:
+            if (self.local.out_dtype == torch.float16 and self.local.weight_stationary
+                    and x2.is_cuda and dist.get_backend(self.group) == "nccl"):
+                try:
+                    y = self.forward_fused(x2)
+                    self.gather_path = "fused-epilogue"
+                    return y.reshape(*lead, self.n_total)
+                except (RuntimeError, NotImplementedError, AttributeError):
+                    if self.fused_gather:
+                        raise
+                    self.fused_gather = False  # no symmetric memory here: NCCL from now on
+            elif self.fused_gather:
+                raise ValueError("fused_gather needs CUDA tensors, NCCL, fp16 output and a "
+                                 "weight-stationary layer")
+        self.gather_path = "nccl-pipelined"
         if chunks is None:
             chunks = 4 if self.world > 1 else 1
         if chunks <= 1 or _timer is not None:
             y = self.forward_local(x2, _timer)
             return gather_columns(y, self.n_total, self.group).reshape(*lead, self.n_total)
         return self.forward_pipelined(x2, chunks).reshape(*lead, self.n_total)
+
+    def forward_fused(self, x2: torch.Tensor) -> torch.Tensor:
+        """Y = x @ W with the all-gather fused into the GEMM epilogue.
+
+        Y lives in symmetric memory (``torch.distributed._symmetric_memory``):
+        every rank's epilogue stores its column block into its own Y and, over
+        NVLink, into every peer's Y (``i8mm_linear_forward_peers``); one
+        device-side barrier then orders the peers' stores before the reads. No
+        NCCL collective runs. The returned tensor is a persistent buffer per
+        row count, overwritten by the next call with the same M.
+        """
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from . import _native as nat
+        from ._tensors import stream_handle
+
+        if self.local.out_dtype != torch.float16 or not self.local.weight_stationary:
+            raise ValueError("forward_fused needs fp16 output and a weight-stationary layer")
+        x16 = as_f16_matrix(x2, "x")
+        m, k = x16.shape
+        key = (m, x16.device.index)
+        if key not in self._symm:
+            out = symm_mem.empty((m, self.n_total), dtype=torch.float16, device=x16.device)
+            group = self.group if self.group is not None else dist.group.WORLD
+            hdl = symm_mem.rendezvous(out, group.group_name)
+            peers = [hdl.get_buffer(r, out.shape, out.dtype) for r in range(self.world) if r != self.rank]
+            ptrs = (ctypes.c_void_p * max(1, len(peers)))(*[t.data_ptr() for t in peers])
+            self._symm[key] = (out, hdl, peers, ptrs)
+        out, hdl, peers, ptrs = self._symm[key]
+        # every rank is done with the previous contents of its Y (work enqueued
+        # before this call) before any peer overwrites them
+        hdl.barrier(channel=1)
+        L = nat.lib()
+        lin = self.local
+        n = self.hi - self.lo
+        ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8, device=x16.device)
+        y_loc = out[:, self.lo:self.hi]  # this rank's block, written in place (ldy = n_total)
+        nat.check(L.i8mm_linear_forward_peers(
+            x16.data_ptr(), x16.stride(0), m, lin.weight.data_ptr(), lin.weight.stride(0),
+            lin.wbuf.data_ptr(), k, n, lin.alpha, y_loc.data_ptr(), self.n_total, ws.data_ptr(),
+            ws.numel(), ptrs, len(peers), self.n_total, self.lo, stream_handle()), "linear_forward_peers")
+        hdl.barrier()
+        return out
 
     def forward_pipelined(self, x2: torch.Tensor, chunks: int) -> torch.Tensor:
         m = x2.shape[0]

@@ -758,3 +758,68 @@ def test_alternating_decode_prefill_calls_stable(p, oracle_mod):
         for m in (16, 32, 8, 64):
             y = lin.matmul(x16[:m].contiguous(), exact=True)
             assert torch.equal(y.cpu(), refs[m]), m
+
+
+@pytest.mark.parametrize("case", [(300, 1024, 700, 0), (8, 512, 256, 0), (100, 8704, 700, 6), (600, 1024, 2000, 6)],
+                         ids=["prefill", "decode", "splitk_patches", "pairs_patches"])
+def test_forward_peers_fused_gather(p, case):
+    """i8mm_linear_forward_peers: the GEMM epilogue stores every output also
+    into peer buffers at a column offset (the fused all-gather); with local
+    stand-ins for the peers every destination must hold exactly this rank's
+    block, and the local output must equal the plain forward."""
+    import ctypes
+
+    from paper_2208_07339_b200 import _native as nat
+    from paper_2208_07339_b200._tensors import stream_handle
+
+    m, k, n, heavy = case
+    x, w = _ws_case(21, m, k, n, 6, heavy)
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    y_ref = lin(x16)
+    L = nat.lib()
+    n_total, col = n + 40, 24  # the block sits at columns [24, 24 + n) of a wider Y
+    peers = [torch.full((m, n_total), -7.0, dtype=torch.float16, device="cuda") for _ in range(2)]
+    ptrs = (ctypes.c_void_p * 2)(*[t.data_ptr() for t in peers])
+    y = torch.empty((m, n), dtype=torch.float16, device="cuda")
+    ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8, device="cuda")
+    nat.check(L.i8mm_linear_forward_peers(
+        x16.data_ptr(), k, m, lin.weight.data_ptr(), n, lin.wbuf.data_ptr(), k, n, 6.0, y.data_ptr(), n,
+        ws.data_ptr(), ws.numel(), ptrs, 2, n_total, col, stream_handle()), "forward_peers")
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+    for t in peers:
+        assert torch.equal(t[:, col:col + n], y_ref)
+        assert bool((t[:, :col] == -7.0).all()) and bool((t[:, col + n:] == -7.0).all())
+
+
+def test_sharded_fused_gather_single_rank(p, oracle_mod):
+    """ShardedInt8Linear.forward_fused (symmetric-memory Y, all-gather fused
+    into the epilogue, device barrier) at world size 1 equals the module."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2208_07339_b200.sharded import ShardedInt8Linear
+
+    x, w = oracle_mod.planted_pair(700, 768, 520, 6, 20.0, 4)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+    y_ref = lin(x16)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sh = ShardedInt8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+        try:
+            y = sh.forward_fused(x16)
+        except (RuntimeError, NotImplementedError) as e:  # symmetric memory unavailable on this box
+            pytest.skip(f"symmetric memory: {str(e).splitlines()[0]}")
+        assert torch.equal(y, y_ref)
+        assert torch.equal(sh.forward_fused(x16), y_ref)  # cached buffer, second call
+    finally:
+        dist.destroy_process_group()
