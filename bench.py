@@ -321,8 +321,9 @@ def run_ours(args, layers, wl) -> None:
     hostio = None if dist_on else pkg.HostIOPipeline(dev, chunks=4)
 
     def step_e2e():
-        if hostio is not None:  # copies overlapped with compute (and with each other)
-            hostio.run(list(zip(mods, xs_host, ys_host)), inputs_ready=True)
+        if hostio is not None:  # copies overlapped with compute (and with each other);
+            # output copies stay in flight across steps, joined before the end event
+            hostio.run(list(zip(mods, xs_host, ys_host)), inputs_ready=True, join=False)
             return
         for mod, xh, yh in zip(mods, xs_host, ys_host):
             x = xh.to(dev, non_blocking=True)
@@ -338,6 +339,8 @@ def run_ours(args, layers, wl) -> None:
         s.record()
         for _ in range(steps):
             fn()
+        if hostio is not None:
+            hostio.join()  # every output copy of the timed steps is inside the region
         e.record()
         torch.cuda.synchronize()
         if dist_on:

@@ -40,13 +40,15 @@ class HostIOPipeline:
         self.d2h = torch.cuda.Stream(device=self.device)
 
     def run(self, calls: list[tuple[Int8Linear, torch.Tensor, torch.Tensor]],
-            inputs_ready: bool = False) -> None:
+            inputs_ready: bool = False, join: bool = True) -> None:
         """Enqueue the calls. By default the input copies wait for the caller's
         current stream (it may still be producing the host inputs, e.g. a D2H
         into ``x_host``). ``inputs_ready=True`` asserts the host inputs are
         already final, so this batch's input copies start at once and overlap
         the previous batch's compute and output copies (a serving loop over
-        independent batches)."""
+        independent batches). ``join=False`` leaves the output copies running
+        (the next batch's compute does not wait for them); call ``join()``
+        before reading any ``y_host``."""
         compute = torch.cuda.current_stream(self.device)
         if not inputs_ready:
             self.h2d.wait_stream(compute)
@@ -70,7 +72,12 @@ class HostIOPipeline:
                 y.record_stream(self.d2h)
 
             mod.matmul_rows(xd, row_ranges(xd.shape[0], self.chunks), on_rows)
-        compute.wait_stream(self.d2h)
+        if join:
+            compute.wait_stream(self.d2h)
+
+    def join(self) -> None:
+        """Make the caller's current stream wait for every output copy enqueued so far."""
+        torch.cuda.current_stream(self.device).wait_stream(self.d2h)
 
 
 def run_host_io(calls, chunks: int = 4) -> None:

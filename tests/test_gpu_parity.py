@@ -687,8 +687,9 @@ def test_host_io_pipeline_back_to_back_batches(p, oracle_mod):
         batches.append((xs, ys, refs))
     torch.cuda.synchronize()
     pipe = p.HostIOPipeline(chunks=2)
-    for xs, ys, _ in batches:
-        pipe.run(list(zip(mods, xs, ys)), inputs_ready=True)
+    for xs, ys, _ in batches:  # output copies left in flight across batches, joined once
+        pipe.run(list(zip(mods, xs, ys)), inputs_ready=True, join=False)
+    pipe.join()
     torch.cuda.synchronize()
     for _, ys, refs in batches:
         for y, r in zip(ys, refs):
