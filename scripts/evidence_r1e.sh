@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-1 (late) evidence capture on one B200 (dev tool; run under gpurun).
-O=gpurun_out/ev2
+O=gpurun_out/ev3
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/gpu.csv
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1
@@ -19,3 +19,4 @@ I8MM_DECODE_MAX_M=0 timeout 600 python scripts/decode_sweep.py > $O/decode_prefi
 timeout 120 python scripts/prologue_bench.py > $O/prologue.log 2>&1
 I8MM_PROLOGUE_1READ=1 timeout 120 python scripts/prologue_bench.py >> $O/prologue.log 2>&1
 ls -la $O
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 1 --steps 30 --warmup 3 --e2e-steps 2 --no-cpu-baseline > $O/bench_torchrun1.json 2> $O/bench_torchrun1.err
