@@ -698,6 +698,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_wait(&bars->full[stage], phase);
                 tc_fence_after();
                 if (lane == 0 && u == u_begin) DSTAMP(p.dbg, 5);
+                if (lane == 0 && u == u_end - 1) DSTAMP(p.dbg, 14);  // last unit's operands landed
                 if (lane == 0) {
                     const uint32_t a0 = smem_addr(ring + static_cast<size_t>(stage) * stage_bytes);
                     const uint32_t b0 = a0 + A_BYTES;

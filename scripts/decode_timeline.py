@@ -44,7 +44,7 @@ def col(i):
 
 
 labels = {0: "start", 1: "P1 done", 3: "P2 done", 4: "sync2 out",
-          10: "1st dots", 9: "patched", 5: "first MMA", 6: "MMA done", 7: "epi done", 8: "end"}
+          10: "1st dots", 9: "patched", 5: "first MMA", 14: "last operands", 6: "MMA done", 7: "epi done", 8: "end"}
 for i, lab in labels.items():
     v = G[:, i]
     arg = int(torch.argmax(v)) if (v > 0).any() else -1
