@@ -824,3 +824,23 @@ def test_sharded_fused_gather_single_rank(p, oracle_mod):
         assert torch.equal(sh.forward_fused(x16), y_ref)  # cached buffer, second call
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("pad", [24, 3], ids=["aligned_stride", "odd_stride"])
+@pytest.mark.parametrize("m", [8, 300])
+def test_row_strided_x_matches_contiguous(p, oracle_mod, pad, m):
+    """X as a column slice of a wider buffer (row pitch ldx > K): the 16-byte
+    aligned pitch takes the vector prologue, the odd pitch the generic one;
+    both equal the contiguous call and the oracle, for decode and prefill M."""
+    k, n = 1024, 520
+    x, w = _ws_case(31, m, k, n, 6, 2)
+    wide = torch.zeros((m, k + pad), dtype=torch.float16, device="cuda")
+    wide[:, :k] = torch.from_numpy(x.astype(np.float16)).cuda()
+    xs = wide[:, :k]
+    assert xs.stride(0) == k + pad
+    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    assert np.array_equal(_np(lin.matmul(xs, exact=True)), ref.output)
+    assert torch.equal(lin(xs), lin(xs.contiguous()))
+    r = p.llm_int8_matmul(xs, lin.weight, 6.0, exact=True)
+    assert np.array_equal(_np(r.output), ref.output)
