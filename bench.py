@@ -365,9 +365,14 @@ def run_ours(args, layers, wl) -> None:
         step_gemm_marked()
     torch.cuda.synchronize()
     timer.enabled = False
-    gemm_ms = timer.total_ms() / g_steps  # per step, this rank
+    gemm_ms_marked = timer.total_ms() / g_steps  # per step, this rank (separate pass)
     ms_step = ms / args.steps
     value = ops / (ms_step * 1e-3) / 1e12
+    # the marked pass runs after the timed one (a warmer, sometimes power-capped
+    # GPU, and no launch overlap across its events): its GEMM time can exceed the
+    # whole timed step on single-GEMM workloads; the GEMM cannot take longer than
+    # the step it is part of, so the roofline uses the smaller of the two
+    gemm_ms = min(gemm_ms_marked, ms_step)
 
     for _ in range(max(1, args.warmup // 2)):
         step_e2e()
@@ -414,6 +419,7 @@ def run_ours(args, layers, wl) -> None:
             "frac_measured_equiv": (achieved / (2.0 * bf16)) if bf16 else None,
             "peak_measured_equiv_source": "2 x MEASURED_PEAKS.bf16_tflops (INT8 dense rate = 2x BF16 on B200)",
             "gemm_ms_per_step": gemm_ms,
+            "gemm_ms_marked_pass": gemm_ms_marked,
             "gemm_share_of_step": gemm_ms / ms_step,
         }
 
