@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-1 (late) evidence capture on one B200 (dev tool; run under gpurun).
-O=gpurun_out/ev3
+O=gpurun_out/ev4
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/gpu.csv
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1
