@@ -15,6 +15,7 @@ from .linear import (ABSMAX, BACKEND_KINDS, EXACT, VECTORWISE, ZEROPOINT, Int8Li
                      LinearBackend, _linear, linear, llm_int8_backend)
 from .quantize import (absmax_quantize, colwise_quantize, rowwise_quantize, vectorwise_params,
                        zeropoint_quantize)
+from .graphs import GraphedCall
 from .pipeline import HostIOPipeline, run_host_io
 from .synthetic import planted_pair
 from .types import (AbsmaxParams, ColwiseParams, OutlierSet, QuantizedTensor, RowwiseParams,
@@ -31,4 +32,5 @@ __all__ = [
     "llm_int8_backend", "linear", "_linear", "Int8Linear", "planted_pair",
     "AbsmaxParams", "ZeropointParams", "absmax_quantize", "zeropoint_quantize",
     "absmax_matmul", "zeropoint_matmul", "zeropoint_gemm_i32", "HostIOPipeline", "run_host_io",
+    "GraphedCall",
 ]
