@@ -255,6 +255,7 @@ struct Workspace {
     int64_t c32_words;
     int32_t* tile_cnt;
     int64_t n_tiles;
+    int32_t* pq_ready;   // decode: ready flags of post-barrier patch rows
     uint32_t* thr_word;  // alpha threshold bits, written by the prologue entry
     void* rp_scratch;    // prefill: per-row group maxima + f64 row scales (launch_row_prologue)
     int32_t* sk_c32;     // prefill M <= 128 (linear): split-K partial sums, then tile counters
@@ -324,6 +325,7 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
             w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (w.n_tiles + 2)));
             w.thr_word = reinterpret_cast<uint32_t*>(w.tile_cnt + w.n_tiles + 1);
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(128 * w.ldq)));  // patch tile rows
+            w.pq_ready = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 128));
         } else {
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
         }
@@ -509,6 +511,8 @@ static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __h
     d.patch_pos = ws.patch_pos;
     d.q2 = b.q2;
     d.pq = ws.wq_p;
+    d.p_src = ws.p_src;
+    d.pq_ready = ws.pq_ready;
     d.c32 = ws.c32;
     d.c32_words = ws.c32_words;
     d.tile_cnt = ws.tile_cnt;

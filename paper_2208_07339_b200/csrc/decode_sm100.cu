@@ -70,6 +70,9 @@ constexpr uint32_t TMEM_COLS = 512;  // two accumulators at column 0 and 256
 constexpr int MAX_M = 256;
 constexpr int LOCAL_CAP = 512;  // fixup columns per CTA (N <= LOCAL_CAP * grid)
 constexpr int PATCH_ROWS = 128; // patched columns handled by the extra tile of the stream
+// the first PT_GATHER_ROWS rows of the patch tile are gathered from q2 (tile::gather4)
+// after the barrier; the rest (many patches) are copied to pq in P2 and box-loaded
+constexpr int PT_GATHER_ROWS = 8;
 
 __device__ __forceinline__ bool bit_of(const uint32_t* m, int64_t k) {
     return (m[k >> 5] >> (k & 31)) & 1u;
@@ -90,6 +93,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if ((ptr) != nullptr) (ptr)[blockIdx.x * 16 + (i)] = gtimer(); \
     } while (0)
 
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -203,6 +209,7 @@ struct __align__(8) Bars {
     float local_a[LOCAL_CAP];       //   amax over keep rows,
     int32_t local_src[LOCAL_CAP];   //   1 = its codes are the cached q2 row
     int32_t red[16 * NWARPS];       // per-warp partial dot products (patched columns)
+    int32_t pt_rows[PATCH_ROWS];    // producer: q2 row (patched column) of each patch-tile row
     int32_t warp_sums[NWARPS];
 };
 
@@ -295,7 +302,9 @@ template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
                         const __grid_constant__ CUtensorMap tmap_x,
-                        const __grid_constant__ CUtensorMap tmap_p, const Params p) {
+                        const __grid_constant__ CUtensorMap tmap_p,
+                        const __grid_constant__ CUtensorMap tmap_q2,
+                        const __grid_constant__ CUtensorMap tmap_pb, const Params p) {
     cg::grid_group grid = cg::this_grid();
     const DecodeArgs& a = p.a;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -328,6 +337,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_prefetch_desc(&tmap_w);
         tma_prefetch_desc(&tmap_x);
         tma_prefetch_desc(&tmap_p);
+        tma_prefetch_desc(&tmap_q2);
+        tma_prefetch_desc(&tmap_pb);
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
@@ -393,6 +404,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i < N; i += G * PT)
             a.patch_pos[i] = 0;
         if (blockIdx.x == 0 && pt == 0) *a.p_count = 0;
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i < PATCH_ROWS; i += G * PT)
+            a.pq_ready[i] = 0;
     }
     __syncthreads();
     // one warp per owned word: lane = column, OR over rows
@@ -523,6 +536,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             a.p_idx[pidx] = static_cast<int32_t>(j);
             a.p_amax[pidx] = a_new;
             a.patch_pos[j] = pidx + 1;
+            a.p_src[pidx] = src;
+            // the patch tile gathers this row from q2 after the barrier: pull it into
+            // L2 now (asynchronous; nothing here waits for it)
+            if (src && pidx < PT_GATHER_ROWS)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.q2 + j * a.ldq),
+                             "r"(static_cast<uint32_t>(a.ldq & ~int64_t(15)))
+                             : "memory");
             const int li = atomicAdd(&bars->n_local, 1);
             bars->local_j[li] = static_cast<int32_t>(j);
             bars->local_p[li] = pidx;
@@ -531,24 +551,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     __syncthreads();
-    // patch-tile rows: the re-derived codes of this CTA's patched columns (the
-    // cached q2 row; W's strided column in the rare deeper case), read by TMA
-    // as the A operand of the extra tile
+    // patch-tile rows: a patched column whose codes are its cached q2 row (the
+    // common case) is gathered straight from q2 by the patch tile's producer
+    // (TMA tile::gather4, no copy here); only re-derived codes (its top-2 rows
+    // are both outlier rows: rare) are written to pq now
     for (int li = 0; li < bars->n_local; ++li) {
         const int pidx = bars->local_p[li];
-        if (pidx >= PATCH_ROWS) continue;  // overflow: CUDA-core path after the barrier
+        if (pidx >= PATCH_ROWS || (bars->local_src[li] && pidx < PT_GATHER_ROWS)) continue;
         const int64_t j = bars->local_j[li];
         int8_t* dst = a.pq + static_cast<int64_t>(pidx) * a.ldq;
-        if (bars->local_src[li]) {
+        if (bars->local_src[li]) {  // rows >= PT_GATHER_ROWS: one box load of pq after the barrier
             const uint4* srcq = reinterpret_cast<const uint4*>(a.q2 + j * a.ldq);
             for (int64_t v = threadIdx.x; v < a.ldq / 16; v += THREADS)
                 reinterpret_cast<uint4*>(dst)[v] = __ldcs(srcq + v);
         } else {
-            const double s = scale_of(bars->local_a[li]);
-            const float s32 = static_cast<float>(s);
+            const double sc = scale_of(bars->local_a[li]);
+            const float s32 = static_cast<float>(sc);
             for (int64_t k = threadIdx.x; k < a.ldq; k += THREADS)
                 dst[k] = (k < K && !bit_of(a.mask, k))
-                             ? static_cast<int8_t>(code_fast(__half2float(a.w[k * a.ldw + j]), s32, s)) : int8_t(0);
+                             ? static_cast<int8_t>(code_fast(__half2float(a.w[k * a.ldw + j]), s32, sc)) : int8_t(0);
         }
     }
     // Xq and the patch rows are read back by TMA (async proxy) after the barrier
@@ -664,16 +685,58 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             int stage = n_pre % p.stages;
             uint32_t phase = n_pre == p.stages ? 1u : 0u;
+            int pt_groups = -1;  // patch tile: gathered 4-row groups (set at its first unit)
+            bool pt_rest = false;  // rows >= PT_GATHER_ROWS present (box load from pq)
+            uint32_t pt_pq = 0;  // bit g: group g is gathered from pq
             for (int64_t u = u_begin + n_pre; u < u_end; ++u) {
                 const int tile = static_cast<int>(u / num_kb);
                 const int kb = static_cast<int>(u % num_kb);
                 mbar_wait(&bars->empty[stage], phase ^ 1u);
-                mbar_arrive_expect_tx(&bars->full[stage], stage_bytes);
                 uint8_t* dst = ring + static_cast<size_t>(stage) * stage_bytes;
-                if (tile < p.n_tiles)
+                if (tile < p.n_tiles) {
+                    mbar_arrive_expect_tx(&bars->full[stage], stage_bytes);
                     tma_load_2d(&tmap_w, &bars->full[stage], dst, kb * BK, tile * TILE_N, pol_w);
-                else  // the patch tile: q2 rows of the patched columns
-                    tma_load_2d(&tmap_p, &bars->full[stage], dst, kb * BK, 0, pol_x);
+                } else {
+                    // the patch tile: row r = patched column p_idx[r]; groups of 4 rows
+                    // are gathered (tile::gather4) from the cached q2 rows, or from pq
+                    // when a group holds a re-derived row (its q2-sourced rows are then
+                    // copied to pq after the barrier, each published with a ready flag)
+                    if (pt_groups < 0) {
+                        const int np = min(__ldcg(a.p_count), PATCH_ROWS);
+                        pt_rest = np > PT_GATHER_ROWS;
+                        pt_groups = (min(np, PT_GATHER_ROWS) + 3) / 4;
+                        bool waited = false;
+                        for (int g = 0; g < pt_groups; ++g) {
+                            int n0 = 0;
+                            for (int r = 4 * g; r < min(4 * g + 4, np); ++r) {
+                                bars->pt_rows[r] = __ldcg(a.p_idx + r);
+                                n0 += __ldcg(a.p_src + r) == 0 ? 1 : 0;
+                            }
+                            for (int r = np; r < 4 * g + 4; ++r) bars->pt_rows[r] = bars->pt_rows[4 * g];
+                            if (n0 > 0) {
+                                pt_pq |= 1u << g;
+                                for (int r = 4 * g; r < min(4 * g + 4, np); ++r)
+                                    if (__ldcg(a.p_src + r) != 0)
+                                        while (ld_acquire(a.pq_ready + r) == 0) {
+                                        }
+                                waited = true;
+                            }
+                        }
+                        if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    mbar_arrive_expect_tx(&bars->full[stage], static_cast<uint32_t>(pt_groups) * 4u * BK + p.b_bytes +
+                                                                  (pt_rest ? static_cast<uint32_t>(PATCH_ROWS - PT_GATHER_ROWS) * BK : 0u));
+                    if (pt_rest)  // rows PT_GATHER_ROWS.. : copied to pq in P2 (many patches)
+                        tma_load_2d(&tmap_pb, &bars->full[stage], dst + PT_GATHER_ROWS * BK, kb * BK, 0, pol_x);
+                    for (int g = 0; g < pt_groups; ++g) {
+                        uint8_t* gd = dst + g * 4 * BK;
+                        if ((pt_pq >> g) & 1u)
+                            tma_gather4(&tmap_p, &bars->full[stage], gd, kb * BK, 4 * g, 4 * g + 1, 4 * g + 2, 4 * g + 3);
+                        else
+                            tma_gather4(&tmap_q2, &bars->full[stage], gd, kb * BK, bars->pt_rows[4 * g],
+                                        bars->pt_rows[4 * g + 1], bars->pt_rows[4 * g + 2], bars->pt_rows[4 * g + 3]);
+                    }
+                }
                 tma_load_2d(&tmap_x, &bars->full[stage], dst + A_BYTES, kb * BK, 0, pol_x);
                 if (++stage == p.stages) {
                     stage = 0;
@@ -722,7 +785,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (lane == 0) DSTAMP(p.dbg, 6);
     } else {
-        if (warp >= 4) {
+        if (warp == 2 || warp == 3) {
+            // ---------------- rare: a q2-sourced patch row whose 4-row group also holds
+            // a re-derived row must be in pq too (the group is gathered from pq)
+            const int t64 = threadIdx.x - 64;
+            const int np = min(__ldcg(a.p_count), PATCH_ROWS);
+            for (int li = 0; li < bars->n_local; ++li) {
+                const int pidx = bars->local_p[li];
+                if (pidx >= PT_GATHER_ROWS || !bars->local_src[li]) continue;
+                bool mixed = false;
+                for (int r = pidx & ~3; r < min((pidx & ~3) + 4, np); ++r) mixed |= __ldcg(a.p_src + r) == 0;
+                if (!mixed) continue;
+                const int64_t j = bars->local_j[li];
+                const uint4* srcq = reinterpret_cast<const uint4*>(a.q2 + j * a.ldq);
+                uint4* dst = reinterpret_cast<uint4*>(a.pq + static_cast<int64_t>(pidx) * a.ldq);
+                for (int64_t v = t64; v < a.ldq / 16; v += 64) dst[v] = __ldcs(srcq + v);
+                __threadfence();
+                named_bar_sync(3, 64);
+                if (t64 == 0) st_release(a.pq_ready + pidx, 1);
+            }
+        } else if (warp >= 4) {
             // ---------------- epilogue: thread = weight row n of the tile
             const int np_all = __ldcg(a.p_count);  // final after barrier 2
             const int quad = warp & 3;
@@ -895,6 +977,7 @@ unsigned long long* debug_timeline() { return g_dbg; }
 
 template <int EPI>
 static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tp,
+                                const CUtensorMap& tq, const CUtensorMap& tb,
                                 const dec::Params& prm, size_t smem, int grid, cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -915,7 +998,7 @@ static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, co
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, dec::decode_fused_kernel<EPI>, tw, tx, tp, prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dec::decode_fused_kernel<EPI>, tw, tx, tp, tq, tb, prm);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -939,14 +1022,21 @@ cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st) {
     CUtensorMap tw, tx, tp;
     if (!make_tmap_i8_rows(&tw, a.wq_t, a.N, a.K, a.ldq, TILE_N)) return cudaErrorInvalidValue;
     if (!make_tmap_i8_rows(&tx, a.xq, a.M, a.K, a.ldq, prm.mpad)) return cudaErrorInvalidValue;
-    if (!make_tmap_i8_rows(&tp, a.pq, PATCH_ROWS, a.K, a.ldq, TILE_N)) return cudaErrorInvalidValue;
+    // patch tile A rows: 1-row boxes for tile::gather4 from pq and from q2
+    CUtensorMap tq;
+    if (!make_tmap_i8_rows(&tp, a.pq, PATCH_ROWS, a.K, a.ldq, 1)) return cudaErrorInvalidValue;
+    if (!make_tmap_i8_rows(&tq, a.q2, a.N, a.K, a.ldq, 1)) return cudaErrorInvalidValue;
+    CUtensorMap tb;  // pq rows PT_GATHER_ROWS..PATCH_ROWS-1 as one box
+    if (!make_tmap_i8_rows(&tb, a.pq + PT_GATHER_ROWS * a.ldq, PATCH_ROWS - PT_GATHER_ROWS, a.K, a.ldq,
+                           PATCH_ROWS - PT_GATHER_ROWS))
+        return cudaErrorInvalidValue;
     const size_t smem =
         1024 + static_cast<size_t>(prm.stages) * (A_BYTES + prm.b_bytes) + smem_extra();
     const int grid = decode_grid(a.K, a.N);
     switch (epi) {
-        case EPI_F16: return launch_fused<EPI_F16>(tw, tx, tp, prm, smem, grid, st);
-        case EPI_F32: return launch_fused<EPI_F32>(tw, tx, tp, prm, smem, grid, st);
-        case EPI_F32_EXACT: return launch_fused<EPI_F32_EXACT>(tw, tx, tp, prm, smem, grid, st);
+        case EPI_F16: return launch_fused<EPI_F16>(tw, tx, tp, tq, tb, prm, smem, grid, st);
+        case EPI_F32: return launch_fused<EPI_F32>(tw, tx, tp, tq, tb, prm, smem, grid, st);
+        case EPI_F32_EXACT: return launch_fused<EPI_F32_EXACT>(tw, tx, tp, tq, tb, prm, smem, grid, st);
         default: return cudaErrorInvalidValue;
     }
 }

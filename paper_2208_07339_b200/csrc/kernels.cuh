@@ -219,6 +219,8 @@ struct DecodeArgs {
     int32_t* c32;         // [2 x grid] x [M x 128] split-tile partial slots
     int64_t c32_words;
     int32_t* tile_cnt;    // [n_tiles + 1] (+ the patch tile)
+    int32_t* p_src;       // [N] per patch: 1 = its codes are the cached q2 row
+    int32_t* pq_ready;    // [128] pq row r holds a q2 row copied after barrier 2 (rare)
     int64_t n_tiles;
     void* y;
     int64_t ldy;
