@@ -702,23 +702,39 @@ __global__ void __launch_bounds__(THREADS, 1)
                     // when a group holds a re-derived row (its q2-sourced rows are then
                     // copied to pq after the barrier, each published with a ready flag)
                     if (pt_groups < 0) {
-                        const int np = min(__ldcg(a.p_count), PATCH_ROWS);
+                        // one round trip: the count and the first rows' column / source
+                        // (entries past the count are ignored)
+                        int32_t pr[PT_GATHER_ROWS], ps[PT_GATHER_ROWS];
+                        const int np_raw = __ldcg(a.p_count);
+#pragma unroll
+                        for (int r = 0; r < PT_GATHER_ROWS; ++r) {
+                            pr[r] = __ldcg(a.p_idx + r);
+                            ps[r] = __ldcg(a.p_src + r);
+                        }
+                        const int np = min(np_raw, PATCH_ROWS);
                         pt_rest = np > PT_GATHER_ROWS;
                         pt_groups = (min(np, PT_GATHER_ROWS) + 3) / 4;
                         bool waited = false;
                         for (int g = 0; g < pt_groups; ++g) {
                             int n0 = 0;
-                            for (int r = 4 * g; r < min(4 * g + 4, np); ++r) {
-                                bars->pt_rows[r] = __ldcg(a.p_idx + r);
-                                n0 += __ldcg(a.p_src + r) == 0 ? 1 : 0;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int r = 4 * g + i;
+                                if (r < np) {
+                                    bars->pt_rows[r] = pr[r];
+                                    n0 += ps[r] == 0 ? 1 : 0;
+                                }
                             }
                             for (int r = np; r < 4 * g + 4; ++r) bars->pt_rows[r] = bars->pt_rows[4 * g];
                             if (n0 > 0) {
                                 pt_pq |= 1u << g;
-                                for (int r = 4 * g; r < min(4 * g + 4, np); ++r)
-                                    if (__ldcg(a.p_src + r) != 0)
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const int r = 4 * g + i;
+                                    if (r < np && ps[r] != 0)
                                         while (ld_acquire(a.pq_ready + r) == 0) {
                                         }
+                                }
                                 waited = true;
                             }
                         }
