@@ -1,8 +1,12 @@
 """GEMM-only timing of the prefill kernel (dev tool) for env A/B knobs
 (I8MM_DBG_EPI, I8MM_GEMM_MC, ...). Prints us and TOPS per shape."""
+import os
 import sys
 import torch
 sys.path.insert(0, ".")
+if os.environ.get("I8MM_LIB_ALT"):  # A/B against another build of the library
+    from paper_2208_07339_b200 import _native
+    _native.load_library(os.environ["I8MM_LIB_ALT"])
 from paper_2208_07339_b200 import gemm as G
 from paper_2208_07339_b200.synthetic import planted_pair_device
 
