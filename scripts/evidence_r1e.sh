@@ -1,7 +1,8 @@
 #!/bin/bash
 # Round-1 (late) evidence capture on one B200 (dev tool; run under gpurun).
-O=gpurun_out/ev4
+O=gpurun_out/ev5
 mkdir -p $O
+timeout 120 python scripts/pcie_bw.py > $O/pcie.json 2>&1
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/gpu.csv
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1
 timeout 600 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
