@@ -4,7 +4,7 @@ nvcc cross-compiles for ``-gencode arch=compute_100a,code=sm_100a`` (no GPU
 needed). The library exports the C ABI of ``include/llmint8.h`` and links
 cudart statically, so it only needs the NVIDIA driver at run time.
 
-    python -m paper_2208_07339_b200.build [--force] [--verbose]
+    python -m paper_2208_07339_b200.build [--force] [--verbose] [--devtools]
 """
 
 from __future__ import annotations
@@ -23,7 +23,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB_NAME = "libllmint8_sm100.so"
 SOURCES = ["capi.cu", "prologue.cu", "weights.cu", "gemm_sm100.cu", "decode_sm100.cu", "siblings.cu"]
-HEADERS = ["kernels.cuh", "sm100_ptx.cuh", "quant_common.cuh"]
+HEADERS = ["kernels.cuh", "sm100_ptx.cuh", "quant_common.cuh", "percall_dev.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -34,8 +34,9 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found (need CUDA 12.9 for sm_100a)")
 
 
-def lib_path() -> Path:
-    return OUT_DIR / LIB_NAME
+def lib_path(devtools: bool = False) -> Path:
+    """The production library, or the dev build (timeline stamps, wait counters)."""
+    return (OUT_DIR / "dev" if devtools else OUT_DIR) / LIB_NAME
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:
@@ -45,15 +46,18 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OUT_DIR.mkdir(exist_ok=True)
-    objdir = OUT_DIR / "obj"
+def build(force: bool = False, verbose: bool = False, devtools: bool = False) -> Path:
+    out = lib_path(devtools).parent
+    out.mkdir(parents=True, exist_ok=True)
+    objdir = out / "obj"
     objdir.mkdir(exist_ok=True)
     headers = [CSRC / h for h in HEADERS] + [ROOT / "include" / "llmint8.h"]
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                     "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    if devtools:  # scripts/*_timeline.py, I8MM_DBG_EPI: never the shipped library
+        flags += ["-DI8MM_GEMM_DEVTOOLS"]
     cc = nvcc()
 
     def compile_one(src: str) -> Path:
@@ -70,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    lib = lib_path()
+    lib = lib_path(devtools)
     if force or _stale(lib, objs):
         cmd = [cc, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -83,5 +87,6 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--devtools", action="store_true", help="dev build into _lib/dev/")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, devtools=a.devtools))

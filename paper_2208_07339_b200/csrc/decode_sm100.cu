@@ -88,9 +88,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 // timeline stamp i of this CTA (dev tool: i8mm_debug_decode_timeline)
-#define DSTAMP(ptr, i)                                                \
-    do {                                                              \
-        if ((ptr) != nullptr) (ptr)[blockIdx.x * 16 + (i)] = gtimer(); \
+// (dev build only: see gemm_sm100.cu, I8MM_GEMM_DEVTOOLS)
+#ifdef I8MM_GEMM_DEVTOOLS
+constexpr bool kDevStamps = true;
+#else
+constexpr bool kDevStamps = false;
+#endif
+#define DSTAMP(ptr, i)                                                               \
+    do {                                                                             \
+        if (kDevStamps && (ptr) != nullptr) (ptr)[blockIdx.x * 16 + (i)] = gtimer(); \
     } while (0)
 
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -584,7 +590,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // stream resumes (memory is quiet; nothing downstream waits on them): exact
     // int32 dots of the re-derived codes (q2 row, or W's column in the rare
     // multi-outlier case) with Xq, then the same epilogue math
-    if (threadIdx.x == 0 && p.dbg != nullptr) {
+    if (threadIdx.x == 0 && (kDevStamps && p.dbg != nullptr)) {
         p.dbg[blockIdx.x * 16 + 12] = static_cast<unsigned long long>(bars->n_local);
         p.dbg[blockIdx.x * 16 + 13] = static_cast<unsigned long long>(bars->n_local ? bars->local_src[0] : 9);
     }

@@ -131,8 +131,18 @@ struct Params {
     int peer_vec;
 };
 
+// Dev instrumentation (timeline stamps, wait-cycle counters, the I8MM_DBG_EPI
+// knob) is compiled only into the dev build (`build.py --devtools`, defines
+// I8MM_GEMM_DEVTOOLS): even never taken, its branches in the producer / MMA /
+// epilogue loops cost the production kernel 13-15 % (measured same-box A/B)
+#ifdef I8MM_GEMM_DEVTOOLS
+constexpr bool kDev = true;
+#else
+constexpr bool kDev = false;
+#endif
+
 __device__ __forceinline__ void gstamp(unsigned long long* dbg, int i) {
-    if (dbg != nullptr) {
+    if (kDev && dbg != nullptr) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         dbg[blockIdx.x * 16 + i] = t;
@@ -288,7 +298,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int q = 0; q < MC; ++q) b_mask |= static_cast<uint16_t>(1u << (q * CG + crank));
                 if (u == cluster_id) gstamp(p.dbg, 2);
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    if (p.dbg != nullptr) {
+                    if ((kDev && p.dbg != nullptr)) {
                         const long long c0 = clock64();
                         mbar_wait(&bars->empty[stage], phase ^ 1u);
                         w_empty += clock64() - c0;
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
             }
-            if (p.dbg != nullptr) p.dbg[blockIdx.x * 16 + 14] = static_cast<unsigned long long>(w_empty);
+            if ((kDev && p.dbg != nullptr)) p.dbg[blockIdx.x * 16 + 14] = static_cast<unsigned long long>(w_empty);
         }
     } else if (warp == 1 && leader) {
         // ===================== MMA issuer (leader CTA) =====================
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int kb0 = sl * p.num_kb / p.ksplit, kb1 = (sl + 1) * p.num_kb / p.ksplit;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            if (p.dbg != nullptr) {
+            if ((kDev && p.dbg != nullptr)) {
                 const long long c0 = clock64();
                 mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1u);
                 w_acc += clock64() - c0;
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
             for (int kb = kb0; kb < kb1; ++kb) {
-                if (p.dbg != nullptr) {
+                if ((kDev && p.dbg != nullptr)) {
                     const long long c0 = clock64();
                     mbar_wait(&bars->full[stage], phase);
                     w_full += clock64() - c0;
@@ -382,7 +392,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             __syncwarp();
         }
-        if (p.dbg != nullptr && lane == 0) {
+        if ((kDev && p.dbg != nullptr) && lane == 0) {
             p.dbg[blockIdx.x * 16 + 12] = static_cast<unsigned long long>(w_full);
             p.dbg[blockIdx.x * 16 + 13] = static_cast<unsigned long long>(w_acc);
         }
@@ -473,7 +483,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
 
             if (warp == EPI_WARP0 && lane == 0 && it == 0) gstamp(p.dbg, 8);
-            if (p.dbg != nullptr) {
+            if ((kDev && p.dbg != nullptr)) {
                 const long long c0 = clock64();
                 mbar_wait(&bars->tmem_full[acc], acc_phase);
                 w_tf += clock64() - c0;
@@ -548,7 +558,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             v2[2 * u] = __fmul2_rn(__fmul2_rn(c01, rf2), make_float2(f.x, f.y));
                             v2[2 * u + 1] = __fmul2_rn(__fmul2_rn(c23, rf2), make_float2(f.z, f.w));
                         }
-                        if (n_out > 0 && !(p.dbg_epi & 1)) {
+                        if (n_out > 0 && !(kDev && (p.dbg_epi & 1))) {
                             if (stage_wo) {
                                 const __half* wrow = smem_wo_h + ch * 32;
                                 if (n_cls == 4) outlier_fma_h<4>(v2, xo_r, wrow);
@@ -597,7 +607,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             }
                         }
                     }
-                    if (p.dbg_epi & 2) {
+                    if (kDev && (p.dbg_epi & 2)) {
                         if (v[0] == 1234.5f) reinterpret_cast<float*>(p.y)[0] = v[1];  // keep v live
                     } else if (tma_chunk) {
                         // stage this row's 32 outputs (64 B) in the warp's tile, then one
@@ -716,7 +726,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         if (TS && lane == 0) tma_store_wait<0>();  // staged outputs fully written
-        if (p.dbg != nullptr && warp == EPI_WARP0 && lane == 0)
+        if ((kDev && p.dbg != nullptr) && warp == EPI_WARP0 && lane == 0)
             p.dbg[blockIdx.x * 16 + 15] = static_cast<unsigned long long>(w_tf);
     }
 

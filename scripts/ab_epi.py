@@ -1,5 +1,6 @@
 """GEMM-only timing of the prefill kernel (dev tool) for env A/B knobs
-(I8MM_DBG_EPI, I8MM_GEMM_MC, ...). Prints us and TOPS per shape."""
+(I8MM_GEMM_MC, ...; I8MM_DBG_EPI only with I8MM_LIB_ALT pointing at the dev build,
+_lib/dev/). Prints us and TOPS per shape."""
 import os
 import sys
 import torch

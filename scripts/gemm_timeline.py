@@ -9,8 +9,10 @@ import torch
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
+from paper_2208_07339_b200 import _native as nat, build as _build  # noqa: E402
+# the stamps are compiled only into the dev build (python -m paper_2208_07339_b200.build --devtools)
+nat.load_library(_build.lib_path(devtools=True))
 import paper_2208_07339_b200 as pkg  # noqa: E402
-from paper_2208_07339_b200 import _native as nat  # noqa: E402
 from paper_2208_07339_b200.synthetic import planted_pair_device  # noqa: E402
 
 PROJ = {"qkvo": (5120, 5120), "fc1": (5120, 20480), "fc2": (20480, 5120),
