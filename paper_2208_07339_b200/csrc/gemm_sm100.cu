@@ -74,7 +74,7 @@ struct __align__(8) Barriers {
     uint32_t tmem_slot;
 };
 
-constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(__half);
+constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(float);
 constexpr size_t SMEM_COLS = static_cast<size_t>(BN) * sizeof(double);
 constexpr int STG_BYTES = 32 * 32 * 2;  // one 32 x 32 fp16 staging tile
 constexpr size_t SMEM_STG = static_cast<size_t>(EPI_WARPS) * 2 * STG_BYTES;  // double-buffered per warp
@@ -191,24 +191,23 @@ __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0
 
 // v[0..31] += sum_o xo[o] * wo[o][0..31] over NO staged (zero-padded) outlier
 // rows: straight-line packed f32x2 FMAs, no per-row guards. The rows are staged
-// as fp16 (exact: they are fp16 values) and widened in registers, which halves
-// the epilogue's shared-memory wavefronts.
+// widened to f32 once per tile: staging them as fp16 halves the shared-memory
+// wavefronts but costs two conversions per pair in every chunk (+58 M warp
+// instructions on fc1, +31 %, which a power-capped part pays in clock)
 template <int NO>
-__device__ __forceinline__ void outlier_fma_h(float2* v2, const float* xo_r, const __half* wrow) {
+__device__ __forceinline__ void outlier_fma(float2* v2, const float* xo_r, const float* wrow) {
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
         const float2 xv2 = make_float2(xo_r[o], xo_r[o]);
-        const uint4* wr = reinterpret_cast<const uint4*>(wrow + o * BN);
+        const float4* wr = reinterpret_cast<const float4*>(wrow + o * BN);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint4 q = wr[u];
-            const __half2* h2 = reinterpret_cast<const __half2*>(&q);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) v2[4 * u + e] = __ffma2_rn(xv2, __half22float2(h2[e]), v2[4 * u + e]);
+        for (int u = 0; u < 8; ++u) {
+            const float4 f = wr[u];
+            v2[2 * u] = __ffma2_rn(xv2, make_float2(f.x, f.y), v2[2 * u]);
+            v2[2 * u + 1] = __ffma2_rn(xv2, make_float2(f.z, f.w), v2[2 * u + 1]);
         }
     }
 }
-
 
 template <int EPI, int CG, int MC>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -229,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + static_cast<size_t>(STAGES) * A_BYTES;
     uint8_t* smem_stg = smem + SMEM_OPERANDS;  // TS: per-warp output staging tiles
-    __half* smem_wo_h = reinterpret_cast<__half*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT);
+    float* smem_wo = reinterpret_cast<float*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT);
     double* smem_col = reinterpret_cast<double*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT + SMEM_WO);
     Barriers* bars = reinterpret_cast<Barriers*>(smem + SMEM_OPERANDS + SMEM_STAGE_OUT + SMEM_WO + SMEM_COLS);
 
@@ -450,7 +449,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                             const int o = i / (BN / 8), v = i % (BN / 8);
                             const uint4 q = o < n_out ? *reinterpret_cast<const uint4*>(
                                 p.wo + static_cast<int64_t>(o) * p.ldwo + col0 + v * 8) : make_uint4(0, 0, 0, 0);
-                            *reinterpret_cast<uint4*>(smem_wo_h + o * BN + v * 8) = q;
+                            const __half2* h2 = reinterpret_cast<const __half2*>(&q);
+                            float4* dst = reinterpret_cast<float4*>(smem_wo + o * BN + v * 8);
+                            const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]);
+                            const float2 f2 = __half22float2(h2[2]), f3 = __half22float2(h2[3]);
+                            dst[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
+                            dst[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
                         }
                     } else {
                         for (int i = et; i < n_cls * BN; i += EPI_THREADS) {
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 v = wo_fast ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + gc])
                                             : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + gc]);
                             }
-                            smem_wo_h[o * BN + j] = __float2half_rn(v);  // exact: v is an fp16 value
+                            smem_wo[o * BN + j] = v;
                         }
                     }
                 }
@@ -560,10 +564,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                         if (n_out > 0 && !(kDev && (p.dbg_epi & 1))) {
                             if (stage_wo) {
-                                const __half* wrow = smem_wo_h + ch * 32;
-                                if (n_cls == 4) outlier_fma_h<4>(v2, xo_r, wrow);
-                                else if (n_cls == 8) outlier_fma_h<8>(v2, xo_r, wrow);
-                                else outlier_fma_h<WO_CAP>(v2, xo_r, wrow);
+                                const float* wrow = smem_wo + ch * 32;
+                                if (n_cls == 4) outlier_fma<4>(v2, xo_r, wrow);
+                                else if (n_cls == 8) outlier_fma<8>(v2, xo_r, wrow);
+                                else outlier_fma<WO_CAP>(v2, xo_r, wrow);
                             } else {
                                 for (int o = 0; o < n_out; ++o) {
                                     const int64_t k = p.o_idx[o];
