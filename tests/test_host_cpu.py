@@ -59,6 +59,11 @@ def test_library_is_sm100a_tcgen05():
     assert "sm_100a" in sass
     for mnemonic in ("UTCIMMA", "LDTM", "UTMALDG", "UTMASTG", "UTCIMMA.2CTA", "UBLKCP"):
         assert mnemonic in sass, mnemonic
+    # no dev instrumentation in the shipped kernels (timeline stamps / wait-cycle
+    # counters live in the `build.py --devtools` library only): even untaken, their
+    # branches cost the GEMM 13-15 % (profiles/r1/gemm_ncu_cfg2_r1f.md)
+    for reg in ("SR_GLOBALTIMER", "SR_CLOCK"):
+        assert reg not in sass, reg
 
 
 def test_backend_plugin_validation():
