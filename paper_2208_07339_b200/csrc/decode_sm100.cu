@@ -327,15 +327,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t G = gridDim.x;
-    const int64_t T = p.total_units;
-    const int64_t u_begin = T * blockIdx.x / G;
-    const int64_t u_end = T * (blockIdx.x + 1) / G;
+    // unit indices fit 32 bits (decode_fits bounds T * G < 2^31): 32-bit division on
+    // the producer / MMA / finisher paths (a 64-bit one is a ~100-instruction call)
+    const uint32_t T = static_cast<uint32_t>(p.total_units);
+    const uint32_t Gu = gridDim.x;
+    const int u_begin = static_cast<int>(T * blockIdx.x / Gu);
+    const int u_end = static_cast<int>(T * (blockIdx.x + 1) / Gu);
     const int num_kb = p.num_kb;
     // the last tile (index n_tiles) is the patch tile: its A rows are the q2 rows
     // of this call's patched columns, written in P2, so it is never prefetched
-    const int64_t main_units = static_cast<int64_t>(p.n_tiles) * num_kb;
-    const int n_pre = static_cast<int>(
-        max(static_cast<int64_t>(0), min(static_cast<int64_t>(p.prefetch), min(u_end, main_units) - u_begin)));
+    const int main_units = p.n_tiles * num_kb;
+    const int n_pre = max(0, min(p.prefetch, min(u_end, main_units) - u_begin));
 
     if (threadIdx.x == 0) DSTAMP(p.dbg, 0);
     // ================= W0: setup + weight prefetch (independent of X)
@@ -357,10 +359,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         bars->n_local = 0;
         const uint64_t pol_w = l2_policy_evict_normal();
         for (int i = 0; i < n_pre; ++i) {
-            const int64_t u = u_begin + i;
+            const int u = u_begin + i;
             mbar_arrive_expect_tx(&bars->full[i], stage_bytes);
             tma_load_2d(&tmap_w, &bars->full[i], ring + static_cast<size_t>(i) * stage_bytes,
-                        static_cast<int>(u % num_kb) * BK, static_cast<int>(u / num_kb) * TILE_N,
+                        (u % num_kb) * BK, (u / num_kb) * TILE_N,
                         pol_w);
         }
     }
@@ -400,8 +402,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- P1: load this CTA's column slice of X (all M rows) into
     // smem; its outlier bits (final) and per-row partial absmax over keep columns
     if (pro) {
-        for (int64_t i = pt; i < M * nvec; i += PT) {
-            const int64_t m = i / nvec, v8 = i % nvec;
+        const int nv = static_cast<int>(nvec);  // 32-bit index math (see u_begin)
+        for (int i = pt; i < static_cast<int>(M) * nv; i += PT) {
+            const int m = i / nv, v8 = i - m * nv;
             const uint4 q = load8(a.x + m * a.ldx, c0 + v8 * 8, K, a.x_vec);
             *reinterpret_cast<uint4*>(xs + m * xs_ld + v8 * 8) = q;
         }
@@ -467,8 +470,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n_out = bars->n_out;
     // codes: 8 consecutive columns per thread item, stored as 8 bytes
     {
-        for (int64_t i = threadIdx.x; i < M * nvec; i += THREADS) {
-            const int64_t m = i / nvec, v8 = i % nvec;
+        const int nv = static_cast<int>(nvec);
+        for (int i = threadIdx.x; i < static_cast<int>(M) * nv; i += THREADS) {
+            const int m = i / nv, v8 = i - m * nv;
             const float amax = hbits_to_float(sram[m]);
             const double s = scale_of(amax);
             const float s32 = static_cast<float>(s);
@@ -499,8 +503,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();  // the X slice (xs) is consumed: its bytes become sxo
     // x[:, O] factors for the epilogue (X is read-only: no need to wait for anyone)
     if (n_out > 0 && n_out <= WO_CAP) {
-        for (int64_t i = threadIdx.x; i < M * n_out; i += THREADS) {
-            const int64_t m = i / n_out, o = i % n_out;
+        for (int i = threadIdx.x; i < static_cast<int>(M) * n_out; i += THREADS) {
+            const int m = i / n_out, o = i - m * n_out;
             sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
         }
     }
@@ -685,18 +689,18 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint64_t pol_w = l2_policy_evict_normal();
             const uint64_t pol_x = l2_policy_evict_last();
             for (int i = 0; i < n_pre; ++i) {  // token halves of the prefilled stages
-                const int64_t u = u_begin + i;
+                const int u = u_begin + i;
                 tma_load_2d(&tmap_x, &bars->full[i], ring + static_cast<size_t>(i) * stage_bytes + A_BYTES,
-                            static_cast<int>(u % num_kb) * BK, 0, pol_x);
+                            (u % num_kb) * BK, 0, pol_x);
             }
             int stage = n_pre % p.stages;
             uint32_t phase = n_pre == p.stages ? 1u : 0u;
             int pt_groups = -1;  // patch tile: gathered 4-row groups (set at its first unit)
             bool pt_rest = false;  // rows >= PT_GATHER_ROWS present (box load from pq)
             uint32_t pt_pq = 0;  // bit g: group g is gathered from pq
-            for (int64_t u = u_begin + n_pre; u < u_end; ++u) {
-                const int tile = static_cast<int>(u / num_kb);
-                const int kb = static_cast<int>(u % num_kb);
+            for (int u = u_begin + n_pre; u < u_end; ++u) {
+                const int tile = u / num_kb;
+                const int kb = u - tile * num_kb;
                 mbar_wait(&bars->empty[stage], phase ^ 1u);
                 uint8_t* dst = ring + static_cast<size_t>(stage) * stage_bytes;
                 if (tile < p.n_tiles) {
@@ -772,9 +776,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         int stage = 0;
         uint32_t phase = 0;
         int seg = 0;
-        for (int64_t u = u_begin; u < u_end; ++seg) {
-            const int64_t tile = u / num_kb;
-            const int64_t seg_end = min(u_end, (tile + 1) * num_kb);
+        for (int u = u_begin; u < u_end; ++seg) {
+            const int tile = u / num_kb;
+            const int seg_end = min(u_end, (tile + 1) * num_kb);
             const int acc = seg & 1;
             mbar_wait(&bars->tmem_empty[acc], ((seg >> 1) & 1) ^ 1u);
             tc_fence_after();
@@ -833,9 +837,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int n_local = quad * 32 + lane;
             const int chunks = p.mpad / 16;
             int seg = 0;
-            for (int64_t u = u_begin; u < u_end; ++seg) {
-                const int64_t tile = u / num_kb;
-                const int64_t seg_end = min(u_end, (tile + 1) * num_kb);
+            for (int u = u_begin; u < u_end; ++seg) {
+                const int tile = u / num_kb;
+                const int seg_end = min(u_end, (tile + 1) * num_kb);
                 const int len = static_cast<int>(seg_end - u);
                 const bool full = len == num_kb;
                 u = seg_end;
@@ -912,16 +916,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
                 } else if (finisher && n_ok && !pp) {
                     // contributors: the CTAs whose unit ranges intersect this tile
-                    const int64_t t0 = tile * num_kb, t1 = t0 + num_kb;
-                    const int64_t cf = ((t0 + 1) * G - 1) / T;
-                    const int64_t cl = (t1 * G - 1) / T;
+                    const uint32_t t0 = static_cast<uint32_t>(tile * num_kb), t1 = t0 + num_kb;
+                    const uint32_t cf = ((t0 + 1) * Gu - 1) / T;
+                    const uint32_t cl = (t1 * Gu - 1) / T;
                     for (int64_t m0 = 0; m0 < M; m0 += 16) {
                         int32_t cv[16];
 #pragma unroll
                         for (int jj = 0; jj < 16; ++jj) cv[jj] = 0;
-                        for (int64_t c = cf; c <= cl; ++c) {
-                            const int64_t first_tile = (T * c / G) / num_kb;
-                            const int32_t* src = a.c32 + (c * 2 + (first_tile == tile ? 0 : 1)) * (M * TILE_N) + n_local;
+                        for (uint32_t c = cf; c <= cl; ++c) {
+                            const int first_tile = static_cast<int>(T * c / Gu) / num_kb;
+                            const int32_t* src = a.c32 + (static_cast<int64_t>(c) * 2 + (first_tile == tile ? 0 : 1)) * (M * TILE_N) + n_local;
 #pragma unroll
                             for (int jj = 0; jj < 16; ++jj)
                                 if (m0 + jj < M) cv[jj] += __ldcg(src + (m0 + jj) * TILE_N);
