@@ -405,10 +405,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool wo_fast = n_out <= WO_CAP && p.wo != nullptr && n_out <= p.wo_cap;
         const bool xo_fast = n_out <= WO_CAP && p.xo != nullptr && n_out <= p.o_cap;
         const bool stage_wo = n_out > 0 && n_out <= WO_CAP;
-        // staged outlier rows are padded with zeros to a class of 4 / 8 / 16 so the
+        // staged outlier rows are padded with zeros to a class of 4 / 6 / 8 / 16 so the
         // FMA loop is straight-line code (per-outlier guards made the compiler
         // shuffle the 32 accumulators between registers at every join)
-        const int n_cls = n_out <= 4 ? 4 : (n_out <= 8 ? 8 : WO_CAP);
+        const int n_cls = n_out <= 4 ? 4 : (n_out <= 6 ? 6 : (n_out <= 8 ? 8 : WO_CAP));
         uint32_t stg_cnt = 0;  // TS: output boxes issued by this warp
         __shared__ int split_last;
         long long w_tf = 0;
@@ -566,6 +566,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             if (stage_wo) {
                                 const float* wrow = smem_wo + ch * 32;
                                 if (n_cls == 4) outlier_fma<4>(v2, xo_r, wrow);
+                                else if (n_cls == 6) outlier_fma<6>(v2, xo_r, wrow);
                                 else if (n_cls == 8) outlier_fma<8>(v2, xo_r, wrow);
                                 else outlier_fma<WO_CAP>(v2, xo_r, wrow);
                             } else {
