@@ -123,7 +123,7 @@ __device__ __forceinline__ uint4 load8(const __half* row, int64_t col, int64_t K
 __device__ void compact_block(const uint32_t* __restrict__ mask, int64_t nwords,
                               int32_t* __restrict__ o_idx, int32_t* __restrict__ o_count,
                               int32_t* warp_sums) {
-    const int64_t per = (nwords + blockDim.x - 1) / blockDim.x;
+    const int64_t per = (static_cast<uint32_t>(nwords) + blockDim.x - 1) / blockDim.x;
     const int64_t w0 = threadIdx.x * per;
     const int64_t w1 = w0 + per < nwords ? w0 + per : nwords;
     int32_t local = 0;
@@ -163,7 +163,7 @@ __device__ void compact_block(const uint32_t* __restrict__ mask, int64_t nwords,
 // same scan, but only the first WO_CAP indices (to shared memory) and the count
 __device__ void compact_block_smem(const uint32_t* __restrict__ mask, int64_t nwords, int32_t* o_s,
                                    int32_t* n_s, int32_t* warp_sums) {
-    const int64_t per = (nwords + blockDim.x - 1) / blockDim.x;
+    const int64_t per = (static_cast<uint32_t>(nwords) + blockDim.x - 1) / blockDim.x;
     const int64_t w0 = threadIdx.x * per;
     const int64_t w1 = w0 + per < nwords ? w0 + per : nwords;
     int32_t local = 0;
@@ -380,7 +380,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int64_t M = a.M, K = a.K, N = a.N;
     const int64_t nwords = (K + 31) >> 5;
     int64_t w0, w1;
-    owned_words(nwords, G, blockIdx.x, w0, w1);
+    // 32-bit division (decode_fits bounds nwords * G and N * G below 2^32)
+    w0 = static_cast<uint32_t>(nwords) * blockIdx.x / Gu;
+    w1 = static_cast<uint32_t>(nwords) * (blockIdx.x + 1) / Gu;
     const int64_t c0 = w0 * 32;
     const int64_t c1 = min(w1 * 32, K);
     const int64_t ncols = c1 > c0 ? c1 - c0 : 0;
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     // fixup candidates of this CTA's column range (weight-side data: fetched now,
     // consumed after barrier 1)
-    const int64_t j0 = N * blockIdx.x / G, j1 = N * (blockIdx.x + 1) / G;
+    const int64_t j0 = static_cast<uint32_t>(N) * blockIdx.x / Gu, j1 = static_cast<uint32_t>(N) * (blockIdx.x + 1) / Gu;
     int32_t crA[kTopT], crB[kTopT];
 #pragma unroll
     for (int i = 0; i < kTopT; ++i) {
