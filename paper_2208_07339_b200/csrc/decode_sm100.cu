@@ -449,6 +449,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     // ---------------- P2: row absmax (every CTA reduces the partials), sorted
     // outlier list (CTA 0), codes of this CTA's slice, column fixup
+    // the mask words the fixup tests first (its candidates' rows are known since
+    // P1): loaded now, in flight with the partials below
+    const uint32_t fmA = crA[0] >= 0 ? __ldcg(a.mask + (crA[0] >> 5)) : 0u;
+    const uint32_t fmB = crB[0] >= 0 ? __ldcg(a.mask + (crB[0] >> 5)) : 0u;
     // warp per 4 rows, lanes over the CTAs' partials (all loads in flight first)
     for (int64_t m0 = warp * 4; m0 < M; m0 += NWARPS * 4) {
         uint32_t mx[4] = {0u, 0u, 0u, 0u};
@@ -470,6 +474,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (blockIdx.x == 0 && threadIdx.x < WO_CAP && threadIdx.x < K) bars->o_s[threadIdx.x] = a.o_idx[threadIdx.x];
     __syncthreads();
     const int n_out = bars->n_out;
+    // x[:, O] factor of this thread's first item: loaded before the codes (stored
+    // after them, when the X slice's shared memory is free)
+    const bool xo_on = n_out > 0 && n_out <= WO_CAP;
+    const int xo_items = xo_on ? static_cast<int>(M) * n_out : 0;
+    float xo_first = 0.0f;
+    if (static_cast<int>(threadIdx.x) < xo_items) {
+        const int m = threadIdx.x / n_out, o = threadIdx.x - m * n_out;
+        xo_first = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
+    }
     // codes: 8 consecutive columns per thread item, stored as 8 bytes
     {
         const int nv = static_cast<int>(nvec);
@@ -504,11 +517,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();  // the X slice (xs) is consumed: its bytes become sxo
     // x[:, O] factors for the epilogue (X is read-only: no need to wait for anyone)
-    if (n_out > 0 && n_out <= WO_CAP) {
-        for (int i = threadIdx.x; i < static_cast<int>(M) * n_out; i += THREADS) {
-            const int m = i / n_out, o = i - m * n_out;
-            sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
-        }
+    if (static_cast<int>(threadIdx.x) < xo_items) {
+        const int m = threadIdx.x / n_out, o = threadIdx.x - m * n_out;
+        sxo[m * WO_CAP + o] = xo_first;
+    }
+    for (int i = threadIdx.x + THREADS; i < xo_items; i += THREADS) {
+        const int m = i / n_out, o = i - m * n_out;
+        sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
     }
     // weight-stationary fixup (weights.cu fixup_kernel semantics) over this
     // CTA's column range; the four candidates were fetched during P1
@@ -519,7 +534,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int32_t cr[kTopT];
 #pragma unroll
         for (int i = 0; i < kTopT; ++i) cr[i] = h ? crB[i] : crA[i];
-        if (cr[0] < 0 || !bit_of(a.mask, cr[0])) continue;
+        if (cr[0] < 0 || !(((h ? fmB : fmA) >> (cr[0] & 31)) & 1u)) continue;
         float a_new = -1.0f;
         bool exhausted = true;
         int src = 0;  // 1: the cached q2 row holds this column's new codes
