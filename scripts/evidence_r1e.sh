@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-1 (late) evidence capture on one B200 (dev tool; run under gpurun).
-O=gpurun_out/ev6
+O=gpurun_out/ev8
 mkdir -p $O
 timeout 120 python scripts/pcie_bw.py > $O/pcie.json 2>&1
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > $O/gpu.csv
