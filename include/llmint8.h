@@ -252,6 +252,15 @@ int i8mm_zeropoint_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw
                           int64_t N, float* y, int64_t ldy, void* workspace, size_t workspace_bytes,
                           void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Measurement (not on the reference path): the box's own dense
+ * INT8 tensor-core ceiling, the roofline denominator of bench.py. Launches a
+ * kernel that only issues tcgen05.mma.kind::i8 from shared memory (random
+ * operands), one CTA (cg = 1, M = 128) or CTA pair (cg = 2, M = 256) per SM,
+ * N = 256, `iters` x 8 MMAs each. i8mm_peak_mma_ops = int8 ops of one launch. */
+int i8mm_peak_mma_launch(int cg, int iters, void* stream);
+double i8mm_peak_mma_ops(int cg, int iters);
+
 #ifdef __cplusplus
 }
 #endif

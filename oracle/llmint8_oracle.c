@@ -206,3 +206,47 @@ int64_t oracle_llm_int8_matmul(const float* x, const float* w, int64_t M, int64_
     if (own_c) free(c);
     return n_out;
 }
+
+/* gemm.py:242-247 for a block of rows once O (mask) and the column side
+ * (gemm.py:243: wq full-height codes with zeros at outlier rows, sw) are known:
+ * rows are independent (rowwise scales, int8 GEMM, dequant, ordered f64
+ * outlier term). bench.py's reference arm times this together with the scan
+ * and the column quantization of the matching share of the workload. */
+void oracle_llm_int8_rows(const float* x, int64_t M, int64_t K, int64_t N, const uint8_t* mask,
+                          const int8_t* wq, const double* sw, const float* w, float* out,
+                          int threads) {
+    set_threads(threads);
+    int64_t n_out = 0;
+    for (int64_t k = 0; k < K; ++k) n_out += mask[k] ? 1 : 0;
+    int64_t n_keep = K - n_out;
+    int8_t* xq = (int8_t*)malloc((size_t)(M * K));
+    int32_t* c = (int32_t*)malloc((size_t)(M * N) * sizeof(int32_t));
+    double* sx = (double*)malloc((size_t)M * sizeof(double));
+    if (n_keep > 0) {
+        oracle_rowwise_quantize(x, M, K, mask, xq, sx);
+        oracle_gemm_i32(xq, wq, c, M, N, K, threads);
+        oracle_dequantize_output(c, sx, sw, out, M, N);
+    }
+    if (n_out > 0) {
+        int64_t* idx = (int64_t*)malloc((size_t)n_out * sizeof(int64_t));
+        int64_t t = 0;
+        for (int64_t k = 0; k < K; ++k)
+            if (mask[k]) idx[t++] = k;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < M; ++i) {
+            for (int64_t j = 0; j < N; ++j) {
+                double acc = 0.0;
+                for (int64_t o = 0; o < n_out; ++o) {
+                    volatile double p = (double)x[i * K + idx[o]] * (double)w[idx[o] * N + j];
+                    acc = acc + p;
+                }
+                if (n_keep > 0) out[i * N + j] = (float)((double)out[i * N + j] + acc);
+                else out[i * N + j] = (float)acc;
+            }
+        }
+        free(idx);
+    }
+    free(xq);
+    free(c);
+    free(sx);
+}

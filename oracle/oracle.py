@@ -301,6 +301,8 @@ def c_oracle() -> ctypes.CDLL:
                                                ctypes.c_int]
         lib.oracle_llm_int8_matmul.restype = I64
         lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_llm_int8_rows.argtypes = [P, I64, I64, I64, P, P, P, P, P, ctypes.c_int]
+        lib.oracle_llm_int8_rows.restype = None
         _LIB = lib
     return _LIB
 

@@ -72,6 +72,8 @@ EXPORTED_SYMBOLS = (
     "i8mm_scalar_workspace_size",
     "i8mm_absmax_matmul",
     "i8mm_zeropoint_matmul",
+    "i8mm_peak_mma_launch",
+    "i8mm_peak_mma_ops",
 )
 
 _lib = None
@@ -134,6 +136,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_scalar_workspace_size": ([I64, I64, I64], SZ),
         "i8mm_absmax_matmul": ([P, I64, P, I64, I64, I64, I64, P, I64, P, SZ, P], I32),
         "i8mm_zeropoint_matmul": ([P, I64, P, I64, I64, I64, I64, P, I64, P, SZ, P], I32),
+        "i8mm_peak_mma_launch": ([I32, I32, P], I32),
+        "i8mm_peak_mma_ops": ([I32, I32], F64),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)

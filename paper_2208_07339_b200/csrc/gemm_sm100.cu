@@ -719,13 +719,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                         for (int cc = 0; cc < COLS_PER_EPI_WARP / 32; ++cc) {
                             const int ch = half * (COLS_PER_EPI_WARP / 32) + cc;
                             uint32_t r[32];
-                            const int32_t* cr = p.c32 + (c32_col + ch * 32) * p.c32_rows + (row_ok ? row : 0);
+                            int32_t* cr = p.c32 + (c32_col + ch * 32) * p.c32_rows + (row_ok ? row : 0);
 #pragma unroll
                             for (int j = 0; j < 32; ++j)
                                 r[j] = row_ok ? static_cast<uint32_t>(__ldcg(cr + j * p.c32_rows)) : 0u;
+                            // leave the scratch zeroed for the next GEMM over it
+                            if (row_ok) {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) __stcg(cr + j * p.c32_rows, 0);
+                            }
                             emit(ch, r);
                         }
-                        if (et == 0) gstamp(p.dbg, 11);
+                        named_bar_sync(2, EPI_THREADS);
+                        if (et == 0) {
+                            p.c32_cnt[t] = 0;  // and the tile's arrival counter
+                            gstamp(p.dbg, 11);
+                        }
                     }
                 }
             }
@@ -835,7 +844,14 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
     });
     if (attr_err != cudaSuccess) return attr_err;
     const int64_t units = max_tiles * p.ksplit;
-    const int64_t clusters = units < max_clusters ? units : max_clusters;
+    int64_t clusters = units < max_clusters ? units : max_clusters;
+    // tests only: I8MM_GEMM_MAX_CLUSTERS=c caps the persistent grid so that
+    // small shapes run many tiles per CTA (pair): accumulator double-buffering,
+    // per-tile restaging and the grouped raster at production depth
+    if (const char* e = getenv("I8MM_GEMM_MAX_CLUSTERS")) {
+        const int cap = atoi(e);
+        if (cap > 0 && clusters > cap) clusters = cap;
+    }
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, tp, ty, p);

@@ -223,6 +223,42 @@ class Int8Linear(torch.nn.Module):
         p = int(ws[p_off:p_off + 4].view(torch.int32).item())
         return {"decomposed_cols": o, "patched_cols": p}
 
+    def last_views(self) -> dict:
+        """Device views of the last weight-stationary call's intermediates (for
+        parity checks): sorted outlier columns, Xq (M x K codes, 0 at outlier
+        columns), row amax, and the per-call column amax over the keep rows
+        (the cached full-column amax with the patched columns replaced)."""
+        if self._last_ws is None:
+            return {}
+        import ctypes
+
+        ws, m = self._last_ws
+        k, n = self.weight.shape
+        L = nat.lib()
+        views = (ctypes.c_void_p * 8)()
+        nat.check(L.i8mm_linear_workspace_views(ws.data_ptr(), m, k, n, views, 8))
+        wv = (ctypes.c_void_p * 5)()
+        nat.check(L.i8mm_linear_weight_views(self.wbuf.data_ptr(), k, n, wv, 5))
+        base = ws.data_ptr()
+        ldq = (k + 15) // 16 * 16
+
+        def at(ptr, count, dtype, buf=ws, b0=base):
+            off = ptr - b0
+            nbytes = count * torch.tensor([], dtype=dtype).element_size()
+            return buf[off:off + nbytes].view(dtype)
+
+        o = int(at(views[0], 1, torch.int32).item())
+        dims = at(views[1], k, torch.int32)[:o]
+        xq = at(views[2], m * ldq, torch.int8).view(m, ldq)[:, :k]
+        row_amax = at(views[3], m, torch.float32)
+        pc = int(at(views[4], 1, torch.int32).item())
+        col_amax = at(wv[1], n, torch.float32, self.wbuf, self.wbuf.data_ptr()).clone()
+        if pc:
+            pidx = at(views[5], pc, torch.int32).long()
+            col_amax[pidx] = at(views[6], pc, torch.float32)
+        return {"dims": dims, "xq": xq, "row_amax": row_amax, "col_amax": col_amax,
+                "patched_cols": pc}
+
     @classmethod
     def from_linear(cls, lin: torch.nn.Linear, alpha: float = 6.0) -> "Int8Linear":
         return cls(lin.weight.detach().t(), alpha,
