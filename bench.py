@@ -105,6 +105,8 @@ def config_dict(name: str, dist_on: bool, world: int) -> dict:
                "inputs larger than L2 (no flush needed)"),
         "weights": "Int8Linear weight-stationary: cached int8 codes + exact per-call column-scale "
                    "fixup (identical outputs to per-call requantization)",
+        "validation": "NaN/Inf flag raised on the device by the prologue scan; the per-call host "
+                      "read of it is off (Int8Linear(check_finite=False)) in the timed loop",
     }
 
 
@@ -439,10 +441,10 @@ class WorkloadRun:
         for li, (m, k, n) in enumerate(self.layers):
             x, w, _ = planted_pair_device(m, k, n, 6, 20.0, seed=li, device=dev)
             if dist_on:
-                self.mods.append(ShardedInt8Linear(w, alpha=6.0,
+                self.mods.append(ShardedInt8Linear(w, alpha=6.0, check_finite=False,
                                                    fused_gather=False if nccl_gather else None))
             else:
-                self.mods.append(pkg.Int8Linear(w, alpha=6.0))
+                self.mods.append(pkg.Int8Linear(w, alpha=6.0, check_finite=False))
             del w
             self.xs.append(x)
         torch.cuda.synchronize()

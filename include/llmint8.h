@@ -253,6 +253,70 @@ int i8mm_zeropoint_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw
                           void* stream);
 
 /* ---------------------------------------------------------------------------
+ * float32 operands: the reference's DenseMatrix holds float32
+ * (tensors.py:31-49). Values that are all exactly fp16 run the fp16 kernels
+ * above (bit-identical); otherwise these reproduce the reference on the f32
+ * values themselves. Flags words: bit 0 = a NaN/Inf entry (the reference's
+ * DenseMatrix raises ValueError, tensors.py:47-48), bit 1 = an entry that is
+ * not exactly an fp16 value, bit 2 = an int8 code of -128 (tensors.py:95-98).
+ */
+#define I8MM_FLAG_NONFINITE 1
+#define I8MM_FLAG_NOT_F16 2
+#define I8MM_FLAG_CODE_128 4
+/* One pass over f32 X: outlier column mask (|x| >= f32(alpha), gemm.py:208-210;
+ * zeroed here; NULL = no mask), flags |= (atomic OR; caller zeroes), and an
+ * fp16 copy when y16 != NULL. */
+int i8mm_f32_scan(const float* x, int64_t rows, int64_t cols, int64_t ld, float alpha, uint32_t* col_mask,
+                  int32_t* flags, void* y16, int64_t ldy, void* stream);
+/* quantize.py:168-179 / 182-187 on f32 operands (mask NULL = no outliers). */
+int i8mm_f32_quantize_rows(const float* x, int64_t M, int64_t K, int64_t ldx, const uint32_t* col_mask,
+                           int8_t* xq, int64_t ldq, float* row_amax, void* stream);
+int i8mm_f32_quantize_cols_t(const float* w, int64_t K, int64_t N, int64_t ldw, const uint32_t* row_mask,
+                             int8_t* wq_t, int64_t ldq, float* col_amax, void* stream);
+/* gemm.py:239-247 from the int32 accumulator: row x col dequantization, the
+ * ordered f64 outlier term over the sorted o_idx[0..*o_count), the sum. */
+int i8mm_f32_llm_int8_combine(const int32_t* c, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                              const float* row_amax, const float* col_amax, const float* x, int64_t ldx,
+                              const float* w, int64_t ldw, const int32_t* o_idx, const int32_t* o_count,
+                              float* y, int64_t ldy, void* stream);
+/* The whole of gemm.py:214-247 on f32 X (M x K) and W (K x N), float32 Y,
+ * bit-identical to the reference for every finite input. status_out (2 device
+ * int32): [|O|, flags]; never synchronizes the host. */
+size_t i8mm_f32_workspace_size(int64_t M, int64_t K, int64_t N);
+int i8mm_llm_int8_matmul_f32(const float* x, int64_t ldx, const float* w, int64_t ldw, int64_t M,
+                             int64_t K, int64_t N, float alpha, float* y, int64_t ldy, void* workspace,
+                             size_t workspace_bytes, int32_t* status_out, void* stream);
+/* gemm.py:110-117 ordered_matmul_f64: f64 accumulation in ascending inner
+ * index, each product and sum one IEEE op; x, w f32 (elt_bytes 4) or f64 (8). */
+int i8mm_ordered_matmul_f64(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M, int64_t K,
+                            int64_t N, int elt_bytes, double* out, int64_t ldo, void* stream);
+/* quantize.py:26-29 round_half_away on n f32 (4) / f64 (8) values -> f64. */
+int i8mm_round_half_away(const void* src, int64_t n, int elt_bytes, double* dst, void* stream);
+/* quantize.py:214-227 dequantize: codes -> float32 per params kind. */
+#define I8MM_DEQ_ABSMAX 0
+#define I8MM_DEQ_ZEROPOINT 1
+#define I8MM_DEQ_ROWWISE 2
+#define I8MM_DEQ_COLWISE 3
+int i8mm_dequantize_codes(const int8_t* q, int64_t rows, int64_t cols, int64_t ldq, int mode,
+                          const double* s_row, const double* s_col, double scale, int32_t zp, double nd,
+                          double offset, float* out, int64_t ldo, void* stream);
+/* flags |= I8MM_FLAG_CODE_128 when any code is -128 (tensors.py:95-98). */
+int i8mm_check_codes(const int8_t* q, int64_t rows, int64_t cols, int64_t ldq, int32_t* flags, void* stream);
+/* flags |= I8MM_FLAG_NONFINITE when an fp16 entry is NaN/Inf (tensors.py:47-48). */
+int i8mm_f16_check(const void* x, int64_t rows, int64_t cols, int64_t ld, int32_t* flags, void* stream);
+/* exact fp16 -> f32 widening (mixed f16 / f32 operand pairs). */
+int i8mm_f16_to_f32(const void* x, int64_t rows, int64_t cols, int64_t ld, float* y, int64_t ldy, void* stream);
+/* stream-ordered memset 0 of device bytes (flag words, counters). */
+int i8mm_zero(void* p, size_t bytes, void* stream);
+/* tensor-wise statistics / quantizers of the sibling schemes on f32 operands. */
+int i8mm_tensor_stats_f32(const float* x, int64_t rows, int64_t cols, int64_t ld, int32_t* scratch,
+                          float* out3, void* stream);
+int i8mm_absmax_quantize_f32(const float* x, int64_t rows, int64_t cols, int64_t ld, const float* amax,
+                             int8_t* q, int64_t ldq, int transpose, void* stream);
+int i8mm_zeropoint_quantize_f32(const float* x, int64_t rows, int64_t cols, int64_t ld, double nd, int32_t zp,
+                                int8_t* q, int64_t ldq, int transpose, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Measurement (not on the reference path): the box's own dense
  * INT8 tensor-core ceiling, the roofline denominator of bench.py. Launches a
  * kernel that only issues tcgen05.mma.kind::i8 from shared memory (random

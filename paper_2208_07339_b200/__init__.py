@@ -9,17 +9,19 @@ CUDA kernels for sm_100a (tcgen05 + TMA + TMEM) behind the C ABI in
 
 from .errors import GemmOverflowError, ParamsMismatchError, ShapeMismatchError
 from .gemm import (MAX_INNER_DIM, MatmulResult, absmax_matmul, dequantize_output,
-                   extract_outlier_columns, int8_gemm_i32, llm_int8_matmul, vectorwise_matmul,
-                   zeropoint_gemm_i32, zeropoint_matmul)
+                   extract_outlier_columns, int8_gemm_i32, llm_int8_matmul, ordered_matmul_f64,
+                   vectorwise_matmul, zeropoint_gemm_i32, zeropoint_matmul)
 from .linear import (ABSMAX, BACKEND_KINDS, EXACT, VECTORWISE, ZEROPOINT, Int8Linear,
                      LinearBackend, _linear, linear, llm_int8_backend)
-from .quantize import (absmax_quantize, colwise_quantize, rowwise_quantize, vectorwise_params,
-                       zeropoint_quantize)
+from .quantize import (absmax_quantize, colwise_quantize, dequantize, round_half_away,
+                       rowwise_quantize, vectorwise_params, zeropoint_quantize)
 from .graphs import GraphedCall
 from .pipeline import HostIOPipeline, run_host_io
 from .synthetic import planted_pair
-from .types import (AbsmaxParams, ColwiseParams, OutlierSet, QuantizedTensor, RowwiseParams,
-                    ZeropointParams)
+from .tensors import DenseMatrix, Int8Matrix, Int32Matrix, seeded_random_matrix
+from .types import (AbsmaxParams, ColwiseParams, OutlierSet, QuantizedTensor, QuantParams,
+                    RowwiseParams, ZeropointParams)
+from . import int8mm  # the reference-typed API (import swap)
 
 __version__ = "0.1.0"
 
@@ -32,5 +34,6 @@ __all__ = [
     "llm_int8_backend", "linear", "_linear", "Int8Linear", "planted_pair",
     "AbsmaxParams", "ZeropointParams", "absmax_quantize", "zeropoint_quantize",
     "absmax_matmul", "zeropoint_matmul", "zeropoint_gemm_i32", "HostIOPipeline", "run_host_io",
-    "GraphedCall",
+    "GraphedCall", "ordered_matmul_f64", "round_half_away", "dequantize", "QuantParams",
+    "DenseMatrix", "Int8Matrix", "Int32Matrix", "seeded_random_matrix", "int8mm",
 ]

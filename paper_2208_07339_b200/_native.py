@@ -26,6 +26,15 @@ I8MM_ERR_CUDA = 6
 I8MM_ERR_UNSUPPORTED = 7
 I8MM_ERR_ZEROPOINT = 8
 
+FLAG_NONFINITE = 1
+FLAG_NOT_F16 = 2
+FLAG_CODE_128 = 4
+
+DEQ_ABSMAX = 0
+DEQ_ZEROPOINT = 1
+DEQ_ROWWISE = 2
+DEQ_COLWISE = 3
+
 OUT_F16 = 0
 OUT_F32 = 1
 OUT_F32_EXACT = 2
@@ -72,6 +81,22 @@ EXPORTED_SYMBOLS = (
     "i8mm_scalar_workspace_size",
     "i8mm_absmax_matmul",
     "i8mm_zeropoint_matmul",
+    "i8mm_f32_scan",
+    "i8mm_f32_quantize_rows",
+    "i8mm_f32_quantize_cols_t",
+    "i8mm_f32_llm_int8_combine",
+    "i8mm_f32_workspace_size",
+    "i8mm_llm_int8_matmul_f32",
+    "i8mm_ordered_matmul_f64",
+    "i8mm_round_half_away",
+    "i8mm_dequantize_codes",
+    "i8mm_check_codes",
+    "i8mm_f16_check",
+    "i8mm_f16_to_f32",
+    "i8mm_zero",
+    "i8mm_tensor_stats_f32",
+    "i8mm_absmax_quantize_f32",
+    "i8mm_zeropoint_quantize_f32",
     "i8mm_peak_mma_launch",
     "i8mm_peak_mma_ops",
 )
@@ -136,6 +161,23 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_scalar_workspace_size": ([I64, I64, I64], SZ),
         "i8mm_absmax_matmul": ([P, I64, P, I64, I64, I64, I64, P, I64, P, SZ, P], I32),
         "i8mm_zeropoint_matmul": ([P, I64, P, I64, I64, I64, I64, P, I64, P, SZ, P], I32),
+        "i8mm_f32_scan": ([P, I64, I64, I64, F32, P, P, P, I64, P], I32),
+        "i8mm_f32_quantize_rows": ([P, I64, I64, I64, P, P, I64, P, P], I32),
+        "i8mm_f32_quantize_cols_t": ([P, I64, I64, I64, P, P, I64, P, P], I32),
+        "i8mm_f32_llm_int8_combine": ([P, I64, I64, I64, I64, P, P, P, I64, P, I64, P, P, P, I64, P],
+                                      I32),
+        "i8mm_f32_workspace_size": ([I64, I64, I64], SZ),
+        "i8mm_llm_int8_matmul_f32": ([P, I64, P, I64, I64, I64, I64, F32, P, I64, P, SZ, P, P], I32),
+        "i8mm_ordered_matmul_f64": ([P, I64, P, I64, I64, I64, I64, I32, P, I64, P], I32),
+        "i8mm_round_half_away": ([P, I64, I32, P, P], I32),
+        "i8mm_dequantize_codes": ([P, I64, I64, I64, I32, P, P, F64, I32, F64, F64, P, I64, P], I32),
+        "i8mm_check_codes": ([P, I64, I64, I64, P, P], I32),
+        "i8mm_f16_check": ([P, I64, I64, I64, P, P], I32),
+        "i8mm_f16_to_f32": ([P, I64, I64, I64, P, I64, P], I32),
+        "i8mm_zero": ([P, SZ, P], I32),
+        "i8mm_tensor_stats_f32": ([P, I64, I64, I64, P, P, P], I32),
+        "i8mm_absmax_quantize_f32": ([P, I64, I64, I64, P, P, I64, I32, P], I32),
+        "i8mm_zeropoint_quantize_f32": ([P, I64, I64, I64, F64, I32, P, I64, I32, P], I32),
         "i8mm_peak_mma_launch": ([I32, I32, P], I32),
         "i8mm_peak_mma_ops": ([I32, I32], F64),
     }

@@ -42,7 +42,7 @@ int num_sms() {
     return sms;
 }
 
-static int check_device() {
+int check_device() {
     static int ok = -1;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -397,7 +397,7 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
     // gemm.py:225 extract_outlier_columns
     // + gemm.py:242 rowwise over keep columns + gather of x[:, O] (gemm.py:238)
     if ((e = launch_row_prologue(xh, M, K, ldx, alpha, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
-                                 ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st)))
+                                 ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st, nullptr, ws.nonfinite)))
         return I8MM_ERR_CUDA;
     // gemm.py:243 colwise over keep rows, stored K-major
     if ((e = launch_quantize_cols_t(wh, K, N, ldw, ws.mask, ws.wq_t, ws.ldq, ws.col_amax, st)))
@@ -547,7 +547,7 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
                          b.col_amax, b.cand_v, b.cand_r, b.q2, ws.p_count, ws.p_idx, ws.p_amax, ws.p_src,
                          ws.wq_p};
     if (launch_row_prologue(xh, M, K, ldx, alpha, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
-                            ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st, &fix))
+                            ws.row_amax, ws.xo, ws.o_cap, ws.rp_scratch, st, &fix, ws.nonfinite))
         return I8MM_ERR_CUDA;
     return I8MM_OK;
 }
@@ -841,6 +841,32 @@ int i8mm_zeropoint_quantize(const void* x, int64_t rows, int64_t cols, int64_t l
     if (rows <= 0 || cols <= 0 || ld < cols || ldq < need || !x || !q || !(nd > 0.0)) return I8MM_ERR_ARGUMENT;
     return cuda_status(launch_quantize_scalar(static_cast<const __half*>(x), rows, cols, ld, 1, nullptr, nd, zp,
                                               q, ldq, transpose, static_cast<cudaStream_t>(stream)));
+}
+
+// float32-operand forms (the reference's DenseMatrix is float32, tensors.py:31-49)
+int i8mm_tensor_stats_f32(const float* x, int64_t rows, int64_t cols, int64_t ld, int32_t* scratch,
+                          float* out3, void* stream) {
+    if (int s = check_device()) return s;
+    if (rows <= 0 || cols <= 0 || ld < cols || !x || !scratch || !out3) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_tensor_stats(x, rows, cols, ld, scratch, out3, static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_absmax_quantize_f32(const float* x, int64_t rows, int64_t cols, int64_t ld, const float* amax,
+                             int8_t* q, int64_t ldq, int transpose, void* stream) {
+    if (int s = check_device()) return s;
+    const int64_t need = transpose ? rows : cols;
+    if (rows <= 0 || cols <= 0 || ld < cols || ldq < need || !x || !amax || !q) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_quantize_scalar(x, rows, cols, ld, 0, amax, 0.0, 0, q, ldq, transpose,
+                                              static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_zeropoint_quantize_f32(const float* x, int64_t rows, int64_t cols, int64_t ld, double nd, int32_t zp,
+                                int8_t* q, int64_t ldq, int transpose, void* stream) {
+    if (int s = check_device()) return s;
+    const int64_t need = transpose ? rows : cols;
+    if (rows <= 0 || cols <= 0 || ld < cols || ldq < need || !x || !q || !(nd > 0.0)) return I8MM_ERR_ARGUMENT;
+    return cuda_status(launch_quantize_scalar(x, rows, cols, ld, 1, nullptr, nd, zp, q, ldq, transpose,
+                                              static_cast<cudaStream_t>(stream)));
 }
 
 int i8mm_rowsum_i8(const int8_t* q, int64_t rows, int64_t cols, int64_t ld, int32_t* out, void* stream) {

@@ -9,6 +9,7 @@ namespace i8mm {
 // launch accounting + device properties (capi.cu)
 void count_launch();
 int num_sms();
+int check_device();  // I8MM_OK on sm_100, else I8MM_ERR_UNSUPPORTED
 bool pdl_enabled();  // I8MM_PDL (default 1)
 
 // Launch with programmatic dependent launch allowed (see pdl_wait in
@@ -67,7 +68,8 @@ struct PerCallFix {
 cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                                 uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
                                 int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
-                                void* scratch, cudaStream_t st, const PerCallFix* fix = nullptr);
+                                void* scratch, cudaStream_t st, const PerCallFix* fix = nullptr,
+                                int32_t* nonfinite = nullptr);
 cudaError_t launch_quantize_cols_t(const __half* w, int64_t K, int64_t N, int64_t ldw,
                                    const uint32_t* row_mask, int8_t* wq_t, int64_t ldq,
                                    float* col_amax, cudaStream_t st);
@@ -111,6 +113,11 @@ cudaError_t launch_tensor_stats(const __half* x, int64_t rows, int64_t cols, int
                                 int32_t* stats_scratch, float* out3, cudaStream_t st);
 // mode 0 = absmax (amax_dev), 1 = zeropoint (nd, zp); transpose writes K-major (cols x ld_out)
 cudaError_t launch_quantize_scalar(const __half* x, int64_t rows, int64_t cols, int64_t ld, int mode,
+                                   const float* amax_dev, double nd, int32_t zp, int8_t* out,
+                                   int64_t ld_out, int transpose, cudaStream_t st);
+cudaError_t launch_tensor_stats(const float* x, int64_t rows, int64_t cols, int64_t ld,
+                                int32_t* stats_scratch, float* out3, cudaStream_t st);
+cudaError_t launch_quantize_scalar(const float* x, int64_t rows, int64_t cols, int64_t ld, int mode,
                                    const float* amax_dev, double nd, int32_t zp, int8_t* out,
                                    int64_t ld_out, int transpose, cudaStream_t st);
 cudaError_t launch_rowsum_i8(const int8_t* q, int64_t rows, int64_t cols, int64_t ld, int32_t* out,

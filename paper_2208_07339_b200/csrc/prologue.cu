@@ -216,12 +216,15 @@ __global__ void zero_u32_kernel(uint32_t* p, int64_t n) {
 
 // two ranges in one launch (the mask and the caller's per-call counters)
 __global__ void zero2_u32_kernel(uint32_t* p, int64_t n, uint32_t* p2, int64_t n2, uint32_t* one,
-                                 uint32_t* p3, int64_t n3) {
+                                 uint32_t* p3, int64_t n3, uint32_t* one2) {
     pdl_wait();
     pdl_trigger();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i0 == 0) *one = 0u;
+    if (i0 == 0) {
+        *one = 0u;
+        if (one2 != nullptr) *one2 = 0u;
+    }
     for (int64_t i = i0; i < n + n2; i += stride) {
         if (i < n) p[i] = 0u;
         else p2[i - n] = 0u;
@@ -1295,7 +1298,8 @@ size_t row_prologue_scratch_bytes(int64_t M, int64_t K) {
 cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t ldx, float alpha,
                                 uint32_t* mask, int32_t* o_idx, int32_t* o_count, int8_t* xq,
                                 int64_t ldq, float* row_amax, __half* xo, int64_t o_cap,
-                                void* scratch, cudaStream_t st, const PerCallFix* fix) {
+                                void* scratch, cudaStream_t st, const PerCallFix* fix,
+                                int32_t* nonfinite) {
     cudaError_t e;
     uint32_t* zero2 = fix != nullptr ? reinterpret_cast<uint32_t*>(fix->p_count) : nullptr;
     const int64_t zero2_n = fix != nullptr ? fixup_zero_words(fix->N) : 0;
@@ -1314,8 +1318,9 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
                 return e;
             count_launch();
         }
+        if (nonfinite != nullptr && (e = cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), st))) return e;
         if (M == 0 || scratch == nullptr || !row_prologue_split_ok(K, ldx, ldq, x, xq)) {
-            if ((e = launch_outlier_scan(x, M, K, ldx, alpha, mask, nullptr, st))) return e;
+            if ((e = launch_outlier_scan(x, M, K, ldx, alpha, mask, nonfinite, st))) return e;
             if ((e = launch_outlier_compact(mask, K, o_idx, o_count, st))) return e;
             e = launch_quantize_rows(x, M, K, ldx, mask, o_idx, o_count, xq, ldq, row_amax, xo, o_cap, st);
         } else {
@@ -1342,7 +1347,8 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
         const int64_t work = nwords + n2 + n3 / 4 + 256;
         if ((e = launch_pdl(zero2_u32_kernel, dim3(static_cast<unsigned>(imin64(work / 256 + 1, 1184))),
                             dim3(256), 0, st, mask, nwords, zero2, n2,
-                            reinterpret_cast<uint32_t*>(done_ctr), z3, n3)))
+                            reinterpret_cast<uint32_t*>(done_ctr), z3, n3,
+                            reinterpret_cast<uint32_t*>(nonfinite))))
             return e;
         count_launch();
     }
@@ -1351,7 +1357,7 @@ cudaError_t launch_row_prologue(const __half* x, int64_t M, int64_t K, int64_t l
     int rb = grid_rows_chunk(M, cb, static_cast<int64_t>(sms) * 8, &rpb);
     if ((e = launch_pdl(outlier_scan_vec_kernel<true>, dim3(static_cast<unsigned>(cb), rb), dim3(256), 0, st,
                         x, M, K, ldx, alpha_threshold_bits(alpha), rpb, mask,
-                        static_cast<int32_t*>(nullptr), gmax, ng, done_ctr, o_idx, o_count, dgrp)))
+                        nonfinite, gmax, ng, done_ctr, o_idx, o_count, dgrp)))
         return e;
     count_launch();
     const int64_t rs_grid = imin64((M + 7) / 8, static_cast<int64_t>(sms) * 8);

@@ -39,7 +39,24 @@ __global__ void stats_init_kernel(int32_t* stats) {
     stats[2] = INT_MIN;
 }
 
-__global__ void __launch_bounds__(256) tensor_stats_kernel(const __half* __restrict__ x, int64_t rows,
+// Element access for fp16 and float32 operands (the reference's DenseMatrix
+// is float32, tensors.py:31-49): value as float, |x| as order-preserving bits.
+template <typename T> struct Elt;
+template <> struct Elt<__half> {
+    static __device__ __forceinline__ float f(__half h) { return __half2float(h); }
+    static __device__ __forceinline__ uint32_t abits(__half h) { return __half_as_ushort(h) & 0x7FFFu; }
+    static __device__ __forceinline__ float from_abits(uint32_t b) {
+        return __half2float(__ushort_as_half(static_cast<unsigned short>(b)));
+    }
+};
+template <> struct Elt<float> {
+    static __device__ __forceinline__ float f(float v) { return v; }
+    static __device__ __forceinline__ uint32_t abits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+    static __device__ __forceinline__ float from_abits(uint32_t b) { return __uint_as_float(b); }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) tensor_stats_kernel(const T* __restrict__ x, int64_t rows,
                                                            int64_t cols, int64_t ld,
                                                            int32_t* __restrict__ stats) {
     uint32_t amax = 0;
@@ -48,9 +65,9 @@ __global__ void __launch_bounds__(256) tensor_stats_kernel(const __half* __restr
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t r = i / cols, c = i % cols;
-        const __half h = x[r * ld + c];
-        amax = max(amax, static_cast<uint32_t>(__half_as_ushort(h)) & 0x7FFFu);
-        const int o = f32_ordered(__half2float(h));
+        const T h = x[r * ld + c];
+        amax = max(amax, Elt<T>::abits(h));
+        const int o = f32_ordered(Elt<T>::f(h));
         mn = min(mn, o);
         mx = max(mx, o);
     }
@@ -68,8 +85,9 @@ __global__ void __launch_bounds__(256) tensor_stats_kernel(const __half* __restr
 }
 
 // stats -> floats: out[0] = amax, out[1] = min, out[2] = max
+template <typename T>
 __global__ void stats_finish_kernel(const int32_t* stats, float* out) {
-    out[0] = __half2float(__ushort_as_half(static_cast<unsigned short>(stats[0])));
+    out[0] = Elt<T>::from_abits(static_cast<uint32_t>(stats[0]));
     out[1] = ordered_f32(stats[1]);
     out[2] = ordered_f32(stats[2]);
 }
@@ -96,9 +114,9 @@ __device__ __forceinline__ int scalar_code(float x, const float* amax_dev, doubl
     }
 }
 
-template <int MODE, bool TRANSPOSE>
+template <typename T, int MODE, bool TRANSPOSE>
 __global__ void __launch_bounds__(256) quantize_scalar_kernel(
-    const __half* __restrict__ x, int64_t rows, int64_t cols, int64_t ld, const float* amax_dev,
+    const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ld, const float* amax_dev,
     double nd, int32_t zp, int8_t* __restrict__ out, int64_t ld_out, int64_t out_rows,
     int64_t out_cols) {
     __shared__ int8_t tile[32][33];
@@ -109,7 +127,7 @@ __global__ void __launch_bounds__(256) quantize_scalar_kernel(
             const int64_t r = r0 + i, c = c0 + tx;
             if (r < out_rows && c < out_cols)
                 out[r * ld_out + c] = (r < rows && c < cols)
-                                          ? static_cast<int8_t>(scalar_code<MODE>(__half2float(x[r * ld + c]), amax_dev, nd, zp))
+                                          ? static_cast<int8_t>(scalar_code<MODE>(Elt<T>::f(x[r * ld + c]), amax_dev, nd, zp))
                                           : int8_t(0);
         }
     } else {
@@ -117,7 +135,7 @@ __global__ void __launch_bounds__(256) quantize_scalar_kernel(
         for (int i = ty; i < 32; i += 8) {
             const int64_t r = r0 + i, c = c0 + tx;
             tile[i][tx] = (r < rows && c < cols)
-                              ? static_cast<int8_t>(scalar_code<MODE>(__half2float(x[r * ld + c]), amax_dev, nd, zp))
+                              ? static_cast<int8_t>(scalar_code<MODE>(Elt<T>::f(x[r * ld + c]), amax_dev, nd, zp))
                               : int8_t(0);
         }
         __syncthreads();
@@ -202,21 +220,31 @@ static unsigned blocks_for(int64_t n, int64_t per = 256, int64_t cap = 4096) {
     return static_cast<unsigned>(b);
 }
 
-cudaError_t launch_tensor_stats(const __half* x, int64_t rows, int64_t cols, int64_t ld,
-                                int32_t* stats_scratch, float* out3, cudaStream_t st) {
+template <typename T>
+static cudaError_t tensor_stats_t(const T* x, int64_t rows, int64_t cols, int64_t ld,
+                                  int32_t* stats_scratch, float* out3, cudaStream_t st) {
     stats_init_kernel<<<1, 1, 0, st>>>(stats_scratch);
     count_launch();
-    tensor_stats_kernel<<<blocks_for(rows * cols, 256, num_sms() * 8), 256, 0, st>>>(x, rows, cols, ld,
-                                                                                 stats_scratch);
+    tensor_stats_kernel<T><<<blocks_for(rows * cols, 256, num_sms() * 8), 256, 0, st>>>(x, rows, cols, ld,
+                                                                                    stats_scratch);
     count_launch();
-    stats_finish_kernel<<<1, 1, 0, st>>>(stats_scratch, out3);
+    stats_finish_kernel<T><<<1, 1, 0, st>>>(stats_scratch, out3);
     count_launch();
     return cudaGetLastError();
 }
+cudaError_t launch_tensor_stats(const __half* x, int64_t rows, int64_t cols, int64_t ld,
+                                int32_t* stats_scratch, float* out3, cudaStream_t st) {
+    return tensor_stats_t(x, rows, cols, ld, stats_scratch, out3, st);
+}
+cudaError_t launch_tensor_stats(const float* x, int64_t rows, int64_t cols, int64_t ld,
+                                int32_t* stats_scratch, float* out3, cudaStream_t st) {
+    return tensor_stats_t(x, rows, cols, ld, stats_scratch, out3, st);
+}
 
-cudaError_t launch_quantize_scalar(const __half* x, int64_t rows, int64_t cols, int64_t ld, int mode,
-                                   const float* amax_dev, double nd, int32_t zp, int8_t* out,
-                                   int64_t ld_out, int transpose, cudaStream_t st) {
+template <typename T>
+static cudaError_t quantize_scalar_t(const T* x, int64_t rows, int64_t cols, int64_t ld, int mode,
+                                     const float* amax_dev, double nd, int32_t zp, int8_t* out,
+                                     int64_t ld_out, int transpose, cudaStream_t st) {
     // output covers [out_rows x ld_out] including the K..ld_out padding
     const int64_t out_rows = transpose ? cols : rows;
     const int64_t out_cols = ld_out;
@@ -225,21 +253,33 @@ cudaError_t launch_quantize_scalar(const __half* x, int64_t rows, int64_t cols, 
     const dim3 grid(static_cast<unsigned>((in_c + 31) / 32), static_cast<unsigned>((in_r + 31) / 32));
     if (mode == MODE_ABSMAX) {
         if (transpose)
-            quantize_scalar_kernel<MODE_ABSMAX, true><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd, zp, out,
-                                                                          ld_out, out_rows, out_cols);
-        else
-            quantize_scalar_kernel<MODE_ABSMAX, false><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd, zp, out,
-                                                                           ld_out, out_rows, out_cols);
-    } else {
-        if (transpose)
-            quantize_scalar_kernel<MODE_ZEROPOINT, true><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd, zp,
+            quantize_scalar_kernel<T, MODE_ABSMAX, true><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd, zp,
                                                                              out, ld_out, out_rows, out_cols);
         else
-            quantize_scalar_kernel<MODE_ZEROPOINT, false><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd, zp,
+            quantize_scalar_kernel<T, MODE_ABSMAX, false><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd, zp,
                                                                               out, ld_out, out_rows, out_cols);
+    } else {
+        if (transpose)
+            quantize_scalar_kernel<T, MODE_ZEROPOINT, true><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd,
+                                                                                zp, out, ld_out, out_rows,
+                                                                                out_cols);
+        else
+            quantize_scalar_kernel<T, MODE_ZEROPOINT, false><<<grid, 256, 0, st>>>(x, rows, cols, ld, amax_dev, nd,
+                                                                                 zp, out, ld_out, out_rows,
+                                                                                 out_cols);
     }
     count_launch();
     return cudaGetLastError();
+}
+cudaError_t launch_quantize_scalar(const __half* x, int64_t rows, int64_t cols, int64_t ld, int mode,
+                                   const float* amax_dev, double nd, int32_t zp, int8_t* out,
+                                   int64_t ld_out, int transpose, cudaStream_t st) {
+    return quantize_scalar_t(x, rows, cols, ld, mode, amax_dev, nd, zp, out, ld_out, transpose, st);
+}
+cudaError_t launch_quantize_scalar(const float* x, int64_t rows, int64_t cols, int64_t ld, int mode,
+                                   const float* amax_dev, double nd, int32_t zp, int8_t* out,
+                                   int64_t ld_out, int transpose, cudaStream_t st) {
+    return quantize_scalar_t(x, rows, cols, ld, mode, amax_dev, nd, zp, out, ld_out, transpose, st);
 }
 
 cudaError_t launch_rowsum_i8(const int8_t* q, int64_t rows, int64_t cols, int64_t ld, int32_t* out,

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _native as nat
-from ._tensors import as_f16_matrix, stream_handle
+from ._tensors import as_f16_matrix, as_operand, new_flags, raise_for_flags, stream_handle
 from .errors import ShapeMismatchError
 from .gemm import (_out_kind, absmax_matmul, llm_int8_matmul, vectorwise_matmul,
                    zeropoint_matmul)
@@ -47,25 +47,33 @@ def llm_int8_backend(alpha: float = 6.0) -> LinearBackend:
     return LinearBackend("llm_int8", alpha)
 
 
-def linear(x, w, backend: LinearBackend, out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+def linear(x, w, backend: LinearBackend, out_dtype: torch.dtype = torch.float32,
+           exact: bool = True, validate: bool = True) -> torch.Tensor:
     """x @ w through the selected backend (transformer.py:257-267).
 
-    The reference returns float32; ``out_dtype`` defaults to that (the
-    tensor-wise ``absmax`` / ``zeropoint`` schemes compute in float32 and are
-    cast when another dtype is requested).
+    Like the reference, inputs are validated as DenseMatrix would
+    (tensors.py:47-48: NaN/Inf raise ValueError; device flags, one 4-byte host
+    read) and the result is float32. ``exact=True`` (default) gives the
+    reference's float32 output bit for bit; ``exact=False`` uses the fast fp32
+    (or fp16 with ``out_dtype``) epilogue, within the stated tolerance.
     """
     if backend.kind == "exact":
-        x16 = as_f16_matrix(x, "x")
-        w16 = as_f16_matrix(w, "w")
-        return (x16.double() @ w16.double()).to(out_dtype)
+        # transformer.py:259: float64 product cast to float32 (a library DGEMM;
+        # not on the LLM.int8() path)
+        xt = as_operand(x, "x", validate=False)
+        wt = as_operand(w, "w", validate=False)
+        return (xt.double() @ wt.double()).to(out_dtype)
     if backend.kind == "vectorwise":
-        return vectorwise_matmul(x, w, out_dtype=out_dtype, validate=False).output
+        return vectorwise_matmul(x, w, out_dtype=out_dtype, exact=exact, validate=validate).output
     if backend.kind == "llm_int8":
-        return llm_int8_matmul(x, w, backend.alpha, out_dtype=out_dtype, validate=False).output
+        return llm_int8_matmul(x, w, backend.alpha, out_dtype=out_dtype, exact=exact,
+                               validate=validate).output
     if backend.kind == "absmax":
-        return absmax_matmul(x, w).output.to(out_dtype)
+        y = absmax_matmul(x, w, validate=validate).output
+        return y if out_dtype == torch.float32 else y.to(out_dtype)
     if backend.kind == "zeropoint":
-        return zeropoint_matmul(x, w).output.to(out_dtype)
+        y = zeropoint_matmul(x, w, validate=validate).output
+        return y if out_dtype == torch.float32 else y.to(out_dtype)
     raise ValueError(f"backend kind must be one of {BACKEND_KINDS}, got {backend.kind!r}")
 
 
@@ -88,14 +96,22 @@ class Int8Linear(torch.nn.Module):
     """
 
     def __init__(self, weight, alpha: float = 6.0, bias=None,
-                 out_dtype: torch.dtype = torch.float16, weight_stationary: bool = True) -> None:
+                 out_dtype: torch.dtype = torch.float16, weight_stationary: bool = True,
+                 check_finite: bool = True) -> None:
         super().__init__()
         if not (float(alpha) > 0):
             raise ValueError(f"alpha must be positive, got {alpha}")
         self.alpha = float(alpha)
         self.out_dtype = out_dtype
         self.weight_stationary = bool(weight_stationary)
+        self.check_finite = bool(check_finite)
         self.register_buffer("weight", as_f16_matrix(weight, "weight"))
+        # the weight is checked once (tensors.py:47-48 rejects NaN/Inf)
+        flags = new_flags(1)
+        nat.check(nat.lib().i8mm_f16_check(self.weight.data_ptr(), self.weight.shape[0],
+                                           self.weight.shape[1], self.weight.stride(0),
+                                           flags.data_ptr(), stream_handle()), "f16_check")
+        raise_for_flags(int(flags.item()))
         if bias is not None:
             b = torch.as_tensor(bias).to(device=self.weight.device, dtype=out_dtype)
             self.register_buffer("bias", b)
@@ -121,8 +137,11 @@ class Int8Linear(torch.nn.Module):
     def matmul(self, x2: torch.Tensor, exact: bool = False, _timer=None) -> torch.Tensor:
         """Y = x2 @ W for an M x K fp16 CUDA matrix (no bias)."""
         if not self.weight_stationary:
+            self._last_ws = None
             return llm_int8_matmul(x2, self.weight, self.alpha, out_dtype=self.out_dtype,
-                                   exact=exact, validate=False, _timer=_timer).output
+                                   exact=exact, _timer=_timer,
+                                   validate=self.check_finite and
+                                   not torch.cuda.is_current_stream_capturing()).output
         L = nat.lib()
         k, n = self.weight.shape
         m = x2.shape[0]
@@ -272,10 +291,37 @@ class Int8Linear(torch.nn.Module):
     def out_features(self) -> int:
         return self.weight.shape[1]
 
+    def _raise_if_nonfinite(self, x2: torch.Tensor) -> None:
+        """check_finite: the reference's DenseMatrix(x) rejects NaN/Inf
+        (transformer.py:260, tensors.py:47-48). The prefill prologue's scan
+        raises a device flag on the way; decode-routed calls check X in one
+        small extra launch. One 4-byte host read; skipped under CUDA-graph
+        capture."""
+        if not self.check_finite or torch.cuda.is_current_stream_capturing():
+            return
+        if self._last_ws is None:
+            return
+        ws, m = self._last_ws
+        k, n = self.weight.shape
+        if self.weight_stationary and not self.uses_decode(m):
+            import ctypes
+
+            views = (ctypes.c_void_p * 8)()
+            nat.check(nat.lib().i8mm_linear_workspace_views(ws.data_ptr(), m, k, n, views, 8))
+            off = views[0] - ws.data_ptr() + 4  # the word after |O|
+            flag = int(ws[off:off + 4].view(torch.int32).item())
+        else:
+            fl = new_flags(1)
+            nat.check(nat.lib().i8mm_f16_check(x2.data_ptr(), x2.shape[0], x2.shape[1],
+                                               x2.stride(0), fl.data_ptr(), stream_handle()))
+            flag = int(fl.item())
+        raise_for_flags(nat.FLAG_NONFINITE if flag else 0)
+
     def forward(self, x: torch.Tensor, _timer=None) -> torch.Tensor:
         lead = x.shape[:-1]
         x2 = as_f16_matrix(x.reshape(-1, x.shape[-1]), "x")
         y = self.matmul(x2, _timer=_timer)
+        self._raise_if_nonfinite(x2)
         if self.bias is not None:
             y = y + self.bias
         return y.reshape(*lead, y.shape[-1])

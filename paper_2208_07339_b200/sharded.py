@@ -138,7 +138,8 @@ class ShardedInt8Linear(torch.nn.Module):
 
     def __init__(self, weight, n_total: int | None = None, alpha: float = 6.0,
                  group=None, local: bool = False, out_dtype: torch.dtype = torch.float16,
-                 weight_stationary: bool = True, fused_gather: bool | None = None):
+                 weight_stationary: bool = True, fused_gather: bool | None = None,
+                 check_finite: bool = True):
         super().__init__()
         # forward() -> forward_fused (symmetric memory) when True; None = use it
         # when the process group supports symmetric memory, else the NCCL pipeline
@@ -152,7 +153,8 @@ class ShardedInt8Linear(torch.nn.Module):
         self.lo, self.hi = shard_bounds(self.n_total, self.world, self.rank)
         if not local:
             w = w[:, self.lo:self.hi].contiguous()
-        self.local = Int8Linear(w, alpha, out_dtype=out_dtype, weight_stationary=weight_stationary)
+        self.local = Int8Linear(w, alpha, out_dtype=out_dtype, weight_stationary=weight_stationary,
+                                check_finite=check_finite)
         self._symm = {}  # forward_fused: (M, device) -> symmetric Y buffer and peer handles
 
     def forward_local(self, x: torch.Tensor, _timer=None) -> torch.Tensor:

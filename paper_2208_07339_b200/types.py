@@ -53,7 +53,7 @@ def _scales_from_amax(amax: torch.Tensor) -> np.ndarray:
     reference (torch's CUDA ``scalar / tensor`` is a reciprocal-multiply and is
     not correctly rounded). The device kernels carry amax, never the scale.
     """
-    a = amax.detach().to("cpu", torch.float64).numpy().copy()
+    a = amax.detach().cpu().numpy().astype(np.float64)  # D2H copy, widened on the host
     a[a == 0.0] = 127.0
     return 127.0 / a
 
@@ -62,7 +62,7 @@ class _VectorParams:
     __slots__ = ("amax", "_scales")
     _what = "scales"
 
-    def __init__(self, amax: torch.Tensor | None = None, scales=None) -> None:
+    def __init__(self, scales=None, *, amax: torch.Tensor | None = None) -> None:
         if (amax is None) == (scales is None):
             raise ValueError("give exactly one of amax or scales")
         if amax is not None:
@@ -91,7 +91,8 @@ class _VectorParams:
 
 
 class RowwiseParams(_VectorParams):
-    """One absmax scale per row (quantize.py:74-81)."""
+    """One absmax scale per row (quantize.py:74-81). ``RowwiseParams(scales)``
+    as in the reference, or ``RowwiseParams(amax=device_tensor)`` from a kernel."""
 
     __slots__ = ()
     _what = "row scales"
@@ -136,6 +137,9 @@ class ZeropointParams:
             raise ValueError(f"zeropoint {self.zp} outside the signed 16-bit range")
         if not np.isfinite(self.offset):
             raise ValueError("offset must be finite")
+
+
+QuantParams = AbsmaxParams | ZeropointParams | RowwiseParams | ColwiseParams  # quantize.py:94
 
 
 @dataclass(frozen=True, eq=False)

@@ -50,3 +50,14 @@ def fp16_tolerance(ref: np.ndarray) -> np.ndarray:
     e = np.floor(np.log2(np.maximum(a, 2.0 ** -14)))
     ulp = 2.0 ** (e - 10)
     return ulp + 1e-5 * max(1.0, float(a.max(initial=0.0)))
+
+
+def f32_cases() -> dict[str, dict]:
+    """float32 (non-fp16) cases written by tests/golden/make_golden_f32.py."""
+    z = np.load(GOLDEN / "f32_cases.npz")
+    out: dict[str, dict] = {}
+    for name in z["_names"].tolist():
+        rec = {k[len(name) + 1:]: z[k] for k in z.files if k.startswith(name + "/")}
+        rec["alpha"] = float(rec["alpha"])
+        out[name] = rec
+    return out

@@ -36,6 +36,30 @@ def test_numpy_oracle_matches_reference(oracle_mod, name):
     assert np.array_equal(oracle_mod.vectorwise_matmul(g["x"], g["w"]), g["vw"])
 
 
+F32 = _golden.f32_cases()
+
+
+@pytest.mark.parametrize("name", sorted(F32))
+def test_oracles_match_reference_on_f32_operands(oracle_mod, name):
+    """Both restatements on float32 values that are not fp16 values (the
+    reference's DenseMatrix is float32, tensors.py:31-49)."""
+    g = F32[name]
+    for tr in (oracle_mod.llm_int8_matmul(g["x"], g["w"], g["alpha"]),
+               oracle_mod.c_llm_int8_matmul(g["x"], g["w"], g["alpha"])):
+        assert tr.dims == tuple(int(d) for d in g["dims"])
+        keep = _golden.keep_mask(g["x"].shape[1], tr.dims)
+        if keep.any():
+            assert np.array_equal(tr.xq[:, keep], g["xq"])
+            assert np.array_equal(tr.sx, g["sx"])
+            assert np.array_equal(tr.wq[keep], g["wq"])
+            assert np.array_equal(tr.sw, g["sw"])
+            assert np.array_equal(tr.c, g["c"])
+        assert np.array_equal(tr.output, g["out"])
+    assert np.array_equal(oracle_mod.vectorwise_matmul(g["x"], g["w"]), g["vw"])
+    assert np.array_equal(oracle_mod.absmax_matmul(g["x"], g["w"]), g["absmax"])
+    assert np.array_equal(oracle_mod.zeropoint_matmul(g["x"], g["w"]), g["zeropoint"])
+
+
 @pytest.mark.parametrize("name", sorted(GOLDEN))
 def test_c_oracle_matches_reference(oracle_mod, name):
     g = GOLDEN[name]
