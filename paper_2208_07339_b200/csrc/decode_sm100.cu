@@ -471,7 +471,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     else compact_block_smem(a.mask, nwords, bars->o_s, &bars->n_out, bars->warp_sums);
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) bars->n_out = *a.o_count;
-    if (blockIdx.x == 0 && threadIdx.x < WO_CAP && threadIdx.x < K) bars->o_s[threadIdx.x] = a.o_idx[threadIdx.x];
+    if (blockIdx.x == 0 && threadIdx.x < WO_CAP && threadIdx.x < *a.o_count)
+        bars->o_s[threadIdx.x] = a.o_idx[threadIdx.x];  // only written entries (initcheck)
     __syncthreads();
     const int n_out = bars->n_out;
     // x[:, O] factor of this thread's first item: loaded before the codes (stored

@@ -90,6 +90,7 @@ __global__ void stats_finish_kernel(const int32_t* stats, float* out) {
     out[0] = Elt<T>::from_abits(static_cast<uint32_t>(stats[0]));
     out[1] = ordered_f32(stats[1]);
     out[2] = ordered_f32(stats[2]);
+    out[3] = 0.0f;  // the host reads the 4-float record whole
 }
 
 // ------------------------------------------------------------------ quantizers

@@ -24,6 +24,7 @@ GEMM epilogue stores each output tile into every rank's Y over NVLink
 from __future__ import annotations
 
 import ctypes
+from collections import OrderedDict
 
 import torch
 import torch.distributed as dist
@@ -155,38 +156,68 @@ class ShardedInt8Linear(torch.nn.Module):
             w = w[:, self.lo:self.hi].contiguous()
         self.local = Int8Linear(w, alpha, out_dtype=out_dtype, weight_stationary=weight_stationary,
                                 check_finite=check_finite)
-        self._symm = {}  # forward_fused: (M, device) -> symmetric Y buffer and peer handles
+        # forward_fused: (M, device) -> symmetric Y buffer and peer handles, LRU-bounded
+        self._symm: "OrderedDict[tuple, tuple]" = OrderedDict()
+        self.symm_cache_size = 4
+        self._fused_ok: bool | None = None  # agreed by all ranks on first use
 
     def forward_local(self, x: torch.Tensor, _timer=None) -> torch.Tensor:
         """This rank's column block Y[:, lo:hi] (no communication)."""
         return self.local(x, _timer=_timer)
 
-    def forward(self, x: torch.Tensor, _timer=None, chunks: int | None = None) -> torch.Tensor:
-        """Y = x @ W over all ranks. ``chunks`` row ranges pipeline the
-        all-gather behind the GEMM (default 4 when world > 1, else 1)."""
+    def fused_supported(self, x2: torch.Tensor) -> bool:
+        """Whether the fused peer-store gather can run, decided ONCE and agreed
+        by every rank (an all-reduce MIN of each rank's probe), so no rank
+        takes a different path than its peers (which would hang the job)."""
+        if self._fused_ok is None:
+            ok = int(self.local.out_dtype == torch.float16 and self.local.weight_stationary
+                     and x2.is_cuda and dist.get_backend(self.group) == "nccl")
+            if ok:
+                try:  # probe: symmetric memory allocation + rendezvous on a tiny buffer
+                    import torch.distributed._symmetric_memory as symm_mem
+
+                    group = self.group if self.group is not None else dist.group.WORLD
+                    t = symm_mem.empty((8,), dtype=torch.float16, device=x2.device)
+                    symm_mem.rendezvous(t, group.group_name)
+                except (ImportError, NotImplementedError, AttributeError, RuntimeError):
+                    ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=x2.device if x2.is_cuda else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+            self._fused_ok = bool(flag.item())
+        return self._fused_ok
+
+    def forward(self, x: torch.Tensor, _timer=None, chunks: int | None = None,
+                out: torch.Tensor | None = None, alias: bool = False) -> torch.Tensor:
+        """Y = x @ W over all ranks. ``chunks`` row ranges pipeline the NCCL
+        all-gather behind the GEMM (default 4 when world > 1, else 1).
+
+        With the fused gather, Y is assembled in a symmetric-memory buffer that
+        the next call with the same M overwrites: by default it is copied into
+        ``out`` (or a fresh tensor); ``alias=True`` returns the buffer itself
+        (valid until the next call -- for callers that consume Y at once)."""
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
-        if self.fused_gather is not False and _timer is None and chunks is None:
-            if (self.local.out_dtype == torch.float16 and self.local.weight_stationary
-                    and x2.is_cuda and dist.get_backend(self.group) == "nccl"):
-                try:
-                    y = self.forward_fused(x2)
-                    self.gather_path = "fused-epilogue"
-                    return y.reshape(*lead, self.n_total)
-                except (RuntimeError, NotImplementedError, AttributeError):
-                    if self.fused_gather:
-                        raise
-                    self.fused_gather = False  # no symmetric memory here: NCCL from now on
-            elif self.fused_gather:
-                raise ValueError("fused_gather needs CUDA tensors, NCCL, fp16 output and a "
-                                 "weight-stationary layer")
+        want_fused = self.fused_gather is not False and _timer is None and chunks is None
+        if want_fused and self.fused_supported(x2):
+            y = self.forward_fused(x2)
+            self.gather_path = "fused-epilogue"
+            if not alias:
+                y = y.clone() if out is None else out.view(-1, self.n_total).copy_(y)
+            return y.reshape(*lead, self.n_total)
+        if self.fused_gather:
+            raise ValueError("fused_gather needs CUDA tensors, NCCL with symmetric memory, fp16 "
+                             "output and a weight-stationary layer")
         self.gather_path = "nccl-pipelined"
         if chunks is None:
             chunks = 4 if self.world > 1 else 1
         if chunks <= 1 or _timer is not None:
             y = self.forward_local(x2, _timer)
-            return gather_columns(y, self.n_total, self.group).reshape(*lead, self.n_total)
-        return self.forward_pipelined(x2, chunks).reshape(*lead, self.n_total)
+            y = gather_columns(y, self.n_total, self.group)
+        else:
+            y = self.forward_pipelined(x2, chunks)
+        if out is not None:
+            y = out.view(-1, self.n_total).copy_(y)
+        return y.reshape(*lead, self.n_total)
 
     def forward_fused(self, x2: torch.Tensor) -> torch.Tensor:
         """Y = x @ W with the all-gather fused into the GEMM epilogue.
@@ -196,7 +227,8 @@ class ShardedInt8Linear(torch.nn.Module):
         NVLink, into every peer's Y (``i8mm_linear_forward_peers``); one
         device-side barrier then orders the peers' stores before the reads. No
         NCCL collective runs. The returned tensor is a persistent buffer per
-        row count, overwritten by the next call with the same M.
+        row count (at most ``symm_cache_size`` row counts are kept, least
+        recently used evicted), overwritten by the next call with the same M.
         """
         import torch.distributed._symmetric_memory as symm_mem
 
@@ -208,7 +240,11 @@ class ShardedInt8Linear(torch.nn.Module):
         x16 = as_f16_matrix(x2, "x")
         m, k = x16.shape
         key = (m, x16.device.index)
-        if key not in self._symm:
+        if key in self._symm:
+            self._symm.move_to_end(key)
+        else:
+            while len(self._symm) >= self.symm_cache_size:
+                self._symm.popitem(last=False)  # the buffer is freed with its last reference
             out = symm_mem.empty((m, self.n_total), dtype=torch.float16, device=x16.device)
             group = self.group if self.group is not None else dist.group.WORLD
             hdl = symm_mem.rendezvous(out, group.group_name)

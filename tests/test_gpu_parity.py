@@ -763,35 +763,44 @@ def test_alternating_decode_prefill_calls_stable(p, oracle_mod):
 
 @pytest.mark.parametrize("case", [(300, 1024, 700, 0), (8, 512, 256, 0), (100, 8704, 700, 6), (600, 1024, 2000, 6)],
                          ids=["prefill", "decode", "splitk_patches", "pairs_patches"])
-def test_forward_peers_fused_gather(p, case):
-    """i8mm_linear_forward_peers: the GEMM epilogue stores every output also
-    into peer buffers at a column offset (the fused all-gather); with local
-    stand-ins for the peers every destination must hold exactly this rank's
-    block, and the local output must equal the plain forward."""
+def test_forward_peers_fused_gather(p, oracle_mod, case):
+    """i8mm_linear_forward_peers as an emulated 2-rank N-shard: each "rank"
+    holds one column block of W and its GEMM epilogue stores its block into
+    BOTH ranks' full-width Y buffers (the fused all-gather). Afterwards every
+    buffer must hold the whole Y: within the fp16 tolerance of the oracle,
+    bitwise equal to the unsharded module, and nothing outside the blocks."""
     import ctypes
 
     from paper_2208_07339_b200 import _native as nat
     from paper_2208_07339_b200._tensors import stream_handle
+    from paper_2208_07339_b200.sharded import shard_bounds
 
     m, k, n, heavy = case
     x, w = _ws_case(21, m, k, n, 6, heavy)
-    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
     x16 = torch.from_numpy(x.astype(np.float16)).cuda()
-    y_ref = lin(x16)
+    y_full = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())(x16)
     L = nat.lib()
-    n_total, col = n + 40, 24  # the block sits at columns [24, 24 + n) of a wider Y
-    peers = [torch.full((m, n_total), -7.0, dtype=torch.float16, device="cuda") for _ in range(2)]
-    ptrs = (ctypes.c_void_p * 2)(*[t.data_ptr() for t in peers])
-    y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-    ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8, device="cuda")
-    nat.check(L.i8mm_linear_forward_peers(
-        x16.data_ptr(), k, m, lin.weight.data_ptr(), n, lin.wbuf.data_ptr(), k, n, 6.0, y.data_ptr(), n,
-        ws.data_ptr(), ws.numel(), ptrs, 2, n_total, col, stream_handle()), "forward_peers")
+    pad = 16  # the buffers are wider than Y: nothing may land past column n
+    bufs = [torch.full((m, n + pad), -7.0, dtype=torch.float16, device="cuda") for _ in range(2)]
+    ptrs = (ctypes.c_void_p * 2)(*[t.data_ptr() for t in bufs])
+    for r in range(2):
+        lo, hi = shard_bounds(n, 2, r)
+        lin = p.Int8Linear(torch.from_numpy(np.ascontiguousarray(w[:, lo:hi]).astype(np.float16)).cuda())
+        y = torch.empty((m, hi - lo), dtype=torch.float16, device="cuda")
+        ws = torch.empty(L.i8mm_linear_workspace_size(m, k, hi - lo), dtype=torch.uint8, device="cuda")
+        nat.check(L.i8mm_linear_forward_peers(
+            x16.data_ptr(), k, m, lin.weight.data_ptr(), hi - lo, lin.wbuf.data_ptr(), k, hi - lo, 6.0,
+            y.data_ptr(), hi - lo, ws.data_ptr(), ws.numel(), ptrs, 2, n + pad, lo, stream_handle()),
+            "forward_peers")
+        assert torch.equal(y, y_full[:, lo:hi])
     torch.cuda.synchronize()
-    assert torch.equal(y, y_ref)
-    for t in peers:
-        assert torch.equal(t[:, col:col + n], y_ref)
-        assert bool((t[:, :col] == -7.0).all()) and bool((t[:, col + n:] == -7.0).all())
+    for t in bufs:
+        got = t[:, :n]
+        assert torch.equal(got, y_full)
+        err = np.abs(_np(got).astype(np.float64) - ref.output)
+        assert (err <= _golden.fp16_tolerance(ref.output)).all()
+        assert bool((t[:, n:] == -7.0).all())
 
 
 def test_sharded_fused_gather_single_rank(p, oracle_mod):
@@ -822,6 +831,15 @@ def test_sharded_fused_gather_single_rank(p, oracle_mod):
             pytest.skip(f"symmetric memory: {str(e).splitlines()[0]}")
         assert torch.equal(y, y_ref)
         assert torch.equal(sh.forward_fused(x16), y_ref)  # cached buffer, second call
+        # forward(): the agreed path is the fused one; results are not aliased
+        y1 = sh(x16)
+        assert sh.gather_path == "fused-epilogue" and torch.equal(y1, y_ref)
+        y2 = sh(torch.zeros_like(x16))
+        assert torch.equal(y1, y_ref) and not bool(y2.abs().max() > 0)
+        assert sh(x16, alias=True).data_ptr() == sh._symm[(700, 0)][0].data_ptr()
+        for mm in (1, 2, 3, 4, 5, 6):  # LRU-bounded symmetric buffers
+            sh(x16[:mm].contiguous())
+        assert len(sh._symm) <= sh.symm_cache_size
     finally:
         dist.destroy_process_group()
 
