@@ -170,21 +170,33 @@ int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, in
                         int out_kind, void* workspace, size_t workspace_bytes,
                         int32_t* o_count_dev, void* stream);
 /* Decode routing. Calls with M <= max_m (default 16, env I8MM_DECODE_MAX_M,
- * at most 256) whose per-CTA slice of X fits shared memory run ONE
- * cooperative kernel (decode_sm100.cu): outlier scan, row
- * quantization, column fixup, patched-column dot products and a swap-AB
- * stream-K tcgen05 GEMM that streams WqT once over all SMs (weight tiles are
- * prefetched while the prologue runs). i8mm_linear_forward issues exactly that
+ * at most 16) run ONE launch of 8-CTA thread-block clusters (decode_sm100.cu):
+ * each cluster derives the outlier set, row scales and codes in distributed
+ * shared memory, the weight stream starts before the dependency wait, and a
+ * swap-AB stream-K tcgen05 GEMM streams WqT once over all SMs; patched columns
+ * are decided and dotted per tile. i8mm_linear_forward issues exactly that
  * launch; with the split entries, i8mm_linear_prologue only records alpha and
  * i8mm_linear_gemm runs the kernel. Outputs are bit-identical to the prefill
  * kernels. The workspace layout depends on the routing, so set max_m before
- * sizing a workspace. */
+ * sizing a workspace. A decode-routed workspace carries per-tile arrival
+ * counters that must be zero when it is first used: call
+ * i8mm_linear_workspace_init once after allocating it (every decode call
+ * leaves them zero; one workspace per stream). */
+int i8mm_linear_workspace_init(void* workspace, size_t workspace_bytes, int64_t M, int64_t K, int64_t N,
+                               void* stream);
+/* Patched-column list of the last decode-routed call on this workspace
+ * (p_count / p_idx / p_amax views): the decode kernel decides patched columns
+ * per tile without publishing them; this recomputes the list the prefill
+ * prologue writes (introspection only, not needed for the outputs). No-op for
+ * prefill-routed workspaces. */
+int i8mm_linear_patch_stats(const void* w, int64_t ldw, const void* wbuf, int64_t M, int64_t K, int64_t N,
+                            void* workspace, size_t workspace_bytes, void* stream);
 void i8mm_debug_set_decode_max_m(int max_m);
 /* Programmatic dependent launch on the prefill path: 1 on (default), 0 off
    (same as I8MM_PDL=0); for A/B measurements. */
 void i8mm_debug_set_pdl(int on);
 int i8mm_linear_uses_decode(int64_t M, int64_t K, int64_t N);
-/* Dev tool: per-CTA %globaltimer stamps of the decode kernel (16 u64 per CTA,
+/* Dev tool: per-CTA %globaltimer stamps of the decode kernel (32 u64 per CTA,
  * device buffer sized for one CTA per SM; NULL disables). */
 void i8mm_debug_decode_timeline(void* stamps);
 /* Fused output all-gather for N-sharded layers (fp16 out): like

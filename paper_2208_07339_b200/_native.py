@@ -67,6 +67,8 @@ EXPORTED_SYMBOLS = (
     "i8mm_linear_forward_peers",
     "i8mm_linear_workspace_views",
     "i8mm_linear_weight_views",
+    "i8mm_linear_workspace_init",
+    "i8mm_linear_patch_stats",
     "i8mm_debug_set_decode_max_m",
     "i8mm_debug_set_pdl",
     "i8mm_linear_uses_decode",
@@ -145,6 +147,8 @@ def _declare(lib: ctypes.CDLL) -> None:
                                        ctypes.c_size_t, P, I32, I64, I64, P], I32),
         "i8mm_linear_workspace_views": ([P, I64, I64, I64, P, I32], I32),
         "i8mm_linear_weight_views": ([P, I64, I64, P, I32], I32),
+        "i8mm_linear_workspace_init": ([P, ctypes.c_size_t, I64, I64, I64, P], I32),
+        "i8mm_linear_patch_stats": ([P, I64, P, I64, I64, I64, P, ctypes.c_size_t, P], I32),
         "i8mm_dequantize_output": ([P, I64, I64, I64, P, P, P, I64, P], I32),
         "i8mm_transpose_i8": ([P, I64, I64, I64, P, I64, P], I32),
         "i8mm_llm_int8_workspace_size": ([I64, I64, I64], ctypes.c_size_t),

@@ -248,14 +248,12 @@ struct Workspace {
     int8_t* wq_p;
     // decode path (M <= decode_max_m(), weight-stationary only)
     bool decode;
-    uint32_t* part;
     uint32_t* ramax_bits;
     int32_t* patch_pos;
     int32_t* c32;
     int64_t c32_words;
     int32_t* tile_cnt;
     int64_t n_tiles;
-    int32_t* pq_ready;   // decode: ready flags of post-barrier patch rows
     uint32_t* thr_word;  // alpha threshold bits, written by the prologue entry
     void* rp_scratch;    // prefill: per-row group maxima + f64 row scales (launch_row_prologue)
     int32_t* sk_c32;     // prefill M <= 128 (linear): split-K partial sums, then tile counters
@@ -315,17 +313,17 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
             // patched columns are dotted in the prologue: no patch codes, but
             // split-K accumulators, partial mask words and per-column state
             const int64_t grid = decode_grid(K, N);
-            w.part = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * grid * M));
             w.ramax_bits = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * M));
             w.patch_pos = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * N));
-            // split-tile partials: two [M x 128] int32 slots per CTA
-            w.c32_words = 2 * grid * M * 128;
+            // split-tile partials: one [16 x 128] int32 slot per CTA
+            w.c32_words = grid * 16 * 128;
             w.c32 = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(w.c32_words)));
             w.n_tiles = (N + 127) / 128;
+            // per-tile arrival counters: zero when the workspace is first used
+            // (i8mm_linear_workspace_init), left zero by every decode call
             w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (w.n_tiles + 2)));
             w.thr_word = reinterpret_cast<uint32_t*>(w.tile_cnt + w.n_tiles + 1);
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(128 * w.ldq)));  // patch tile rows
-            w.pq_ready = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * 128));
         } else {
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(N * w.ldq)));
         }
@@ -486,7 +484,7 @@ static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __h
     d.N = N;
     d.x_vec = (ldx % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
     d.thr_bits = alpha_threshold_bits(alpha);
-    d.part = ws.part;
+    d.nonfinite = ws.nonfinite;
     d.mask = ws.mask;
     d.o_idx = ws.o_idx;
     d.o_count = ws.o_count;
@@ -494,29 +492,15 @@ static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __h
     d.row_amax = ws.row_amax;
     d.xq = ws.xq;
     d.ldq = ws.ldq;
-    d.xo = ws.xo;
-    d.o_cap = ws.o_cap;
     d.w = w;
     d.ldw = ldw;
-    d.w_vec = (N % 8 == 0) && (ldw % 8 == 0) && ((reinterpret_cast<uintptr_t>(w) & 15u) == 0);
     d.wq_t = b.wq_t;
     d.amax_full = b.col_amax;
     d.cand_v = b.cand_v;
     d.cand_r = b.cand_r;
-    d.wo = ws.wo;
-    d.ldwo = round_up(N, 8);
-    d.p_count = ws.p_count;
-    d.p_idx = ws.p_idx;
-    d.p_amax = ws.p_amax;
-    d.patch_pos = ws.patch_pos;
     d.q2 = b.q2;
-    d.pq = ws.wq_p;
-    d.p_src = ws.p_src;
-    d.pq_ready = ws.pq_ready;
     d.c32 = ws.c32;
-    d.c32_words = ws.c32_words;
     d.tile_cnt = ws.tile_cnt;
-    d.n_tiles = ws.n_tiles;
     d.y = y;
     d.ldy = ldy;
     return d;
@@ -739,6 +723,33 @@ int i8mm_linear_workspace_views(void* workspace, int64_t M, int64_t K, int64_t N
     views[6] = ws.p_amax;   // float [N]
     views[7] = ws.wq_p;     // int8 [N x ldq]
     return I8MM_OK;
+}
+
+int i8mm_linear_workspace_init(void* workspace, size_t workspace_bytes, int64_t M, int64_t K, int64_t N,
+                               void* stream) {
+    if (!workspace || M <= 0 || K <= 0 || N <= 0) return I8MM_ERR_ARGUMENT;
+    Workspace ws;
+    if (int s = linear_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
+    if (!ws.decode) return I8MM_OK;  // the prefill routing zeroes its counters every call
+    return cuda_status(cudaMemsetAsync(ws.tile_cnt, 0, sizeof(int32_t) * (ws.n_tiles + 2),
+                                       static_cast<cudaStream_t>(stream)));
+}
+
+int i8mm_linear_patch_stats(const void* w, int64_t ldw, const void* wbuf, int64_t M, int64_t K, int64_t N,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+    if (!w || !wbuf || !workspace || M <= 0 || K <= 0 || N <= 0 || ldw < N) return I8MM_ERR_ARGUMENT;
+    Workspace ws;
+    if (int s = linear_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
+    if (!ws.decode) return I8MM_OK;  // the prefill prologue wrote the patch list
+    const WeightBuf b = carve_weight(reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(wbuf), 256)), K, N);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // the decode kernel decides patched columns per tile; the list the prefill
+    // prologue publishes (weights.cu fixup) is recomputed here from its mask / O
+    if (cudaMemsetAsync(ws.p_count, 0, sizeof(int32_t) * fixup_zero_words(N), st) != cudaSuccess)
+        return I8MM_ERR_CUDA;
+    return cuda_status(launch_gather_fixup(static_cast<const __half*>(w), K, N, ldw, ws.mask, ws.o_idx, ws.o_count,
+                                           ws.o_cap, ws.wo, round_up(N, 8), b.col_amax, b.cand_v, b.cand_r,
+                                           ws.p_count, ws.p_idx, ws.p_amax, ws.p_src, st));
 }
 
 int i8mm_linear_weight_views(void* wbuf, int64_t K, int64_t N, void** views, int n_views) {

@@ -1,10 +1,39 @@
 // Decode path of the weight-stationary LLM.int8() linear layer (SURVEY.md 8f
-// rank 2, config 3: M = 1..256 tokens). At these sizes the layer is bound by
-// the stream of int8 weights from HBM (K*N bytes per call), so the design is
-// ONE cooperative launch (one CTA per SM) that keeps HBM busy from its first
-// cycle: the TMA producer starts streaming weight tiles into the shared-memory
-// ring before the activation prologue has even run, and the remaining per-call
-// work (patched columns) runs on otherwise idle warps under the weight stream.
+// rank 2, config 3: M = 1..16 tokens). At these sizes the layer is bound by the
+// stream of int8 weights from HBM (K*N bytes per call); the token side (outlier
+// scan, row scales, codes, column fixup) is a few hundred KB at most, but it is a
+// reduction over all of X that every weight tile's MMA depends on.
+//
+// ONE launch of 8-CTA thread-block clusters, one CTA per SM, no grid barrier and
+// no cross-kernel hand-off: every cluster derives the token side itself, with
+// the reduction in distributed shared memory, so the only global round trip
+// before the first MMA is the read of X (L2-resident: the previous layer's
+// output). Per CTA (256 threads):
+//   setup   barriers + TMEM; the TMA producer fills the weight ring with the
+//           CTA's first weight tiles before the dependency wait (the cached codes
+//           are never written by a preceding kernel), so HBM streams from the
+//           first microsecond
+//   T1      rank r of the cluster owns k-blocks [num_kb*r/8, num_kb*(r+1)/8):
+//           its X columns (all M rows) -> smem by bulk copies; outlier bits of its
+//           columns are final (the owner sees every row); per-row partial absmax
+//           over its keep columns; both broadcast to every rank (st.shared::cluster)
+//                                                               cluster barrier
+//   T2      row absmax = max of the 8 partials (identical in every rank); codes of
+//           its k-blocks, each written ONCE into the shared-memory B-operand
+//           panel of every rank whose stream-K units use it   cluster barrier
+//   then    warp 0  TMA producer of the remaining weight tiles
+//           warp 1  MMA: D[n, m] += WqT[n, k] Xq[m, k]  (tcgen05 kind::i8, swap-AB:
+//                   M = 128 weight rows, N = 16 token rows, K = 32; B from the panel)
+//           warps 4-7  epilogue, one thread per weight row n: the column fixup
+//                   (a column whose cached maximiser row is an outlier row gets its
+//                   keep-row amax from the cached candidates and its exact int32 dot
+//                   from the cached second-candidate codes q2, on CUDA cores while
+//                   the MMAs run), dequant + outlier term, stores coalesced along n
+// The (n-tile, k-block) space is split evenly over the CTAs (stream-K); a tile
+// split between CTAs is finished by the CTA holding its first k-block, which
+// adds the others' int32 partials (handed over through the workspace with
+// per-tile arrival counters that the finisher resets: the counters must be zero
+// when a workspace is first used, i8mm_linear_workspace_init).
 //
 // Same arithmetic as the prefill path, so outputs are bit-identical to it:
 //   Xq / row amax / outlier set  : prologue.cu semantics (quantize.py:168-179,
@@ -12,29 +41,6 @@
 //   column scales                : weights.cu weight-stationary fixup
 //                                   (quantize.py:182-187 on w[keep, :])
 //   epilogue                     : gemm_sm100.cu (gemm.py:120-147, 238, 244-247)
-//
-// decode_fused_kernel (256 threads, grid = #SMs, cooperative):
-//   W0  barriers, TMEM, and thread 0 issues the weight (A operand) TMA loads
-//       of the first ring stages; their token (B operand) halves follow later
-//   P1  zero the per-call state; outlier scan of 16-row x 128-column items
-//       into partial mask words (no atomics, no pre-zeroed memory)   grid.sync
-//   P2  CTA 0: final mask + sorted outlier list (gemm.py:211); the others:
-//       row absmax over keep columns (atomicMax on fp16 bits)        grid.sync
-//   P3  row codes (fast exact rounding, quant_common.cuh) and the column
-//       fixup -> patched columns (amax changed because the cached
-//       maximiser is an outlier row)                                 grid.sync
-//   then, concurrently:
-//   warp 0  TMA producer: token tiles for the prefilled stages, then both
-//   warp 1  MMA: D[n, m] += WqT[n, k] Xq[m, k]  (tcgen05 kind::i8, swap-AB:
-//           M = 128 weight rows, N = tokens padded to 16, K = 32)
-//   warps 2-7  patched columns: re-derived codes dotted with Xq (exact int32
-//           atomics into the workspace)
-//   warps 4-7  epilogue, one thread per weight row n: dequant + outlier term,
-//           stores coalesced along n
-// The (n-tile, k-block) space is split evenly over the CTAs (stream-K); tiles
-// split between CTAs reduce exactly through int32 red.add, and the CTA that
-// completes a tile runs its epilogue.
-#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -47,8 +53,6 @@
 #include "quant_common.cuh"
 #include "sm100_ptx.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace i8mm {
 
 bool make_tmap_i8_rows(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t K, int64_t ld,
@@ -56,23 +60,23 @@ bool make_tmap_i8_rows(CUtensorMap* map, const int8_t* base, int64_t rows, int64
 
 namespace dec {
 
-constexpr int THREADS = 256;    // warp 0 TMA, 1 MMA, 2 TMEM alloc, 2-7 patches, 4-7 epilogue
+constexpr int THREADS = 256;    // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 epilogue; all in T1/T2
 constexpr int NWARPS = THREADS / 32;
-constexpr int ITEM_ROWS = 16;   // rows per scan / quantize item (one warp)
-constexpr int ITEM_COLS = 128;  // columns per item: 16 lanes x 8 halves, 2 row parities
+constexpr int CL = 8;           // cluster size (portable)
 constexpr int WO_CAP = 16;      // outlier rows of W held in registers by the epilogue
 constexpr int TILE_N = 128;     // weight rows per tile (the MMA's M)
 constexpr int BK = 128;         // K bytes per stage (one SWIZZLE_128B row)
 constexpr int UMMA_K = 32;
-constexpr int MAX_STAGES = 12;
-constexpr int A_BYTES = TILE_N * BK;
-constexpr uint32_t TMEM_COLS = 512;  // two accumulators at column 0 and 256
-constexpr int MAX_M = 256;
-constexpr int LOCAL_CAP = 512;  // fixup columns per CTA (N <= LOCAL_CAP * grid)
-constexpr int PATCH_ROWS = 128; // patched columns handled by the extra tile of the stream
-// the first PT_GATHER_ROWS rows of the patch tile are gathered from q2 (tile::gather4)
-// after the barrier; the rest (many patches) are copied to pq in P2 and box-loaded
-constexpr int PT_GATHER_ROWS = 8;
+constexpr int A_BYTES = TILE_N * BK;  // 16 KB weight tile
+constexpr int MAX_M = 16;       // token rows (the MMA's N is 16)
+constexpr int MPAD = 16;
+constexpr int B_BYTES = MPAD * BK;    // 2 KB panel slot (one k-block of codes)
+constexpr int N_ACC = 4;        // independent accumulators per tile buffer (MMA latency chain)
+constexpr uint32_t TMEM_COLS = 128;   // 2 buffers x N_ACC x 16 columns
+constexpr int MAX_STAGES = 16;
+constexpr int MAX_WORDS = 4096; // mask words (K <= 131072, the MAX_INNER_DIM guard)
+constexpr int NSEG_PRE = 3;     // segments whose cached column data is loaded at kernel start
+constexpr int SMEM_LIMIT = 227 * 1024;
 
 __device__ __forceinline__ bool bit_of(const uint32_t* m, int64_t k) {
     return (m[k >> 5] >> (k & 31)) & 1u;
@@ -87,20 +91,54 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// timeline stamp i of this CTA (dev tool: i8mm_debug_decode_timeline)
+// timeline stamp i of this CTA, 32 per CTA (dev tool: i8mm_debug_decode_timeline)
 // (dev build only: see gemm_sm100.cu, I8MM_GEMM_DEVTOOLS)
 #ifdef I8MM_GEMM_DEVTOOLS
 constexpr bool kDevStamps = true;
 #else
 constexpr bool kDevStamps = false;
 #endif
-#define DSTAMP(ptr, i)                                                               \
-    do {                                                                             \
-        if (kDevStamps && (ptr) != nullptr) (ptr)[blockIdx.x * 16 + (i)] = gtimer(); \
+#define DSTAMP(ptr, i)                                                                 \
+    do {                                                                               \
+        if (kDevStamps && (ptr) != nullptr) (ptr)[blockIdx.x * 32 + (i)] = gtimer(); \
     } while (0)
 
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// 8 consecutive fp16 of a row starting at `col` (zeros past K); 16-byte load
+// when the row is aligned, element loads otherwise.
+__device__ __forceinline__ uint4 load8(const __half* row, int64_t col, int64_t K, bool vec) {
+    if (vec && col + 8 <= K) return *reinterpret_cast<const uint4*>(row + col);
+    uint32_t h[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+        h[e] = col + e < K ? static_cast<uint32_t>(__half_as_ushort(row[col + e])) : 0u;
+    return make_uint4(h[0] | h[1] << 16, h[2] | h[3] << 16, h[4] | h[5] << 16, h[6] | h[7] << 16);
+}
+__device__ __forceinline__ uint32_t half_bits(const uint4& q, int e) {
+    const uint32_t w = e < 2 ? q.x : e < 4 ? q.y : e < 6 ? q.z : q.w;
+    return (e & 1) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+// ---------------------------------------------------------------- cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, const uint4& v) {
+    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+// split cluster barrier: arrive early, wait before the first access to a peer's
+// shared memory (every CTA of the cluster has then started)
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -108,134 +146,84 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     return v;
 }
 
-// 8 consecutive fp16 of a row starting at `col` (zeros past K); 16-byte load
-// when the row is aligned, element loads otherwise.
-__device__ __forceinline__ uint4 load8(const __half* row, int64_t col, int64_t K, bool vec) {
-    if (vec && col + 8 <= K) return ld_stream_u4(row + col);
-    uint32_t h[8];
+// Weight-stationary column fixup (weights.cu fixup_kernel semantics, quantize.py:
+// 182-187 on w[keep, :]) for a column whose cached maximiser row cr[0] is an
+// outlier row: the amax over the keep rows from the cached candidates cr/cv
+// (rows / |w| bits, descending), or -1 when every candidate is an outlier row
+// (the column must be scanned). src = 1: the column's new codes are its cached
+// second-candidate row (q2).
+__device__ __forceinline__ float fixup_amax(const int32_t (&cr)[kTopT], const uint16_t (&cv)[kTopT],
+                                            const uint32_t* mask, int& src) {
+    src = 0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-        h[e] = col + e < K ? static_cast<uint32_t>(__half_as_ushort(row[col + e])) : 0u;
-    return make_uint4(h[0] | h[1] << 16, h[2] | h[3] << 16, h[4] | h[5] << 16, h[6] | h[7] << 16);
+    for (int t = 1; t < kTopT; ++t) {
+        if (cr[t] < 0) {
+            src = t == 1;
+            return 0.0f;
+        }
+        if (!bit_of(mask, cr[t])) {
+            src = t == 1;
+            return hbits_to_float(cv[t]);
+        }
+    }
+    return -1.0f;
 }
 
-// one block: prefix popcount over the mask words, sorted outlier indices
-__device__ void compact_block(const uint32_t* __restrict__ mask, int64_t nwords,
-                              int32_t* __restrict__ o_idx, int32_t* __restrict__ o_count,
-                              int32_t* warp_sums) {
-    const int64_t per = (static_cast<uint32_t>(nwords) + blockDim.x - 1) / blockDim.x;
-    const int64_t w0 = threadIdx.x * per;
-    const int64_t w1 = w0 + per < nwords ? w0 + per : nwords;
-    int32_t local = 0;
-    for (int64_t w = w0; w < w1; ++w) local += __popc(mask[w]);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int32_t incl = local;
+// 16 codes of one token row at columns k0..k0+15, from 16 fp16 values; outlier
+// columns and columns past K give 0 (prologue.cu semantics)
+__device__ __forceinline__ uint4 codes16(const uint4& lo, const uint4& hi, uint32_t mbits, int64_t k0,
+                                         int64_t K, float s32, double s) {
+    uint32_t b[16];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += t;
+    for (int e = 0; e < 16; ++e) {
+        const uint32_t h = half_bits(e < 8 ? lo : hi, e & 7);
+        const int c = (((mbits >> e) & 1u) || k0 + e >= K) ? 0 : code_fast(hbits_to_float(h), s32, s);
+        b[e] = static_cast<uint32_t>(c) & 0xFFu;
     }
-    if (lane == 31) warp_sums[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        const int nw = blockDim.x >> 5;
-        int32_t s = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int32_t t = __shfl_up_sync(0xffffffffu, s, d);
-            if (lane >= d) s += t;
-        }
-        if (lane < nw) warp_sums[lane] = s;
-    }
-    __syncthreads();
-    int32_t pos = incl - local + (wid > 0 ? warp_sums[wid - 1] : 0);
-    for (int64_t w = w0; w < w1; ++w) {
-        uint32_t m = mask[w];
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            o_idx[pos++] = static_cast<int32_t>((w << 5) + b);
-        }
-    }
-    if (threadIdx.x == blockDim.x - 1) *o_count = pos;
-}
-
-// same scan, but only the first WO_CAP indices (to shared memory) and the count
-__device__ void compact_block_smem(const uint32_t* __restrict__ mask, int64_t nwords, int32_t* o_s,
-                                   int32_t* n_s, int32_t* warp_sums) {
-    const int64_t per = (static_cast<uint32_t>(nwords) + blockDim.x - 1) / blockDim.x;
-    const int64_t w0 = threadIdx.x * per;
-    const int64_t w1 = w0 + per < nwords ? w0 + per : nwords;
-    int32_t local = 0;
-    for (int64_t w = w0; w < w1; ++w) local += __popc(__ldcg(mask + w));
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int32_t incl = local;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += t;
-    }
-    if (lane == 31) warp_sums[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        const int nw = blockDim.x >> 5;
-        int32_t s = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int32_t t = __shfl_up_sync(0xffffffffu, s, d);
-            if (lane >= d) s += t;
-        }
-        if (lane < nw) warp_sums[lane] = s;
-    }
-    __syncthreads();
-    int32_t pos = incl - local + (wid > 0 ? warp_sums[wid - 1] : 0);
-    for (int64_t w = w0; w < w1 && pos < WO_CAP; ++w) {
-        uint32_t m = __ldcg(mask + w);
-        while (m && pos < WO_CAP) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            o_s[pos++] = static_cast<int32_t>((w << 5) + b);
-        }
-    }
-    if (threadIdx.x == blockDim.x - 1) *n_s = incl + (wid > 0 ? warp_sums[wid - 1] : 0);
+    return make_uint4(b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24, b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24,
+                      b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24, b[12] | b[13] << 8 | b[14] << 16 | b[15] << 24);
 }
 
 struct __align__(8) Bars {
-    uint64_t full[MAX_STAGES];
-    uint64_t empty[MAX_STAGES];
+    uint64_t full[MAX_STAGES];   // weight tile landed
+    uint64_t empty[MAX_STAGES];  // stage consumed by the MMAs
     uint64_t tmem_full[2];
     uint64_t tmem_empty[2];
+    uint64_t xbar;               // bulk copies of the X slice landed
     uint32_t tmem_slot;
-    int32_t finisher;
+    uint32_t nonfinite[CL];      // rank 0: every rank's NaN/Inf flag
     int32_t n_out;
-    int32_t o_s[WO_CAP];            // first outlier columns (this CTA's compaction)
-    int32_t n_local;                // patched columns found in this CTA's fixup range:
-    int32_t local_j[LOCAL_CAP];     //   column,
-    int32_t local_p[LOCAL_CAP];     //   patch index (row of the patch tile),
-    float local_a[LOCAL_CAP];       //   amax over keep rows,
-    int32_t local_src[LOCAL_CAP];   //   1 = its codes are the cached q2 row
-    int32_t red[16 * NWARPS];       // per-warp partial dot products (patched columns)
-    int32_t pt_rows[PATCH_ROWS];    // producer: q2 row (patched column) of each patch-tile row
+    int32_t o_s[WO_CAP];         // first outlier columns (sorted)
     int32_t warp_sums[NWARPS];
+    int32_t peer_start[CL];      // each rank's first k-block and unit count (panel slots)
+    int32_t peer_len[CL];
+    // epilogue: patched columns of the current segment
+    int32_t n_ent;
+    int32_t ent_j[TILE_N];       // tile row
+    int32_t ent_src[TILE_N];     // 1: codes = cached q2 row, 0: re-derived from W, -1: needs a scan, -2: not patched
+    float ent_a[TILE_N];         // the column's amax over the keep rows
+    int32_t ent_of[TILE_N];      // per tile row: its entry or -1
+    int32_t red[NWARPS * MAX_M];
 };
 
 struct Params {
     DecodeArgs a;
-    int mpad, num_kb, n_tiles, stages;
-    int n_acc;     // accumulators per tile buffer (n_acc * mpad <= 256 TMEM columns)
-    int prefetch;  // weight stages loaded before the prologue (<= stages)
+    int num_kb, n_tiles;
+    int s1, s2;          // weight stages before / after the X slice area is released
+    int pre;             // weight tiles loaded before the token phase (<= s1)
+    int slots;           // panel slots (k-blocks of codes) per CTA
+    int xs_cached;       // the X slice is kept in smem (the ring's stages s1..s2-1) for T2
+    int64_t xs_ld;       // halves per cached X-slice row
     int64_t total_units;
-    uint32_t b_bytes;
     unsigned long long* dbg;  // per-CTA %globaltimer stamps (dev tool), nullable
+    int dbg_mode;             // dev build A/B: bit 0 local panel stores only, bit 1 no code math
 };
 
-// srow (per-token factor) + a union of {this CTA's X column slice (prologue),
-// x[:, O] factors (epilogue)} + barriers
-constexpr size_t SMEM_UNION = 24576;
-constexpr int MAX_OWNED_WORDS = 64;
-__host__ __device__ constexpr size_t smem_extra() {
-    return MAX_M * sizeof(float) + SMEM_UNION + MAX_M * sizeof(uint32_t) +
-           MAX_OWNED_WORDS * sizeof(uint32_t) + sizeof(Bars) + 64;
+// dynamic shared memory after the weight ring and the panel
+__host__ __device__ inline size_t smem_tail(int64_t nwords) {
+    return static_cast<size_t>((nwords + 3) & ~int64_t(3)) * 4 + CL * MAX_M * 4 +
+           MAX_M * (sizeof(double) + 3 * sizeof(float)) + MAX_M * WO_CAP * sizeof(float) +
+           TILE_N * MAX_M * sizeof(int32_t) + sizeof(Bars) + 64;
 }
 
 template <int EPI>
@@ -246,11 +234,14 @@ __device__ __forceinline__ void store_out(const DecodeArgs& a, int64_t m, int64_
         reinterpret_cast<float*>(a.y)[m * a.ldy + n] = v;
 }
 
-// y[m, n] from the exact int32 accumulator c (same op order as gemm_sm100.cu)
+// y[m, n] from the exact int32 accumulator c (same op order as gemm_sm100.cu);
+// the outlier term walks o_s (the first WO_CAP outlier columns), or the whole
+// shared-memory mask in ascending column order when there are more
 template <int EPI>
-__device__ __forceinline__ float epi_value(const DecodeArgs& a, int32_t c, int64_t m, int64_t n,
-                                           float rowf, float colf, float aw, int n_out,
-                                           const float* sxo, const float (&wr)[WO_CAP]) {
+__device__ __forceinline__ float epi_value(const DecodeArgs& a, const int32_t* o_s, const uint32_t* smask,
+                                           int64_t nwords, int32_t c, int64_t m, int64_t n, float rowf,
+                                           float colf, float aw, int n_out, const float* sxo,
+                                           const float (&wr)[WO_CAP]) {
     if constexpr (EPI == EPI_F32_EXACT) {
         const double sx = 127.0 / static_cast<double>(rowf);
         const double sw = 127.0 / static_cast<double>(amax_or_127(aw));
@@ -258,11 +249,16 @@ __device__ __forceinline__ float epi_value(const DecodeArgs& a, int32_t c, int64
         float v = __double2float_rn(__ddiv_rn(static_cast<double>(c), d));
         if (n_out > 0) {
             double hacc = 0.0;
-            for (int o = 0; o < n_out; ++o) {
-                const int64_t k = a.o_idx[o];
+            auto term = [&](int64_t k) {
                 const double xv = __half2float(a.x[m * a.ldx + k]);
                 const double wv = __half2float(a.w[k * a.ldw + n]);
                 hacc = __dadd_rn(hacc, __dmul_rn(xv, wv));
+            };
+            if (n_out <= WO_CAP) {
+                for (int o = 0; o < n_out; ++o) term(o_s[o]);
+            } else {
+                for (int64_t w = 0; w < nwords; ++w)
+                    for (uint32_t bits = smask[w]; bits; bits &= bits - 1) term((w << 5) + __ffs(bits) - 1);
             }
             v = __double2float_rn(__dadd_rn(static_cast<double>(v), hacc));
         }
@@ -273,22 +269,67 @@ __device__ __forceinline__ float epi_value(const DecodeArgs& a, int32_t c, int64
 #pragma unroll
             for (int o = 0; o < WO_CAP; ++o)
                 if (o < n_out) v = fmaf(sxo[m * WO_CAP + o], wr[o], v);
-        } else {
-            for (int o = 0; o < n_out; ++o) {
-                const int64_t k = a.o_idx[o];
-                v = fmaf(__half2float(a.x[m * a.ldx + k]), __half2float(a.w[k * a.ldw + n]), v);
-            }
+        } else if (n_out > WO_CAP) {
+            for (int64_t w = 0; w < nwords; ++w)
+                for (uint32_t bits = smask[w]; bits; bits &= bits - 1) {
+                    const int64_t k = (w << 5) + __ffs(bits) - 1;
+                    v = fmaf(__half2float(a.x[m * a.ldx + k]), __half2float(a.w[k * a.ldw + n]), v);
+                }
         }
         return v;
     }
 }
 
-// 16 token columns of this thread's weight row: sum of the n_acc accumulators
-__device__ __forceinline__ void tmem_row16(uint32_t taddr, int n_acc, int mpad, uint32_t (&r)[16]) {
+// one block: sorted outlier columns from the full mask in shared memory: the
+// first WO_CAP to o_s, all of them to o_idx when non-null, the count to n_out
+__device__ void compact_mask(const uint32_t* __restrict__ smask, int64_t nwords, Bars* bars,
+                             int32_t* __restrict__ o_idx) {
+    const int64_t per = (nwords + THREADS - 1) / THREADS;
+    const int64_t w0 = threadIdx.x * per;
+    const int64_t w1 = w0 + per < nwords ? w0 + per : nwords;
+    int32_t local = 0;
+    for (int64_t w = w0; w < w1; ++w) local += __popc(smask[w]);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t incl = local;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) bars->warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int32_t s = lane < NWARPS ? bars->warp_sums[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t t = __shfl_up_sync(0xffffffffu, s, d);
+            if (lane >= d) s += t;
+        }
+        if (lane < NWARPS) bars->warp_sums[lane] = s;
+    }
+    __syncthreads();
+    int32_t pos = incl - local + (wid > 0 ? bars->warp_sums[wid - 1] : 0);
+    for (int64_t w = w0; w < w1; ++w) {
+        uint32_t m = smask[w];
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const int32_t k = static_cast<int32_t>((w << 5) + b);
+            if (pos < WO_CAP) bars->o_s[pos] = k;
+            if (o_idx != nullptr) o_idx[pos] = k;
+            ++pos;
+        }
+    }
+    if (threadIdx.x == THREADS - 1) bars->n_out = pos;
+}
+
+// 16 token columns of this thread's weight row: sum of the N_ACC accumulators
+__device__ __forceinline__ void tmem_row16(uint32_t taddr, uint32_t (&r)[16]) {
     tmem_ld_32x32b_x16(taddr, r);
-    for (int j = 1; j < n_acc; ++j) {
+#pragma unroll
+    for (int j = 1; j < N_ACC; ++j) {
         uint32_t t[16];
-        tmem_ld_32x32b_x16(taddr + static_cast<uint32_t>(j * mpad), t);
+        tmem_ld_32x32b_x16(taddr + static_cast<uint32_t>(j * MPAD), t);
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 16; ++e) r[e] += t[e];
@@ -296,58 +337,54 @@ __device__ __forceinline__ void tmem_row16(uint32_t taddr, int n_acc, int mpad, 
     tmem_ld_wait();
 }
 
-// mask words owned by CTA c (whole words: the owner sees every row of its
-// columns, so its outlier bits are final without a cross-CTA reduction)
-__host__ __device__ __forceinline__ void owned_words(int64_t nwords, int64_t G, int64_t c,
-                                                     int64_t& w0, int64_t& w1) {
-    w0 = nwords * c / G;
-    w1 = nwords * (c + 1) / G;
-}
-
 template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
-    decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
-                        const __grid_constant__ CUtensorMap tmap_x,
-                        const __grid_constant__ CUtensorMap tmap_p,
-                        const __grid_constant__ CUtensorMap tmap_q2,
-                        const __grid_constant__ CUtensorMap tmap_pb, const Params p) {
-    cg::grid_group grid = cg::this_grid();
+    decode_kernel(const __grid_constant__ CUtensorMap tmap_w, const Params p) {
     const DecodeArgs& a = p.a;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-    const uint32_t stage_bytes = A_BYTES + p.b_bytes;
+    const int64_t M = a.M, K = a.K, N = a.N;
+    const int64_t nwords = (K + 31) >> 5;
     uint8_t* ring = smem;
-    float* srow = reinterpret_cast<float*>(smem + static_cast<size_t>(p.stages) * stage_bytes);
-    float* sxo = srow + MAX_M;                                   // epilogue
-    __half* xs = reinterpret_cast<__half*>(sxo);                 // prologue (same bytes)
-    uint32_t* sram = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(sxo) + SMEM_UNION);
-    uint32_t* smw = sram + MAX_M;                                // owned mask words
-    Bars* bars = reinterpret_cast<Bars*>(smw + MAX_OWNED_WORDS);
+    uint8_t* panel = ring + static_cast<size_t>(p.s2) * A_BYTES;
+    uint32_t* smask = reinterpret_cast<uint32_t*>(panel + static_cast<size_t>(p.slots) * B_BYTES);
+    uint32_t* spart = smask + ((nwords + 3) & ~int64_t(3));            // [CL][MAX_M] partial row amax bits
+    double* sscale = reinterpret_cast<double*>(spart + CL * MAX_M);     // [M]
+    float* sscale32 = reinterpret_cast<float*>(sscale + MAX_M);
+    float* srow = sscale32 + MAX_M;                                     // amax_or_127(row amax)
+    float* samax = srow + MAX_M;                                        // row amax
+    float* sxo = samax + MAX_M;                                         // [M][WO_CAP] x[:, O]
+    int32_t* pdot = reinterpret_cast<int32_t*>(sxo + MAX_M * WO_CAP);    // [TILE_N][MAX_M]
+    Bars* bars = reinterpret_cast<Bars*>(pdot + TILE_N * MAX_M);
+    __half* xs = reinterpret_cast<__half*>(ring + static_cast<size_t>(p.s1) * A_BYTES);  // T1/T2 only
 
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t G = gridDim.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t clu = blockIdx.x / CL;
     // unit indices fit 32 bits (decode_fits bounds T * G < 2^31): 32-bit division on
     // the producer / MMA / finisher paths (a 64-bit one is a ~100-instruction call)
     const uint32_t T = static_cast<uint32_t>(p.total_units);
     const uint32_t Gu = gridDim.x;
     const int u_begin = static_cast<int>(T * blockIdx.x / Gu);
     const int u_end = static_cast<int>(T * (blockIdx.x + 1) / Gu);
+    const int L = u_end - u_begin;
     const int num_kb = p.num_kb;
-    // the last tile (index n_tiles) is the patch tile: its A rows are the q2 rows
-    // of this call's patched columns, written in P2, so it is never prefetched
-    const int main_units = p.n_tiles * num_kb;
-    const int n_pre = max(0, min(p.prefetch, min(u_end, main_units) - u_begin));
+    const int S2 = p.s2;
+    const bool all_kb = L >= num_kb;  // the panel holds every k-block (slot = kb)
+    // k-blocks (and X columns, mask words) this rank owns in T1/T2
+    const int kb_lo = num_kb * static_cast<int>(crank) / CL, kb_hi = num_kb * static_cast<int>(crank + 1) / CL;
+    const int64_t c0 = static_cast<int64_t>(kb_lo) * BK, c1 = min(static_cast<int64_t>(kb_hi) * BK, K);
+    const int64_t w0 = static_cast<int64_t>(kb_lo) * 4, w1 = min(static_cast<int64_t>(kb_hi) * 4, nwords);
+    const int nv = c1 > c0 ? static_cast<int>((c1 - c0 + 7) / 8) : 0;  // 8-column vectors
+    const int nfull = c1 > c0 ? static_cast<int>((c1 - c0) / 8) : 0;
+    const bool cached = p.xs_cached != 0;
+    const int64_t xs_ld = p.xs_ld;
 
-    if (threadIdx.x == 0) DSTAMP(p.dbg, 0);
-    // ================= W0: setup + weight prefetch (independent of X)
-    if (threadIdx.x == 0) {
+    DSTAMP(p.dbg, 0);
+    // ================= setup + weight prefetch (independent of this call's tokens)
+    if (tid == 0) {
         tma_prefetch_desc(&tmap_w);
-        tma_prefetch_desc(&tmap_x);
-        tma_prefetch_desc(&tmap_p);
-        tma_prefetch_desc(&tmap_q2);
-        tma_prefetch_desc(&tmap_pb);
-        for (int s = 0; s < p.stages; ++s) {
+        for (int s = 0; s < S2; ++s) {
             mbar_init(&bars->full[s], 1);
             mbar_init(&bars->empty[s], 1);
         }
@@ -355,444 +392,226 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&bars->tmem_full[q], 1);
             mbar_init(&bars->tmem_empty[q], 4);
         }
+        mbar_init(&bars->xbar, 1);
         fence_mbarrier_init();
-        bars->n_local = 0;
         const uint64_t pol_w = l2_policy_evict_normal();
-        for (int i = 0; i < n_pre; ++i) {
+        for (int i = 0; i < min(p.pre, L); ++i) {
             const int u = u_begin + i;
-            mbar_arrive_expect_tx(&bars->full[i], stage_bytes);
-            tma_load_2d(&tmap_w, &bars->full[i], ring + static_cast<size_t>(i) * stage_bytes,
-                        (u % num_kb) * BK, (u / num_kb) * TILE_N,
-                        pol_w);
+            mbar_arrive_expect_tx(&bars->full[i], A_BYTES);
+            tma_load_2d(&tmap_w, &bars->full[i], ring + static_cast<size_t>(i) * A_BYTES, (u % num_kb) * BK,
+                        (u / num_kb) * TILE_N, pol_w);
         }
+    }
+    if (tid < CL) {  // every rank's unit range: which panel slots its k-blocks land in
+        const uint32_t g = clu * CL + tid;
+        const int ub = static_cast<int>(T * g / Gu), ue = static_cast<int>(T * (g + 1) / Gu);
+        bars->peer_start[tid] = ub % num_kb;
+        bars->peer_len[tid] = ue - ub;
     }
     if (warp == 2) tmem_alloc<TMEM_COLS>(&bars->tmem_slot);
-    // programmatic dependent launch: the weight prefetch above (weights are
-    // never written by the preceding kernels) overlaps the previous layer's
-    // tail; X, the threshold word and the workspace only after the wait
-    pdl_wait();
-    pdl_trigger();
-
-    // ================= prologue (warps 1-7; warp 0 is issuing the prefetch)
-    constexpr int PT = (NWARPS - 1) * 32;
-    const bool pro = warp >= 1;
-    const int pt = threadIdx.x - 32;  // 0..PT-1 for prologue threads
-    const int64_t M = a.M, K = a.K, N = a.N;
-    const int64_t nwords = (K + 31) >> 5;
-    int64_t w0, w1;
-    // 32-bit division (decode_fits bounds nwords * G and N * G below 2^32)
-    w0 = static_cast<uint32_t>(nwords) * blockIdx.x / Gu;
-    w1 = static_cast<uint32_t>(nwords) * (blockIdx.x + 1) / Gu;
-    const int64_t c0 = w0 * 32;
-    const int64_t c1 = min(w1 * 32, K);
-    const int64_t ncols = c1 > c0 ? c1 - c0 : 0;
-    const int64_t nvec = (ncols + 7) / 8;         // 8-column vectors of the slice
-    const int64_t xs_ld = (w1 - w0) * 32;          // halves per smem row
-    const uint32_t thr_bits = a.thr_bits_dev != nullptr ? *a.thr_bits_dev : a.thr_bits;
-
-    // fixup candidates of this CTA's column range (weight-side data: fetched now,
-    // consumed after barrier 1)
-    const int64_t j0 = static_cast<uint32_t>(N) * blockIdx.x / Gu, j1 = static_cast<uint32_t>(N) * (blockIdx.x + 1) / Gu;
-    int32_t crA[kTopT], crB[kTopT];
+    // cached per-column data of the first segments (immutable): loads in flight
+    // through the token phase, consumed by the epilogue warps
+    int32_t pre_cr[NSEG_PRE];
+    float pre_aw[NSEG_PRE];
+    if (warp >= 4) {
+        const int n_local = tid - 128;
+        int u = u_begin;
 #pragma unroll
-    for (int i = 0; i < kTopT; ++i) {
-        const int64_t ja = j0 + threadIdx.x, jb = ja + THREADS;
-        crA[i] = ja < j1 ? a.cand_r[i * N + ja] : -1;
-        crB[i] = jb < j1 ? a.cand_r[i * N + jb] : -1;
-    }
-
-    // ---------------- P1: load this CTA's column slice of X (all M rows) into
-    // smem; its outlier bits (final) and per-row partial absmax over keep columns
-    if (pro) {
-        const int nv = static_cast<int>(nvec);  // 32-bit index math (see u_begin)
-        for (int i = pt; i < static_cast<int>(M) * nv; i += PT) {
-            const int m = i / nv, v8 = i - m * nv;
-            const uint4 q = load8(a.x + m * a.ldx, c0 + v8 * 8, K, a.x_vec);
-            *reinterpret_cast<uint4*>(xs + m * xs_ld + v8 * 8) = q;
-        }
-        for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i <= a.n_tiles; i += G * PT)
-            a.tile_cnt[i] = 0;  // main tiles + the patch tile
-        for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i < N; i += G * PT)
-            a.patch_pos[i] = 0;
-        if (blockIdx.x == 0 && pt == 0) *a.p_count = 0;
-        for (int64_t i = static_cast<int64_t>(blockIdx.x) * PT + pt; i < PATCH_ROWS; i += G * PT)
-            a.pq_ready[i] = 0;
-    }
-    __syncthreads();
-    // one warp per owned word: lane = column, OR over rows
-    for (int64_t w = w0 + (warp - 1); pro && w < w1; w += NWARPS - 1) {
-        const int64_t col = (w - w0) * 32 + lane;
-        uint32_t hit = 0;
-        if (w * 32 + lane < K)
-            for (int64_t m = 0; m < M; ++m)
-                hit |= (__half_as_ushort(xs[m * xs_ld + col]) & 0x7FFFu) >= thr_bits ? 1u : 0u;
-        const uint32_t word = __ballot_sync(0xffffffffu, hit != 0);
-        if (lane == 0) {
-            a.mask[w] = word;
-            smw[w - w0] = word;
+        for (int sg = 0; sg < NSEG_PRE; ++sg) {
+            const int tile = u / num_kb;
+            const int64_t n = static_cast<int64_t>(tile) * TILE_N + n_local;
+            const bool ok = u < u_end && n < N;
+            pre_cr[sg] = ok ? __ldg(a.cand_r + n) : -1;
+            pre_aw[sg] = ok ? __ldg(a.amax_full + n) : 127.0f;
+            u = min(u_end, (tile + 1) * num_kb);
         }
     }
-    __syncthreads();
-    // per-row partial absmax over this slice's keep columns -> part[cta][row]
-    // (warp per row, lanes over columns)
-    for (int64_t m = pro ? warp - 1 : M; m < M; m += NWARPS - 1) {
-        uint32_t mx = 0;
-        for (int64_t col = lane; col < ncols; col += 32)
-            if (!((smw[col >> 5] >> (col & 31)) & 1u))
-                mx = max(mx, static_cast<uint32_t>(__half_as_ushort(xs[m * xs_ld + col])) & 0x7FFFu);
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-        if (lane == 0) a.part[static_cast<int64_t>(blockIdx.x) * M + m] = mx;
+    // token rows M..15 of every panel slot stay zero
+    for (int i = tid; i < p.slots * (MPAD - static_cast<int>(M)) * 8; i += THREADS) {
+        const int per = (MPAD - static_cast<int>(M)) * 8;
+        const int sl = i / per, rr = i - sl * per;
+        *reinterpret_cast<uint4*>(panel + static_cast<size_t>(sl) * B_BYTES + (M + rr / 8) * BK + (rr & 7) * 16) =
+            make_uint4(0u, 0u, 0u, 0u);
     }
-    if (threadIdx.x == 32) DSTAMP(p.dbg, 1);
-    grid.sync();
-
-    // ---------------- P2: row absmax (every CTA reduces the partials), sorted
-    // outlier list (CTA 0), codes of this CTA's slice, column fixup
-    // the mask words the fixup tests first (its candidates' rows are known since
-    // P1): loaded now, in flight with the partials below
-    const uint32_t fmA = crA[0] >= 0 ? __ldcg(a.mask + (crA[0] >> 5)) : 0u;
-    const uint32_t fmB = crB[0] >= 0 ? __ldcg(a.mask + (crB[0] >> 5)) : 0u;
-    // warp per 4 rows, lanes over the CTAs' partials (all loads in flight first)
-    for (int64_t m0 = warp * 4; m0 < M; m0 += NWARPS * 4) {
-        uint32_t mx[4] = {0u, 0u, 0u, 0u};
-        for (int64_t c = lane; c < G; c += 32)
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                if (m0 + r < M) mx[r] = max(mx[r], __ldcg(a.part + c * M + m0 + r));
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) mx[r] = max(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], d));
-            if (lane == 0 && m0 + r < M) sram[m0 + r] = mx[r];
-        }
-    }
-    if (blockIdx.x == 0) compact_block(a.mask, nwords, a.o_idx, a.o_count, bars->warp_sums);
-    else compact_block_smem(a.mask, nwords, bars->o_s, &bars->n_out, bars->warp_sums);
-    __syncthreads();
-    if (blockIdx.x == 0 && threadIdx.x == 0) bars->n_out = *a.o_count;
-    if (blockIdx.x == 0 && threadIdx.x < WO_CAP && threadIdx.x < *a.o_count)
-        bars->o_s[threadIdx.x] = a.o_idx[threadIdx.x];  // only written entries (initcheck)
-    __syncthreads();
-    const int n_out = bars->n_out;
-    // x[:, O] factor of this thread's first item: loaded before the codes (stored
-    // after them, when the X slice's shared memory is free)
-    const bool xo_on = n_out > 0 && n_out <= WO_CAP;
-    const int xo_items = xo_on ? static_cast<int>(M) * n_out : 0;
-    float xo_first = 0.0f;
-    if (static_cast<int>(threadIdx.x) < xo_items) {
-        const int m = threadIdx.x / n_out, o = threadIdx.x - m * n_out;
-        xo_first = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
-    }
-    // codes: 8 consecutive columns per thread item, stored as 8 bytes
-    {
-        const int nv = static_cast<int>(nvec);
-        for (int i = threadIdx.x; i < static_cast<int>(M) * nv; i += THREADS) {
-            const int m = i / nv, v8 = i - m * nv;
-            const float amax = hbits_to_float(sram[m]);
-            const double s = scale_of(amax);
-            const float s32 = static_cast<float>(s);
-            const uint32_t mb = (smw[(v8 * 8) >> 5] >> ((v8 * 8) & 31)) & 0xFFu;
-            const __half* h = xs + m * xs_ld + v8 * 8;
-            uint32_t b[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int c = (((mb >> e) & 1u) || c0 + v8 * 8 + e >= K) ? 0 : code_fast(__half2float(h[e]), s32, s);
-                b[e] = static_cast<uint32_t>(c) & 0xFFu;
-            }
-            *reinterpret_cast<uint2*>(a.xq + m * a.ldq + c0 + v8 * 8) =
-                make_uint2(b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24, b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24);
-        }
-        if (blockIdx.x == G - 1) {  // K..ldq padding
-            const int64_t pad0 = (K + 7) / 8 * 8;
-            for (int64_t i = threadIdx.x; i < M * ((a.ldq - pad0) / 8); i += THREADS) {
-                const int64_t per = (a.ldq - pad0) / 8;
-                *reinterpret_cast<uint2*>(a.xq + (i / per) * a.ldq + pad0 + (i % per) * 8) = make_uint2(0u, 0u);
-            }
-        }
-        if (blockIdx.x == 0)
-            for (int64_t m = threadIdx.x; m < M; m += THREADS) {
-                a.row_amax[m] = hbits_to_float(sram[m]);
-                a.ramax_bits[m] = sram[m];
-            }
-    }
-    __syncthreads();  // the X slice (xs) is consumed: its bytes become sxo
-    // x[:, O] factors for the epilogue (X is read-only: no need to wait for anyone)
-    if (static_cast<int>(threadIdx.x) < xo_items) {
-        const int m = threadIdx.x / n_out, o = threadIdx.x - m * n_out;
-        sxo[m * WO_CAP + o] = xo_first;
-    }
-    for (int i = threadIdx.x + THREADS; i < xo_items; i += THREADS) {
-        const int m = i / n_out, o = i - m * n_out;
-        sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
-    }
-    // weight-stationary fixup (weights.cu fixup_kernel semantics) over this
-    // CTA's column range; the four candidates were fetched during P1
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int64_t j = j0 + threadIdx.x + h * THREADS;
-        if (j >= j1) continue;
-        int32_t cr[kTopT];
-#pragma unroll
-        for (int i = 0; i < kTopT; ++i) cr[i] = h ? crB[i] : crA[i];
-        if (cr[0] < 0 || !(((h ? fmB : fmA) >> (cr[0] & 31)) & 1u)) continue;
-        float a_new = -1.0f;
-        bool exhausted = true;
-        int src = 0;  // 1: the cached q2 row holds this column's new codes
-#pragma unroll
-        for (int i = 1; i < kTopT; ++i) {
-            if (!exhausted) break;
-            if (cr[i] < 0) {
-                exhausted = false;
-                a_new = 0.0f;
-                src = i == 1;
-            } else if (!bit_of(a.mask, cr[i])) {
-                exhausted = false;
-                a_new = hbits_to_float(a.cand_v[i * N + j]);
-                src = i == 1;
-            }
-        }
-        if (exhausted) {
-            uint32_t m = 0;
-            for (int64_t k = 0; k < K; ++k)
-                if (!bit_of(a.mask, k))
-                    m = max(m, static_cast<uint32_t>(__half_as_ushort(a.w[k * a.ldw + j])) & 0x7FFFu);
-            a_new = hbits_to_float(m);
-        }
-        if (a_new != a.amax_full[j]) {
-            const int32_t pidx = atomicAdd(a.p_count, 1);
-            a.p_idx[pidx] = static_cast<int32_t>(j);
-            a.p_amax[pidx] = a_new;
-            a.patch_pos[j] = pidx + 1;
-            a.p_src[pidx] = src;
-            // the patch tile gathers this row from q2 after the barrier: pull it into
-            // L2 now (asynchronous; nothing here waits for it)
-            if (src && pidx < PT_GATHER_ROWS)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.q2 + j * a.ldq),
-                             "r"(static_cast<uint32_t>(a.ldq & ~int64_t(15)))
-                             : "memory");
-            const int li = atomicAdd(&bars->n_local, 1);
-            bars->local_j[li] = static_cast<int32_t>(j);
-            bars->local_p[li] = pidx;
-            bars->local_a[li] = a_new;
-            bars->local_src[li] = src;
-        }
-    }
-    __syncthreads();
-    // patch-tile rows: a patched column whose codes are its cached q2 row (the
-    // common case) is gathered straight from q2 by the patch tile's producer
-    // (TMA tile::gather4, no copy here); only re-derived codes (its top-2 rows
-    // are both outlier rows: rare) are written to pq now
-    for (int li = 0; li < bars->n_local; ++li) {
-        const int pidx = bars->local_p[li];
-        if (pidx >= PATCH_ROWS || (bars->local_src[li] && pidx < PT_GATHER_ROWS)) continue;
-        const int64_t j = bars->local_j[li];
-        int8_t* dst = a.pq + static_cast<int64_t>(pidx) * a.ldq;
-        if (bars->local_src[li]) {  // rows >= PT_GATHER_ROWS: one box load of pq after the barrier
-            const uint4* srcq = reinterpret_cast<const uint4*>(a.q2 + j * a.ldq);
-            for (int64_t v = threadIdx.x; v < a.ldq / 16; v += THREADS)
-                reinterpret_cast<uint4*>(dst)[v] = __ldcs(srcq + v);
-        } else {
-            const double sc = scale_of(bars->local_a[li]);
-            const float s32 = static_cast<float>(sc);
-            for (int64_t k = threadIdx.x; k < a.ldq; k += THREADS)
-                dst[k] = (k < K && !bit_of(a.mask, k))
-                             ? static_cast<int8_t>(code_fast(__half2float(a.w[k * a.ldw + j]), s32, sc)) : int8_t(0);
-        }
-    }
-    // Xq and the patch rows are read back by TMA (async proxy) after the barrier
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    if (threadIdx.x == 32) DSTAMP(p.dbg, 3);
-    grid.sync();
-    if (threadIdx.x == 0) DSTAMP(p.dbg, 4);
-    // per-token factors (rows of X) staged once; x[:, O] was staged in P2
-    for (int64_t m = threadIdx.x; m < M; m += THREADS) srow[m] = amax_or_127(hbits_to_float(sram[m]));
-    __syncthreads();
-    // ---------------- this CTA's patched columns, complete, before its weight
-    // stream resumes (memory is quiet; nothing downstream waits on them): exact
-    // int32 dots of the re-derived codes (q2 row, or W's column in the rare
-    // multi-outlier case) with Xq, then the same epilogue math
-    if (threadIdx.x == 0 && (kDevStamps && p.dbg != nullptr)) {
-        p.dbg[blockIdx.x * 16 + 12] = static_cast<unsigned long long>(bars->n_local);
-        p.dbg[blockIdx.x * 16 + 13] = static_cast<unsigned long long>(bars->n_local ? bars->local_src[0] : 9);
-    }
-    for (int li = 0; li < bars->n_local; ++li) {
-        if (bars->local_p[li] < PATCH_ROWS) continue;  // handled by the patch tile
-        const int64_t j = bars->local_j[li];
-        const float aw = bars->local_a[li];
-        const bool src = bars->local_src[li] != 0;
-        const double s = scale_of(aw);
-        const float s32 = static_cast<float>(s);
-        const int64_t nk16 = a.ldq / 16;
-        for (int64_t m0 = 0; m0 < M; m0 += 16) {
-            int acc[16];
-#pragma unroll
-            for (int mm = 0; mm < 16; ++mm) acc[mm] = 0;
-            for (int64_t kv = threadIdx.x; kv < nk16; kv += THREADS) {
-                uint4 cw;
-                if (src) {
-                    cw = __ldcs(reinterpret_cast<const uint4*>(a.q2 + j * a.ldq + kv * 16));
-                } else {  // rare: re-derive 16 codes from the strided W column
-                    uint32_t b[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int64_t k = kv * 16 + e;
-                        const int c = (k < K && !bit_of(a.mask, k))
-                                          ? code_fast(__half2float(a.w[k * a.ldw + j]), s32, s) : 0;
-                        b[e] = static_cast<uint32_t>(c) & 0xFFu;
-                    }
-                    cw = make_uint4(b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24,
-                                    b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24,
-                                    b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24,
-                                    b[12] | b[13] << 8 | b[14] << 16 | b[15] << 24);
-                }
-                // predicated (branch-free) loads: all rows' bytes in flight at once
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint4 xv[8];
-#pragma unroll
-                    for (int mm = 0; mm < 8; ++mm) {
-                        const int64_t m = m0 + h * 8 + mm;
-                        xv[mm] = m < M ? __ldcg(reinterpret_cast<const uint4*>(a.xq + m * a.ldq + kv * 16))
-                                       : make_uint4(0u, 0u, 0u, 0u);
-                    }
-#pragma unroll
-                    for (int mm = 0; mm < 8; ++mm) {
-                        int& ac = acc[h * 8 + mm];
-                        ac = __dp4a(static_cast<int>(xv[mm].x), static_cast<int>(cw.x), ac);
-                        ac = __dp4a(static_cast<int>(xv[mm].y), static_cast<int>(cw.y), ac);
-                        ac = __dp4a(static_cast<int>(xv[mm].z), static_cast<int>(cw.z), ac);
-                        ac = __dp4a(static_cast<int>(xv[mm].w), static_cast<int>(cw.w), ac);
-                    }
-                }
-            }
-            if (threadIdx.x == 0 && li == 0 && m0 == 0) DSTAMP(p.dbg, 10);
-#pragma unroll
-            for (int mm = 0; mm < 16; ++mm) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc[mm] += __shfl_xor_sync(0xffffffffu, acc[mm], o);
-                if (lane == 0) bars->red[mm * NWARPS + warp] = acc[mm];
-            }
-            __syncthreads();
-            if (threadIdx.x < 16 && m0 + threadIdx.x < M) {
-                const int64_t m = m0 + threadIdx.x;
-                int32_t c = 0;
-#pragma unroll
-                for (int w = 0; w < NWARPS; ++w) c += bars->red[threadIdx.x * NWARPS + w];
-                const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
-                float wr[WO_CAP];
-#pragma unroll
-                for (int o = 0; o < WO_CAP; ++o)
-                    wr[o] = (EPI != EPI_F32_EXACT && o < n_out && n_out <= WO_CAP)
-                                ? __half2float(a.w[static_cast<int64_t>(bars->o_s[o]) * a.ldw + j])
-                                : 0.0f;
-                store_out<EPI>(a, m, j, epi_value<EPI>(a, c, m, j, srow[m], colf, aw, n_out, sxo, wr));
-            }
-            __syncthreads();
-        }
-    }
-    // patched columns read L2/HBM with a few dependent round trips: keep the
-    // weight streams of all CTAs paused until they are done (one more grid
-    // barrier, only when the call has patched columns at all)
-
+    for (int64_t w = w0 + tid; w < w1; w += THREADS) smask[w] = 0u;
+    cluster_arrive_relaxed();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (threadIdx.x == 0) DSTAMP(p.dbg, 9);
     const uint32_t tmem_base = bars->tmem_slot;
+    // X and the workspace (written / read by the preceding kernels) after the wait
+    pdl_wait();
+    pdl_trigger();
+    DSTAMP(p.dbg, 1);
+
+    // ================= T1: X slice, outlier bits, row partials -> every rank
+    const uint32_t thr = a.thr_bits_dev != nullptr ? __ldcg(a.thr_bits_dev) : a.thr_bits;
+    const bool bulk = cached && a.x_vec;
+    if (bulk && tid == 0) {
+        const uint32_t row_bytes = static_cast<uint32_t>(nfull) * 16u;
+        if (row_bytes > 0) {
+            mbar_arrive_expect_tx(&bars->xbar, row_bytes * static_cast<uint32_t>(M));
+            for (int64_t m = 0; m < M; ++m) bulk_load_1d(xs + m * xs_ld, a.x + m * a.ldx + c0, row_bytes, &bars->xbar);
+        } else {
+            mbar_arrive(&bars->xbar);
+        }
+    }
+    if (bulk && nv > nfull)  // ragged last vector (K % 8 != 0): element loads
+        for (int64_t m = tid; m < M; m += THREADS)
+            *reinterpret_cast<uint4*>(xs + m * xs_ld + nfull * 8) = load8(a.x + m * a.ldx, c0 + nfull * 8, K, false);
+    __syncthreads();
+    if (bulk) mbar_wait(&bars->xbar, 0);
+    DSTAMP(p.dbg, 2);
+    uint32_t nf = 0;
+    for (int i = tid; i < static_cast<int>(M) * nv; i += THREADS) {
+        const int m = i / nv, v = i - m * nv;
+        uint4 q;
+        if (bulk) {
+            q = *reinterpret_cast<const uint4*>(xs + m * xs_ld + v * 8);
+        } else {
+            q = load8(a.x + m * a.ldx, c0 + v * 8, K, a.x_vec);
+            if (cached) *reinterpret_cast<uint4*>(xs + m * xs_ld + v * 8) = q;
+        }
+        uint32_t fl = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t h = half_bits(q, e);
+            fl |= ((h & 0x7FFFu) >= thr ? 1u : 0u) << e;
+            nf |= (h & 0x7C00u) == 0x7C00u ? 1u : 0u;
+        }
+        if (fl) atomicOr(smask + w0 + (v >> 2), fl << ((v & 3) * 8));
+    }
+    if (tid == 0) DSTAMP(p.dbg, 10);
+    nf = __syncthreads_or(nf);
+    cluster_wait();  // every peer is running: its shared memory can be written
+    if (tid == 0) DSTAMP(p.dbg, 11);
+    for (int m = warp; m < static_cast<int>(M); m += NWARPS) {  // warp per row
+        uint32_t mx = 0;
+        for (int v = lane; v < nv; v += 32) {
+            const uint4 q = cached ? *reinterpret_cast<const uint4*>(xs + m * xs_ld + v * 8)
+                                   : load8(a.x + m * a.ldx, c0 + v * 8, K, a.x_vec);
+            const uint32_t mb = smask[w0 + (v >> 2)] >> ((v & 3) * 8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (!((mb >> e) & 1u)) mx = max(mx, half_bits(q, e) & 0x7FFFu);
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        if (lane < CL) st_cluster_u32(mapa_shared(spart + crank * MAX_M + m, lane), mx);
+    }
+    if (tid == 0) DSTAMP(p.dbg, 12);
+    const int nown = static_cast<int>(w1 - w0);
+    for (int i = tid; i < nown * CL; i += THREADS) {
+        const int q = i / nown, w = static_cast<int>(w0) + (i - q * nown);
+        if (q != static_cast<int>(crank)) st_cluster_u32(mapa_shared(smask + w, q), smask[w]);
+    }
+    if (tid == 0) st_cluster_u32(mapa_shared(&bars->nonfinite[crank], 0), nf);
+    if (tid == 0) DSTAMP(p.dbg, 13);
+    cluster_sync_all();  // 1: full mask and all partials in every rank
+    DSTAMP(p.dbg, 3);
+
+    // ================= T2: row scales, outlier list, codes -> every rank's panel
+    const bool lead = clu == 0;  // cluster 0 also publishes the call's token-side results
+    for (int m = tid; m < static_cast<int>(M); m += THREADS) {
+        uint32_t mx = 0;
+#pragma unroll
+        for (int q = 0; q < CL; ++q) mx = max(mx, spart[q * MAX_M + m]);
+        const float amax = hbits_to_float(mx);
+        const double s = scale_of(amax);
+        sscale[m] = s;
+        sscale32[m] = static_cast<float>(s);
+        samax[m] = amax;
+        srow[m] = amax_or_127(amax);
+        if (lead && crank == 0) {
+            a.row_amax[m] = amax;
+            a.ramax_bits[m] = mx;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) DSTAMP(p.dbg, 14);
+    const int nkb = kb_hi - kb_lo;
+    for (int it = tid; it < nkb * static_cast<int>(M) * 8; it += THREADS) {
+        const int kbi = it / (static_cast<int>(M) * 8);
+        const int rem = it - kbi * static_cast<int>(M) * 8;
+        const int m = rem >> 3, ch = rem & 7;
+        const int kb = kb_lo + kbi;
+        const int64_t k0 = static_cast<int64_t>(kb) * BK + ch * 16;
+        uint4 code = make_uint4(0u, 0u, 0u, 0u);
+        if (k0 < K && !(kDevStamps && (p.dbg_mode & 2))) {
+            uint4 lo, hi;
+            if (cached) {
+                lo = *reinterpret_cast<const uint4*>(xs + m * xs_ld + (k0 - c0));
+                hi = *reinterpret_cast<const uint4*>(xs + m * xs_ld + (k0 - c0) + 8);
+            } else {
+                lo = load8(a.x + m * a.ldx, k0, K, a.x_vec);
+                hi = load8(a.x + m * a.ldx, k0 + 8, K, a.x_vec);
+            }
+            const uint32_t mbits = (smask[k0 >> 5] >> (k0 & 31)) & 0xFFFFu;
+            code = codes16(lo, hi, mbits, k0, K, sscale32[m], sscale[m]);
+            if (lead) *reinterpret_cast<uint4*>(a.xq + m * a.ldq + k0) = code;  // workspace Xq (views)
+        }
+        const uint32_t off = static_cast<uint32_t>(m * BK + ((ch ^ (m & 7)) * 16));
+#pragma unroll
+        for (int q = 0; q < CL; ++q) {
+            const int len = bars->peer_len[q];
+            int slot;
+            if (len >= num_kb) {
+                slot = kb;
+            } else {
+                slot = kb - bars->peer_start[q];
+                if (slot < 0) slot += num_kb;
+                if (slot >= len) continue;
+            }
+            if (kDevStamps && (p.dbg_mode & 1))
+                *reinterpret_cast<uint4*>(panel + static_cast<size_t>(slot) * B_BYTES + off) = code;
+            else
+                st_cluster_v4(mapa_shared(panel + static_cast<size_t>(slot) * B_BYTES + off, q), code);
+        }
+    }
+    if (tid == 0) DSTAMP(p.dbg, 15);
+    asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");  // panels feed tcgen05.mma
+    if (tid == 0) DSTAMP(p.dbg, 16);
+    compact_mask(smask, nwords, bars, lead && crank == 0 ? a.o_idx : nullptr);
+    if (tid == 0) DSTAMP(p.dbg, 17);
+    if (lead) {
+        for (int64_t w = w0 + tid; w < w1; w += THREADS) a.mask[w] = smask[w];
+        if (crank == CL - 1) {  // Xq padding columns K..ldq (whole 16-column chunks)
+            const int64_t pad0 = (K + 15) / 16 * 16;
+            for (int64_t i = tid; i < M * ((a.ldq - pad0) / 16); i += THREADS) {
+                const int64_t per = (a.ldq - pad0) / 16;
+                *reinterpret_cast<uint4*>(a.xq + (i / per) * a.ldq + pad0 + (i % per) * 16) = make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
+    }
+    if (tid == 0) DSTAMP(p.dbg, 18);
+    cluster_sync_all();  // 2: every panel complete; the X slice area becomes weight stages
+    fence_proxy_async_smem();
+    if (lead && crank == 0 && tid == 0) {
+        *a.o_count = bars->n_out;
+        uint32_t any = 0;
+        for (int q = 0; q < CL; ++q) any |= bars->nonfinite[q];
+        if (a.nonfinite != nullptr) *a.nonfinite = any ? 1 : 0;
+    }
+    const int n_out = bars->n_out;
+    const int n_o = n_out <= WO_CAP ? n_out : 0;  // x[:, O] factors staged in smem
+    DSTAMP(p.dbg, 4);
 
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer: the remaining weight tiles
         if (lane == 0) {
             const uint64_t pol_w = l2_policy_evict_normal();
-            const uint64_t pol_x = l2_policy_evict_last();
-            for (int i = 0; i < n_pre; ++i) {  // token halves of the prefilled stages
+            for (int i = min(p.pre, L); i < L; ++i) {
                 const int u = u_begin + i;
-                tma_load_2d(&tmap_x, &bars->full[i], ring + static_cast<size_t>(i) * stage_bytes + A_BYTES,
-                            (u % num_kb) * BK, 0, pol_x);
-            }
-            int stage = n_pre % p.stages;
-            uint32_t phase = n_pre == p.stages ? 1u : 0u;
-            int pt_groups = -1;  // patch tile: gathered 4-row groups (set at its first unit)
-            bool pt_rest = false;  // rows >= PT_GATHER_ROWS present (box load from pq)
-            uint32_t pt_pq = 0;  // bit g: group g is gathered from pq
-            for (int u = u_begin + n_pre; u < u_end; ++u) {
-                const int tile = u / num_kb;
-                const int kb = u - tile * num_kb;
-                mbar_wait(&bars->empty[stage], phase ^ 1u);
-                uint8_t* dst = ring + static_cast<size_t>(stage) * stage_bytes;
-                if (tile < p.n_tiles) {
-                    mbar_arrive_expect_tx(&bars->full[stage], stage_bytes);
-                    tma_load_2d(&tmap_w, &bars->full[stage], dst, kb * BK, tile * TILE_N, pol_w);
-                } else {
-                    // the patch tile: row r = patched column p_idx[r]; groups of 4 rows
-                    // are gathered (tile::gather4) from the cached q2 rows, or from pq
-                    // when a group holds a re-derived row (its q2-sourced rows are then
-                    // copied to pq after the barrier, each published with a ready flag)
-                    if (pt_groups < 0) {
-                        // one round trip: the count and the first rows' column / source
-                        // (entries past the count are ignored)
-                        int32_t pr[PT_GATHER_ROWS], ps[PT_GATHER_ROWS];
-                        const int np_raw = __ldcg(a.p_count);
-#pragma unroll
-                        for (int r = 0; r < PT_GATHER_ROWS; ++r) {
-                            pr[r] = __ldcg(a.p_idx + r);
-                            ps[r] = __ldcg(a.p_src + r);
-                        }
-                        const int np = min(np_raw, PATCH_ROWS);
-                        pt_rest = np > PT_GATHER_ROWS;
-                        pt_groups = (min(np, PT_GATHER_ROWS) + 3) / 4;
-                        bool waited = false;
-                        for (int g = 0; g < pt_groups; ++g) {
-                            int n0 = 0;
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const int r = 4 * g + i;
-                                if (r < np) {
-                                    bars->pt_rows[r] = pr[r];
-                                    n0 += ps[r] == 0 ? 1 : 0;
-                                }
-                            }
-                            for (int r = np; r < 4 * g + 4; ++r) bars->pt_rows[r] = bars->pt_rows[4 * g];
-                            if (n0 > 0) {
-                                pt_pq |= 1u << g;
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    const int r = 4 * g + i;
-                                    if (r < np && ps[r] != 0)
-                                        while (ld_acquire(a.pq_ready + r) == 0) {
-                                        }
-                                }
-                                waited = true;
-                            }
-                        }
-                        if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
-                    }
-                    mbar_arrive_expect_tx(&bars->full[stage], static_cast<uint32_t>(pt_groups) * 4u * BK + p.b_bytes +
-                                                                  (pt_rest ? static_cast<uint32_t>(PATCH_ROWS - PT_GATHER_ROWS) * BK : 0u));
-                    if (pt_rest)  // rows PT_GATHER_ROWS.. : copied to pq in P2 (many patches)
-                        tma_load_2d(&tmap_pb, &bars->full[stage], dst + PT_GATHER_ROWS * BK, kb * BK, 0, pol_x);
-                    for (int g = 0; g < pt_groups; ++g) {
-                        uint8_t* gd = dst + g * 4 * BK;
-                        if ((pt_pq >> g) & 1u)
-                            tma_gather4(&tmap_p, &bars->full[stage], gd, kb * BK, 4 * g, 4 * g + 1, 4 * g + 2, 4 * g + 3);
-                        else
-                            tma_gather4(&tmap_q2, &bars->full[stage], gd, kb * BK, bars->pt_rows[4 * g],
-                                        bars->pt_rows[4 * g + 1], bars->pt_rows[4 * g + 2], bars->pt_rows[4 * g + 3]);
-                    }
-                }
-                tma_load_2d(&tmap_x, &bars->full[stage], dst + A_BYTES, kb * BK, 0, pol_x);
-                if (++stage == p.stages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
+                const int s = i % S2;
+                if (i >= S2) mbar_wait(&bars->empty[s], ((i / S2) & 1) ^ 1u);
+                mbar_arrive_expect_tx(&bars->full[s], A_BYTES);
+                tma_load_2d(&tmap_w, &bars->full[s], ring + static_cast<size_t>(s) * A_BYTES, (u % num_kb) * BK,
+                            (u / num_kb) * TILE_N, pol_w);
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
-        const uint32_t idesc = idesc_i8(TILE_N, static_cast<uint32_t>(p.mpad));
-        int stage = 0;
-        uint32_t phase = 0;
+        const uint32_t idesc = idesc_i8(TILE_N, MPAD);
         int seg = 0;
         for (int u = u_begin; u < u_end; ++seg) {
             const int tile = u / num_kb;
@@ -800,200 +619,318 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int acc = seg & 1;
             mbar_wait(&bars->tmem_empty[acc], ((seg >> 1) & 1) ^ 1u);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * 256);
+            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * N_ACC * MPAD);
             for (int kk = 0; u < seg_end; ++u, ++kk) {
-                mbar_wait(&bars->full[stage], phase);
+                const int i = u - u_begin, s = i % S2;
+                mbar_wait(&bars->full[s], (i / S2) & 1);
                 tc_fence_after();
                 if (lane == 0 && u == u_begin) DSTAMP(p.dbg, 5);
-                if (lane == 0 && u == u_end - 1) DSTAMP(p.dbg, 14);  // last unit's operands landed
                 if (lane == 0) {
-                    const uint32_t a0 = smem_addr(ring + static_cast<size_t>(stage) * stage_bytes);
-                    const uint32_t b0 = a0 + A_BYTES;
-                    // K-steps rotate over n_acc independent accumulators (the
-                    // epilogue adds them back, exact int32)
+                    const int slot = all_kb ? u % num_kb : i;
+                    const uint32_t a0 = smem_addr(ring + static_cast<size_t>(s) * A_BYTES);
+                    const uint32_t b0 = smem_addr(panel + static_cast<size_t>(slot) * B_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK / UMMA_K; ++k)
-                        mma_i8(d_tmem + static_cast<uint32_t>((k % p.n_acc) * p.mpad),
-                               smem_desc_k_sw128(a0 + k * UMMA_K), smem_desc_k_sw128(b0 + k * UMMA_K),
-                               idesc, (kk > 0 || k >= p.n_acc) ? 1u : 0u);
-                    mma_commit(&bars->empty[stage]);
+                        mma_i8(d_tmem + static_cast<uint32_t>(k * MPAD), smem_desc_k_sw128(a0 + k * UMMA_K),
+                               smem_desc_k_sw128(b0 + k * UMMA_K), idesc, kk > 0 ? 1u : 0u);
+                    mma_commit(&bars->empty[s]);
                 }
                 __syncwarp();
-                if (++stage == p.stages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
             }
             if (lane == 0) mma_commit(&bars->tmem_full[acc]);
             __syncwarp();
         }
         if (lane == 0) DSTAMP(p.dbg, 6);
-    } else {
-        if (warp == 2 || warp == 3) {
-            // ---------------- rare: a q2-sourced patch row whose 4-row group also holds
-            // a re-derived row must be in pq too (the group is gathered from pq)
-            const int t64 = threadIdx.x - 64;
-            const int np = min(__ldcg(a.p_count), PATCH_ROWS);
-            for (int li = 0; li < bars->n_local; ++li) {
-                const int pidx = bars->local_p[li];
-                if (pidx >= PT_GATHER_ROWS || !bars->local_src[li]) continue;
-                bool mixed = false;
-                for (int r = pidx & ~3; r < min((pidx & ~3) + 4, np); ++r) mixed |= __ldcg(a.p_src + r) == 0;
-                if (!mixed) continue;
-                const int64_t j = bars->local_j[li];
-                const uint4* srcq = reinterpret_cast<const uint4*>(a.q2 + j * a.ldq);
-                uint4* dst = reinterpret_cast<uint4*>(a.pq + static_cast<int64_t>(pidx) * a.ldq);
-                for (int64_t v = t64; v < a.ldq / 16; v += 64) dst[v] = __ldcs(srcq + v);
-                __threadfence();
-                named_bar_sync(3, 64);
-                if (t64 == 0) st_release(a.pq_ready + pidx, 1);
-            }
-        } else if (warp >= 4) {
-            // ---------------- epilogue: thread = weight row n of the tile
-            const int np_all = __ldcg(a.p_count);  // final after barrier 2
-            const int quad = warp & 3;
-            const int n_local = quad * 32 + lane;
-            const int chunks = p.mpad / 16;
-            int seg = 0;
-            for (int u = u_begin; u < u_end; ++seg) {
-                const int tile = u / num_kb;
-                const int seg_end = min(u_end, (tile + 1) * num_kb);
-                const int len = static_cast<int>(seg_end - u);
-                const bool full = len == num_kb;
-                u = seg_end;
-                const int acc = seg & 1;
-                int64_t n;
-                bool n_ok;
-                int32_t pp;
-                float aw;
-                if (tile < p.n_tiles) {
-                    n = tile * TILE_N + n_local;
-                    n_ok = n < N;
-                    pp = n_ok ? __ldcg(a.patch_pos + n) : 0;  // patched: written by the patch tile
-                    aw = n_ok ? a.amax_full[n] : 127.0f;
-                } else {  // patch tile: row n_local is patched column p_idx[n_local]
-                    n_ok = n_local < min(np_all, PATCH_ROWS);
-                    n = n_ok ? __ldcg(a.p_idx + n_local) : 0;
-                    pp = 0;
-                    aw = n_ok ? __ldcg(a.p_amax + n_local) : 127.0f;
-                }
-                const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
-                float wr[WO_CAP];
-#pragma unroll
-                for (int o = 0; o < WO_CAP; ++o) {
-                    float wv = 0.0f;
-                    if (EPI != EPI_F32_EXACT && o < n_out && n_out <= WO_CAP && n_ok)
-                        wv = __half2float(a.w[static_cast<int64_t>(bars->o_s[o]) * a.ldw + n]);
-                    wr[o] = wv;
-                }
-                mbar_wait(&bars->tmem_full[acc], (seg >> 1) & 1);
-                tc_fence_after();
-                const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                                       static_cast<uint32_t>(acc * 256);
-                bool finisher = full;
-                if (!full) {
-                    // partial sums: plain coalesced stores into this CTA's slot
-                    // (slot 0 = its first segment, 1 = its last), no atomics
-                    int32_t* slot = a.c32 + (blockIdx.x * 2 + (seg == 0 ? 0 : 1)) * (M * TILE_N) + n_local;
-                    for (int ch = 0; ch < chunks; ++ch) {
-                        uint32_t r[16];
-                        tmem_row16(t_row + ch * 16, p.n_acc, p.mpad, r);
-#pragma unroll
-                        for (int jj = 0; jj < 16; ++jj)
-                            if (ch * 16 + jj < M) __stcg(slot + (ch * 16 + jj) * TILE_N, static_cast<int32_t>(r[jj]));
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
-                    __threadfence();
-                    named_bar_sync(1, 128);
-                    if (threadIdx.x == 128) {
-                        bars->finisher = atomicAdd(a.tile_cnt + tile, len) + len == num_kb ? 1 : 0;
-                        __threadfence();
-                    }
-                    named_bar_sync(1, 128);
-                    finisher = bars->finisher != 0;
-                    named_bar_sync(1, 128);
-                    if (finisher) __threadfence();
-                }
-                if (full) {
-                    for (int ch = 0; ch < chunks; ++ch) {
-                        uint32_t r[16];
-                        tmem_row16(t_row + ch * 16, p.n_acc, p.mpad, r);
-                        if (!n_ok || pp) continue;  // patched columns: written by their dot products
-#pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) {
-                            const int64_t m = ch * 16 + jj;
-                            if (m >= M) break;
-                            store_out<EPI>(a, m, n, epi_value<EPI>(a, static_cast<int32_t>(r[jj]), m, n,
-                                                                  srow[m], colf, aw, n_out, sxo, wr));
-                        }
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
-                } else if (finisher && n_ok && !pp) {
-                    // contributors: the CTAs whose unit ranges intersect this tile
-                    const uint32_t t0 = static_cast<uint32_t>(tile * num_kb), t1 = t0 + num_kb;
-                    const uint32_t cf = ((t0 + 1) * Gu - 1) / T;
-                    const uint32_t cl = (t1 * Gu - 1) / T;
-                    for (int64_t m0 = 0; m0 < M; m0 += 16) {
-                        int32_t cv[16];
-#pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) cv[jj] = 0;
-                        for (uint32_t c = cf; c <= cl; ++c) {
-                            const int first_tile = static_cast<int>(T * c / Gu) / num_kb;
-                            const int32_t* src = a.c32 + (static_cast<int64_t>(c) * 2 + (first_tile == tile ? 0 : 1)) * (M * TILE_N) + n_local;
-#pragma unroll
-                            for (int jj = 0; jj < 16; ++jj)
-                                if (m0 + jj < M) cv[jj] += __ldcg(src + (m0 + jj) * TILE_N);
-                        }
-#pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) {
-                            const int64_t m = m0 + jj;
-                            if (m >= M) break;
-                            store_out<EPI>(a, m, n, epi_value<EPI>(a, cv[jj], m, n, srow[m], colf, aw,
-                                                                  n_out, sxo, wr));
-                        }
-                    }
-                }
-            }
-            if (threadIdx.x == 128) DSTAMP(p.dbg, 7);
+    } else if (warp >= 4) {
+        // ---------------- epilogue: thread = weight row n of the tile
+        const int et = tid - 128;
+        const int n_local = et;
+        const int quad = warp & 3;
+        for (int i = et; i < static_cast<int>(M) * n_o; i += 128) {
+            const int m = i / n_o, o = i - m * n_o;
+            sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
         }
+        int seg = 0;
+        for (int u = u_begin; u < u_end; ++seg) {
+            const int tile = u / num_kb;
+            const int su0 = u;
+            const int seg_end = min(u_end, (tile + 1) * num_kb);
+            const bool full = seg_end - u == num_kb;
+            u = seg_end;
+            const int acc = seg & 1;
+            const int64_t n = static_cast<int64_t>(tile) * TILE_N + n_local;
+            const bool n_ok = n < N;
+            int32_t c0r;
+            float aw;
+            if (seg < NSEG_PRE) {
+                c0r = seg == 0 ? pre_cr[0] : seg == 1 ? pre_cr[1] : pre_cr[2];
+                aw = seg == 0 ? pre_aw[0] : seg == 1 ? pre_aw[1] : pre_aw[2];
+            } else {
+                c0r = n_ok ? __ldg(a.cand_r + n) : -1;
+                aw = n_ok ? __ldg(a.amax_full + n) : 127.0f;
+            }
+            float wr[WO_CAP];
+#pragma unroll
+            for (int o = 0; o < WO_CAP; ++o)
+                wr[o] = (EPI != EPI_F32_EXACT && o < n_o && n_ok)
+                            ? __half2float(a.w[static_cast<int64_t>(bars->o_s[o]) * a.ldw + n]) : 0.0f;
+            // -- column fixup: patched when the cached maximiser row is an outlier row
+            //    and the keep-row amax differs (weights.cu fixup_kernel semantics)
+            if (et == 0) bars->n_ent = 0;
+            bars->ent_of[n_local] = -1;
+            named_bar_sync(1, 128);
+            if (n_ok && c0r >= 0 && bit_of(smask, c0r)) {
+                int32_t cr[kTopT];
+                uint16_t cv[kTopT];
+#pragma unroll
+                for (int t = 1; t < kTopT; ++t) {
+                    cr[t] = __ldg(a.cand_r + t * N + n);
+                    cv[t] = __ldg(a.cand_v + t * N + n);
+                }
+                int src;
+                const float a_new = fixup_amax(cr, cv, smask, src);
+                if (a_new < 0.0f || a_new != aw) {
+                    const int e = atomicAdd(&bars->n_ent, 1);
+                    bars->ent_j[e] = n_local;
+                    bars->ent_a[e] = a_new;
+                    bars->ent_src[e] = a_new < 0.0f ? -1 : src;
+                }
+            }
+            named_bar_sync(1, 128);
+            const int n_ent = bars->n_ent;
+            if (n_ent > 0) {
+                // every cached candidate an outlier row (rare): scan the column, warp per entry
+                for (int e = quad; e < n_ent; e += 4) {
+                    if (bars->ent_src[e] != -1) continue;
+                    const int64_t j = static_cast<int64_t>(tile) * TILE_N + bars->ent_j[e];
+                    uint32_t mx = 0;
+                    for (int64_t k = lane; k < K; k += 32)
+                        if (!bit_of(smask, k))
+                            mx = max(mx, static_cast<uint32_t>(__half_as_ushort(a.w[k * a.ldw + j])) & 0x7FFFu);
+#pragma unroll
+                    for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+                    if (lane == 0) {
+                        const float an = hbits_to_float(mx);
+                        bars->ent_a[e] = an;
+                        bars->ent_src[e] = an != __ldg(a.amax_full + j) ? 0 : -2;
+                    }
+                }
+                named_bar_sync(1, 128);
+                for (int e = et; e < n_ent; e += 128)
+                    if (bars->ent_src[e] >= 0) bars->ent_of[bars->ent_j[e]] = e;
+                // exact int32 dots of the patched columns' codes with this segment's
+                // panel codes (all 128 threads per column, on CUDA cores)
+                const int nch = (seg_end - su0) * 8;
+                for (int e = 0; e < n_ent; ++e) {
+                    const int src = bars->ent_src[e];
+                    if (src < 0) continue;
+                    const int64_t j = static_cast<int64_t>(tile) * TILE_N + bars->ent_j[e];
+                    const double sc = scale_of(bars->ent_a[e]);
+                    const float s32 = static_cast<float>(sc);
+                    int accd[MAX_M];
+#pragma unroll
+                    for (int m = 0; m < MAX_M; ++m) accd[m] = 0;
+                    for (int c = et; c < nch; c += 128) {
+                        const int uu = su0 + (c >> 3), ch = c & 7;
+                        const int kb = uu % num_kb;
+                        const int64_t k = static_cast<int64_t>(kb) * BK + ch * 16;
+                        const int slot = all_kb ? kb : uu - u_begin;
+                        uint4 cw;
+                        if (src == 1) {
+                            cw = __ldg(reinterpret_cast<const uint4*>(a.q2 + j * a.ldq + k));
+                        } else {  // re-derived from W's column (its top-2 rows are outlier rows)
+                            uint32_t b[16];
+#pragma unroll
+                            for (int e2 = 0; e2 < 16; ++e2) {
+                                const int64_t kk = k + e2;
+                                const int cd = (kk < K && !bit_of(smask, kk))
+                                                   ? code_fast(__half2float(a.w[kk * a.ldw + j]), s32, sc) : 0;
+                                b[e2] = static_cast<uint32_t>(cd) & 0xFFu;
+                            }
+                            cw = make_uint4(b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24,
+                                            b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24,
+                                            b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24,
+                                            b[12] | b[13] << 8 | b[14] << 16 | b[15] << 24);
+                        }
+                        const uint8_t* ps = panel + static_cast<size_t>(slot) * B_BYTES;
+#pragma unroll
+                        for (int m = 0; m < MAX_M; ++m) {
+                            if (m >= M) break;
+                            const uint4 xv = *reinterpret_cast<const uint4*>(ps + m * BK + ((ch ^ (m & 7)) * 16));
+                            accd[m] = __dp4a(static_cast<int>(xv.x), static_cast<int>(cw.x), accd[m]);
+                            accd[m] = __dp4a(static_cast<int>(xv.y), static_cast<int>(cw.y), accd[m]);
+                            accd[m] = __dp4a(static_cast<int>(xv.z), static_cast<int>(cw.z), accd[m]);
+                            accd[m] = __dp4a(static_cast<int>(xv.w), static_cast<int>(cw.w), accd[m]);
+                        }
+                    }
+#pragma unroll
+                    for (int m = 0; m < MAX_M; ++m) {
+#pragma unroll
+                        for (int d = 16; d > 0; d >>= 1) accd[m] += __shfl_xor_sync(0xffffffffu, accd[m], d);
+                        if (lane == 0) bars->red[quad * MAX_M + m] = accd[m];
+                    }
+                    named_bar_sync(1, 128);
+                    if (et < MAX_M)
+                        pdot[e * MAX_M + et] = bars->red[et] + bars->red[MAX_M + et] + bars->red[2 * MAX_M + et] +
+                                               bars->red[3 * MAX_M + et];
+                    named_bar_sync(1, 128);
+                }
+            }
+            const int my_ent = bars->ent_of[n_local];
+            if (my_ent >= 0) aw = bars->ent_a[my_ent];
+            const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
+            // split tile: the CTA holding its first unit finishes it (that unit range
+            // is its last segment, or its only one); the others are their first
+            // segments and hand over int32 partials
+            const uint32_t t0 = static_cast<uint32_t>(tile * num_kb), t1 = t0 + num_kb;
+            const uint32_t cf = ((t0 + 1) * Gu - 1) / T;
+            const uint32_t cl = (t1 * Gu - 1) / T;
+            mbar_wait(&bars->tmem_full[acc], (seg >> 1) & 1);
+            tc_fence_after();
+            if (et == 0 && seg == 0) DSTAMP(p.dbg, 7);
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                                   static_cast<uint32_t>(acc * N_ACC * MPAD);
+            uint32_t r[16];
+            tmem_row16(t_row, r);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
+            if (my_ent >= 0) {
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) r[jj] = static_cast<uint32_t>(pdot[my_ent * MAX_M + jj]);
+            }
+            if (!full && cf != blockIdx.x) {
+                int32_t* slotp = a.c32 + static_cast<int64_t>(blockIdx.x) * (MAX_M * TILE_N) + n_local;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                    if (jj < M) __stcg(slotp + jj * TILE_N, static_cast<int32_t>(r[jj]));
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (et == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.tile_cnt + tile) : "memory");
+                continue;
+            }
+            if (!full) {  // finisher: the other contributors' partials, then reset the counter
+                if (et == 0) {
+                    // bounded: a workspace whose counters were never zeroed traps
+                    // instead of hanging the GPU
+                    for (uint32_t spin = 0; ld_acquire(a.tile_cnt + tile) < static_cast<int>(cl - cf); ++spin)
+                        if (spin > (1u << 22)) __trap();
+                    a.tile_cnt[tile] = 0;
+                }
+                named_bar_sync(1, 128);
+                __threadfence();
+                for (uint32_t c = cf + 1; c <= cl; ++c) {
+                    const int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj)
+                        if (jj < M) r[jj] += static_cast<uint32_t>(__ldcg(src + jj * TILE_N));
+                }
+            }
+            if (n_ok) {
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    if (jj >= M) break;
+                    store_out<EPI>(a, jj, n, epi_value<EPI>(a, bars->o_s, smask, nwords, static_cast<int32_t>(r[jj]),
+                                                           jj, n, srow[jj], colf, aw, n_out, sxo, wr));
+                }
+            }
+        }
+        if (et == 0) DSTAMP(p.dbg, 8);
     }
+    tc_fence_before();
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
     }
-    if (threadIdx.x == 0) DSTAMP(p.dbg, 8);
+    DSTAMP(p.dbg, 9);
 }
 
 }  // namespace dec
 
 // ------------------------------------------------------------------ host
-int decode_stages(int64_t M) {
-    const int mpad = static_cast<int>((M + 15) / 16 * 16);
-    const int stage = dec::A_BYTES + mpad * dec::BK;
-    const size_t budget = 227 * 1024 - 1024 - dec::smem_extra();
-    int s = static_cast<int>(budget / stage);
-    if (s > dec::MAX_STAGES) s = dec::MAX_STAGES;
-    return s;
+namespace {
+struct DecodeGeom {
+    int grid, s1, s2, slots, xs_cached;
+    int64_t xs_ld, units;
+    size_t smem;
+    bool ok;
+};
+
+// active 8-CTA clusters of the decode kernel (one CTA per SM), measured once
+int decode_clusters() {
+    static int n = -1;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(dec::decode_kernel<EPI_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dec::SMEM_LIMIT);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(dec::CL * 64);
+        cfg.blockDim = dim3(dec::THREADS);
+        cfg.dynamicSmemBytes = dec::SMEM_LIMIT;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = dec::CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int c = 0;
+        if (cudaOccupancyMaxActiveClusters(&c, dec::decode_kernel<EPI_F16>, &cfg) != cudaSuccess) c = 0;
+        cudaGetLastError();
+        n = c > 0 ? c : num_sms() / dec::CL;
+    });
+    return n;
 }
 
-int decode_grid(int64_t K, int64_t N) {
-    const int64_t units = ((N + dec::TILE_N - 1) / dec::TILE_N + 1) * ((K + dec::BK - 1) / dec::BK);
-    return static_cast<int>(units < num_sms() ? units : num_sms());
-}
-
-bool decode_fits(int64_t M, int64_t K, int64_t N) {
-    if (M <= 0 || M > dec::MAX_M || K <= 0 || N <= 0) return false;
-    const int64_t G = decode_grid(K, N);
+DecodeGeom decode_geom(int64_t M, int64_t K, int64_t N) {
+    using namespace dec;
+    DecodeGeom g{};
+    g.ok = false;
+    if (M <= 0 || M > MAX_M || K <= 0 || N <= 0) return g;
     const int64_t nwords = (K + 31) / 32;
-    const int64_t wpc = (nwords + G - 1) / G;  // owned words per CTA (max)
-    return M * wpc * 32 * 2 <= static_cast<int64_t>(dec::SMEM_UNION) && wpc <= 64 &&
-           (N + G - 1) / G <= dec::LOCAL_CAP;
+    if (nwords > MAX_WORDS) return g;
+    const int64_t num_kb = (K + BK - 1) / BK;
+    const int64_t n_tiles = (N + TILE_N - 1) / TILE_N;
+    g.units = n_tiles * num_kb;
+    int64_t grid = static_cast<int64_t>(decode_clusters()) * CL;
+    const int64_t max_grid = (g.units / CL) * CL;  // every CTA gets at least one unit
+    if (grid > max_grid) grid = max_grid;
+    if (grid < CL) return g;
+    g.grid = static_cast<int>(grid);
+    if (g.units * grid >= (int64_t(1) << 31)) return g;
+    const int64_t per = (g.units + grid - 1) / grid;
+    g.slots = static_cast<int>(per < num_kb ? per : num_kb);
+    const int64_t kb_max = (num_kb + CL - 1) / CL;  // k-blocks per rank (max)
+    g.xs_ld = kb_max * BK;
+    static int env_kb = -2;
+    if (env_kb == -2) {
+        const char* e = getenv("I8MM_DECODE_SMEM_KB");
+        env_kb = (e && e[0]) ? atoi(e) : -1;
+    }
+    const size_t limit = env_kb > 0 ? static_cast<size_t>(env_kb) * 1024 : SMEM_LIMIT;
+    const size_t fixed = 1024 + static_cast<size_t>(g.slots) * B_BYTES + smem_tail(nwords);
+    if (fixed + 2 * A_BYTES > limit) return g;
+    int s2 = static_cast<int>((limit - fixed) / A_BYTES);
+    if (s2 > MAX_STAGES) s2 = MAX_STAGES;
+    const size_t xs_bytes = static_cast<size_t>(M * g.xs_ld) * 2;
+    const int xs_stages = static_cast<int>((xs_bytes + A_BYTES - 1) / A_BYTES);
+    // keep the X slice in the ring's last stages while T1/T2 run when at least
+    // two weight stages stay free for the prefetch; else T2 re-reads X
+    g.xs_cached = s2 - xs_stages >= 2 ? 1 : 0;
+    g.s2 = s2;
+    g.s1 = g.xs_cached ? s2 - xs_stages : s2;
+    g.smem = fixed + static_cast<size_t>(s2) * A_BYTES;
+    g.ok = true;
+    return g;
 }
+}  // namespace
+
+int decode_stages(int64_t M) { return decode_geom(M, 4096, 4096).s2; }
+
+int decode_grid(int64_t K, int64_t N) { return decode_geom(1, K, N).grid; }
+
+bool decode_fits(int64_t M, int64_t K, int64_t N) { return decode_geom(M, K, N).ok; }
 
 __global__ void set_word_kernel(uint32_t* dst, uint32_t value) { *dst = value; }
 
@@ -1003,46 +940,40 @@ cudaError_t launch_set_word(uint32_t* dst, uint32_t value, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// weight stages prefetched before the prologue (default 3: deeper prefetch
-// queues the prologue's latency-bound round trips behind the weight stream);
-// env I8MM_DECODE_PREFETCH for A/B measurements
-static int decode_prefetch() {
-    static int v = -2;
-    if (v == -2) {
-        const char* e = getenv("I8MM_DECODE_PREFETCH");
-        v = (e && e[0]) ? atoi(e) : -1;
-    }
-    return v;
-}
-
 static unsigned long long* g_dbg = nullptr;
 void set_decode_timeline(unsigned long long* stamps) { g_dbg = stamps; }
 unsigned long long* debug_timeline() { return g_dbg; }
 
+static int env_int_once(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : dflt;
+}
+
 template <int EPI>
-static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tp,
-                                const CUtensorMap& tq, const CUtensorMap& tb,
-                                const dec::Params& prm, size_t smem, int grid, cudaStream_t st) {
+static cudaError_t launch_decode_epi(const CUtensorMap& tw, const dec::Params& prm, const DecodeGeom& g,
+                                     cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(dec::decode_fused_kernel<EPI>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_err = cudaFuncSetAttribute(dec::decode_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        dec::SMEM_LIMIT);
     });
     if (attr_err != cudaSuccess) return attr_err;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.gridDim = dim3(static_cast<unsigned>(g.grid));
     cfg.blockDim = dim3(dec::THREADS);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = g.smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = dec::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, dec::decode_fused_kernel<EPI>, tw, tx, tp, tq, tb, prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, dec::decode_kernel<EPI>, tw, prm);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -1050,37 +981,30 @@ static cudaError_t launch_fused(const CUtensorMap& tw, const CUtensorMap& tx, co
 
 cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st) {
     using namespace dec;
-    if (!decode_fits(a.M, a.K, a.N)) return cudaErrorInvalidValue;
+    const DecodeGeom g = decode_geom(a.M, a.K, a.N);
+    if (!g.ok) return cudaErrorInvalidValue;
     Params prm{};
     prm.a = a;
-    prm.mpad = static_cast<int>((a.M + 15) / 16 * 16);
     prm.num_kb = static_cast<int>((a.K + BK - 1) / BK);
     prm.n_tiles = static_cast<int>((a.N + TILE_N - 1) / TILE_N);
-    prm.total_units = static_cast<int64_t>(prm.n_tiles + 1) * prm.num_kb;  // + the patch tile
-    prm.stages = decode_stages(a.M);
-    prm.b_bytes = static_cast<uint32_t>(prm.mpad * BK);
-    prm.n_acc = prm.mpad <= 64 ? 4 : (prm.mpad <= 128 ? 2 : 1);
-    const int pf = decode_prefetch() < 0 ? 3 : decode_prefetch();
-    prm.prefetch = pf < prm.stages ? pf : prm.stages;
+    prm.total_units = g.units;
+    prm.s1 = g.s1;
+    prm.s2 = g.s2;
+    // weight tiles prefetched before the token phase (env I8MM_DECODE_PREFETCH, A/B)
+    static const int env_pre = env_int_once("I8MM_DECODE_PREFETCH", -1);
+    prm.pre = env_pre >= 0 && env_pre < g.s1 ? env_pre : g.s1;
+    prm.slots = g.slots;
+    prm.xs_cached = g.xs_cached;
+    prm.xs_ld = g.xs_ld;
     prm.dbg = g_dbg;
-    CUtensorMap tw, tx, tp;
+    static const int env_dbg = env_int_once("I8MM_DECODE_DBG_MODE", 0);
+    prm.dbg_mode = env_dbg;
+    CUtensorMap tw;
     if (!make_tmap_i8_rows(&tw, a.wq_t, a.N, a.K, a.ldq, TILE_N)) return cudaErrorInvalidValue;
-    if (!make_tmap_i8_rows(&tx, a.xq, a.M, a.K, a.ldq, prm.mpad)) return cudaErrorInvalidValue;
-    // patch tile A rows: 1-row boxes for tile::gather4 from pq and from q2
-    CUtensorMap tq;
-    if (!make_tmap_i8_rows(&tp, a.pq, PATCH_ROWS, a.K, a.ldq, 1)) return cudaErrorInvalidValue;
-    if (!make_tmap_i8_rows(&tq, a.q2, a.N, a.K, a.ldq, 1)) return cudaErrorInvalidValue;
-    CUtensorMap tb;  // pq rows PT_GATHER_ROWS..PATCH_ROWS-1 as one box
-    if (!make_tmap_i8_rows(&tb, a.pq + PT_GATHER_ROWS * a.ldq, PATCH_ROWS - PT_GATHER_ROWS, a.K, a.ldq,
-                           PATCH_ROWS - PT_GATHER_ROWS))
-        return cudaErrorInvalidValue;
-    const size_t smem =
-        1024 + static_cast<size_t>(prm.stages) * (A_BYTES + prm.b_bytes) + smem_extra();
-    const int grid = decode_grid(a.K, a.N);
     switch (epi) {
-        case EPI_F16: return launch_fused<EPI_F16>(tw, tx, tp, tq, tb, prm, smem, grid, st);
-        case EPI_F32: return launch_fused<EPI_F32>(tw, tx, tp, tq, tb, prm, smem, grid, st);
-        case EPI_F32_EXACT: return launch_fused<EPI_F32_EXACT>(tw, tx, tp, tq, tb, prm, smem, grid, st);
+        case EPI_F16: return launch_decode_epi<EPI_F16>(tw, prm, g, st);
+        case EPI_F32: return launch_decode_epi<EPI_F32>(tw, prm, g, st);
+        case EPI_F32_EXACT: return launch_decode_epi<EPI_F32_EXACT>(tw, prm, g, st);
         default: return cudaErrorInvalidValue;
     }
 }

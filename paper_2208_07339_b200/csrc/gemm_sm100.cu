@@ -876,6 +876,22 @@ bool make_tmap_i8_rows(CUtensorMap* map, const int8_t* base, int64_t rows, int64
     return gemm::make_tmap_i8(map, base, rows, K, ld, box_rows);
 }
 
+// fp16 [rows x cols] (row pitch ld elements, 16-byte aligned), box = 128 columns
+// x box_rows rows, no swizzle (rows land 256 bytes apart); OOB elements read 0
+bool make_tmap_f16_rows(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                        int box_rows) {
+    gemm::EncodeTiledFn enc = gemm::get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    cuuint32_t box[2] = {128, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Kernel-variant overrides for tests / A-B measurements:
 //   I8MM_FORCE_CG1=1 pins the 1-CTA kernel; I8MM_GEMM_MC=2 enables the
 //   B-multicast cluster of two CTA pairs (M >= 2048).

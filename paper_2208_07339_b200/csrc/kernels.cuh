@@ -198,45 +198,32 @@ struct DecodeArgs {
     int x_vec;  // X rows 16-byte aligned (ldx % 8 == 0, base aligned)
     uint32_t thr_bits;
     const uint32_t* thr_bits_dev;  // nullable: threshold bits stored by i8mm_linear_prologue
-    uint32_t* part;       // [grid] x [M] per-CTA partial row absmax (fp16 bits)
-    uint32_t* mask;       // [ceil(K/32)]
+    int32_t* nonfinite;   // [1] X holds NaN/Inf (the reference's DenseMatrix(x) rejects it)
+    uint32_t* mask;       // [ceil(K/32)] outlier columns (published by cluster 0)
     int32_t* o_idx;       // [K]
     int32_t* o_count;     // [1]
     uint32_t* ramax_bits; // [M] row amax as fp16 bits
     float* row_amax;      // [M]
-    int8_t* xq;           // [M x ldq]
+    int8_t* xq;           // [M x ldq] codes (published by cluster 0)
     int64_t ldq;
-    __half* xo;           // [M x o_cap]
-    int64_t o_cap;
     const __half* w;      // K x N fp16 (resident)
     int64_t ldw;
-    int w_vec;
     const int8_t* wq_t;   // N x ldq cached codes
     const float* amax_full;
     const uint16_t* cand_v;
     const int32_t* cand_r;
-    __half* wo;           // [o_cap x ldwo]
-    int64_t ldwo;
-    int32_t* p_count;
-    int32_t* p_idx;
-    float* p_amax;
-    int32_t* patch_pos;   // [N]: 1 + patch index, 0 = not patched
     const int8_t* q2;     // N x ldq second-candidate codes (weight buffer)
-    int8_t* pq;           // [128 x ldq] A rows of the patch tile (codes of patched columns)
-    int32_t* c32;         // [2 x grid] x [M x 128] split-tile partial slots
-    int64_t c32_words;
-    int32_t* tile_cnt;    // [n_tiles + 1] (+ the patch tile)
-    int32_t* p_src;       // [N] per patch: 1 = its codes are the cached q2 row
-    int32_t* pq_ready;    // [128] pq row r holds a q2 row copied after barrier 2 (rare)
-    int64_t n_tiles;
+    int32_t* c32;         // [grid] x [16 x 128] split-tile partial slots
+    int32_t* tile_cnt;    // [n_tiles] arrival counters: zero on first use, reset by the finishers
     void* y;
     int64_t ldy;
 };
-constexpr int kDecodeMaxM = 256;
+constexpr int kDecodeMaxM = 16;  // decode_sm100.cu: the MMA N is 16 token rows
 int decode_stages(int64_t M);
 int decode_grid(int64_t K, int64_t N);
 bool decode_fits(int64_t M, int64_t K, int64_t N);
-// one cooperative launch: prologue + swap-AB stream-K GEMM + epilogue
+// one launch of 8-CTA clusters: token side in distributed shared memory, then the
+// swap-AB stream-K weight-stream GEMM + epilogue
 cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st);
 cudaError_t launch_set_word(uint32_t* dst, uint32_t value, cudaStream_t st);
 void set_decode_timeline(unsigned long long* stamps);

@@ -119,6 +119,7 @@ class Int8Linear(torch.nn.Module):
             self.bias = None
         self.wbuf = None
         self._last_ws = None
+        self._dws = {}  # decode-routed workspaces, one per (M, stream): their counters persist
         if self.weight_stationary:
             self._prepare()
 
@@ -134,6 +135,26 @@ class Int8Linear(torch.nn.Module):
                                         scratch.data_ptr(), scratch.numel(), stream_handle()),
                   "linear_prepare")
 
+    def workspace(self, m: int) -> torch.Tensor:
+        """A workspace for an M-row call. Prefill routing: a fresh buffer.
+        Decode routing: cached per (M, stream), initialised once
+        (``i8mm_linear_workspace_init``: its per-tile arrival counters must be
+        zero on first use; every decode call leaves them zero)."""
+        L = nat.lib()
+        k, n = self.weight.shape
+        if not self.uses_decode(m):
+            return torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8,
+                               device=self.weight.device)
+        key = (m, torch.cuda.current_stream(self.weight.device).cuda_stream)
+        ws = self._dws.get(key)
+        if ws is None:
+            ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8,
+                             device=self.weight.device)
+            nat.check(L.i8mm_linear_workspace_init(ws.data_ptr(), ws.numel(), m, k, n, stream_handle()),
+                      "linear_workspace_init")
+            self._dws[key] = ws
+        return ws
+
     def matmul(self, x2: torch.Tensor, exact: bool = False, _timer=None) -> torch.Tensor:
         """Y = x2 @ W for an M x K fp16 CUDA matrix (no bias)."""
         if not self.weight_stationary:
@@ -148,8 +169,7 @@ class Int8Linear(torch.nn.Module):
         if x2.shape[1] != k:
             raise ShapeMismatchError(f"inner dimensions differ: X is {m}x{x2.shape[1]}, W is {k}x{n}")
         kind, dt = _out_kind(self.out_dtype, exact)
-        ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8,
-                         device=x2.device)
+        ws = self.workspace(m)
         y = torch.empty((m, n), dtype=dt, device=x2.device)
         st = stream_handle()
         w = self.weight
@@ -204,7 +224,7 @@ class Int8Linear(torch.nn.Module):
         if x2.shape[1] != k:
             raise ShapeMismatchError(f"inner dimensions differ: X is {m}x{x2.shape[1]}, W is {k}x{n}")
         kind, dt = _out_kind(self.out_dtype, False)
-        ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8, device=x2.device)
+        ws = self.workspace(m)
         if y is None:
             y = torch.empty((m, n), dtype=dt, device=x2.device)
             ldy = n
@@ -232,6 +252,7 @@ class Int8Linear(torch.nn.Module):
 
         ws, m = self._last_ws
         k, n = self.weight.shape
+        self._patch_stats(ws, m)
         views = (ctypes.c_void_p * 8)()
         nat.check(nat.lib().i8mm_linear_workspace_views(ws.data_ptr(), m, k, n, views, 8))
         # read the two device counters through byte views of the workspace
@@ -254,6 +275,7 @@ class Int8Linear(torch.nn.Module):
         ws, m = self._last_ws
         k, n = self.weight.shape
         L = nat.lib()
+        self._patch_stats(ws, m)
         views = (ctypes.c_void_p * 8)()
         nat.check(L.i8mm_linear_workspace_views(ws.data_ptr(), m, k, n, views, 8))
         wv = (ctypes.c_void_p * 5)()
@@ -278,6 +300,14 @@ class Int8Linear(torch.nn.Module):
         return {"dims": dims, "xq": xq, "row_amax": row_amax, "col_amax": col_amax,
                 "patched_cols": pc}
 
+    def _patch_stats(self, ws: torch.Tensor, m: int) -> None:
+        """Decode-routed calls decide patched columns per tile without listing
+        them: recompute the list (p_count / p_idx / p_amax) for introspection."""
+        k, n = self.weight.shape
+        nat.check(nat.lib().i8mm_linear_patch_stats(self.weight.data_ptr(), self.weight.stride(0),
+                                                    self.wbuf.data_ptr(), m, k, n, ws.data_ptr(),
+                                                    ws.numel(), stream_handle()), "linear_patch_stats")
+
     @classmethod
     def from_linear(cls, lin: torch.nn.Linear, alpha: float = 6.0) -> "Int8Linear":
         return cls(lin.weight.detach().t(), alpha,
@@ -294,16 +324,15 @@ class Int8Linear(torch.nn.Module):
     def _raise_if_nonfinite(self, x2: torch.Tensor) -> None:
         """check_finite: the reference's DenseMatrix(x) rejects NaN/Inf
         (transformer.py:260, tensors.py:47-48). The prefill prologue's scan
-        raises a device flag on the way; decode-routed calls check X in one
-        small extra launch. One 4-byte host read; skipped under CUDA-graph
-        capture."""
+        and the decode prep kernel raise a device flag on the way. One 4-byte
+        host read; skipped under CUDA-graph capture."""
         if not self.check_finite or torch.cuda.is_current_stream_capturing():
             return
         if self._last_ws is None:
             return
         ws, m = self._last_ws
         k, n = self.weight.shape
-        if self.weight_stationary and not self.uses_decode(m):
+        if self.weight_stationary:
             import ctypes
 
             views = (ctypes.c_void_p * 8)()

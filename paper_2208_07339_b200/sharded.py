@@ -258,7 +258,7 @@ class ShardedInt8Linear(torch.nn.Module):
         L = nat.lib()
         lin = self.local
         n = self.hi - self.lo
-        ws = torch.empty(L.i8mm_linear_workspace_size(m, k, n), dtype=torch.uint8, device=x16.device)
+        ws = lin.workspace(m)
         y_loc = out[:, self.lo:self.hi]  # this rank's block, written in place (ldy = n_total)
         nat.check(L.i8mm_linear_forward_peers(
             x16.data_ptr(), x16.stride(0), m, lin.weight.data_ptr(), lin.weight.stride(0),

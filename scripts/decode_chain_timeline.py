@@ -1,0 +1,52 @@
+"""Per-layer timeline of one cfg3 decode step (dev tool): the six OPT-13B
+projections at M = 8 back to back, as bench.py --workload cfg3_decode runs them
+(eager, PDL-chained), with %globaltimer stamps of every layer's prep and stream
+kernels, relative to the first layer's prep start.
+
+    python scripts/decode_chain_timeline.py
+"""
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2208_07339_b200 import _native as nat, build as _build  # noqa: E402
+nat.load_library(_build.lib_path(devtools=True))
+import bench  # noqa: E402
+
+L = nat.lib()
+run = bench.WorkloadRun("cfg3_decode", "cuda", False)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+bufs = [torch.zeros(sms * 32, dtype=torch.int64, device="cuda") for _ in run.layers]
+for _ in range(5):
+    run.step()
+torch.cuda.synchronize()
+for mod, x, b in zip(run.mods, run.xs, bufs):
+    L.i8mm_debug_decode_timeline(b.data_ptr())
+    mod(x)
+L.i8mm_debug_decode_timeline(None)
+torch.cuda.synchronize()
+G = [b.view(sms, 32).cpu().double() for b in bufs]
+t0 = G[0][:, 0][G[0][:, 0] > 0].min()
+
+
+def stat(g, i, f=min):
+    v = g[:, i]
+    v = v[v > 0]
+    if v.numel() == 0:
+        return float("nan")
+    return float((f(v) - t0) / 1e3)
+
+
+names = ["q", "k", "v", "o", "fc1", "fc2"]
+cols = [(0, "start", min), (0, "start (last CTA)", max), (1, "waited", max), (2, "X landed", max),
+        (10, "flags", max), (11, "cluster wait", max), (12, "partials pushed", max), (13, "mask pushed", max),
+        (3, "cluster barrier 1", max), (14, "row scales", max), (15, "codes pushed", max), (16, "proxy fence", max),
+        (17, "o-list", max), (18, "lead writes", max), (4, "panels ready", max), (5, "1st MMA", max),
+        (6, "MMA issued", max), (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]
+print("us from layer q's prep start (min or max over CTAs)")
+print(f"{'':18s}" + "".join(f"{n:>8s}" for n in names))
+for i, lab, f in cols:
+    print(f"{lab:18s}" + "".join(f"{stat(g, i, f):8.2f}" for g in G))
