@@ -494,6 +494,7 @@ static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __h
     d.ldq = ws.ldq;
     d.w = w;
     d.ldw = ldw;
+    d.w_vec = (ldw % 8 == 0) && ((reinterpret_cast<uintptr_t>(w) & 15u) == 0);
     d.wq_t = b.wq_t;
     d.amax_full = b.col_amax;
     d.cand_v = b.cand_v;

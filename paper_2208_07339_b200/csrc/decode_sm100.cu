@@ -60,9 +60,12 @@ bool make_tmap_i8_rows(CUtensorMap* map, const int8_t* base, int64_t rows, int64
 
 namespace dec {
 
+#ifndef DECODE_CL
+#define DECODE_CL 8
+#endif
 constexpr int THREADS = 256;    // warp 0 TMA, 1 MMA, 2 TMEM alloc, 4-7 epilogue; all in T1/T2
 constexpr int NWARPS = THREADS / 32;
-constexpr int CL = 8;           // cluster size (portable)
+constexpr int CL = DECODE_CL;   // cluster size (portable)
 constexpr int WO_CAP = 16;      // outlier rows of W held in registers by the epilogue
 constexpr int TILE_N = 128;     // weight rows per tile (the MMA's M)
 constexpr int BK = 128;         // K bytes per stage (one SWIZZLE_128B row)
@@ -71,11 +74,16 @@ constexpr int A_BYTES = TILE_N * BK;  // 16 KB weight tile
 constexpr int MAX_M = 16;       // token rows (the MMA's N is 16)
 constexpr int MPAD = 16;
 constexpr int B_BYTES = MPAD * BK;    // 2 KB panel slot (one k-block of codes)
-constexpr int N_ACC = 4;        // independent accumulators per tile buffer (MMA latency chain)
-constexpr uint32_t TMEM_COLS = 128;   // 2 buffers x N_ACC x 16 columns
+// independent accumulators per tile buffer: consecutive MMAs into one accumulator
+// serialise on the tensor pipe's latency (~0.1 us each at N = 16), so the 4 K-steps
+// of a unit and the next units rotate over N_ACC accumulators (the epilogue adds
+// them back, exact int32)
+constexpr int N_ACC = 16;  // a power of two (rotation by mask)
+constexpr uint32_t TMEM_COLS = 2 * N_ACC * 16;  // 2 tile buffers x N_ACC x 16 columns
 constexpr int MAX_STAGES = 16;
 constexpr int MAX_WORDS = 4096; // mask words (K <= 131072, the MAX_INNER_DIM guard)
 constexpr int NSEG_PRE = 3;     // segments whose cached column data is loaded at kernel start
+constexpr int WO_PRE_L2 = 16;   // outlier rows of W prefetched into L2 per segment
 constexpr int SMEM_LIMIT = 227 * 1024;
 
 __device__ __forceinline__ bool bit_of(const uint32_t* m, int64_t k) {
@@ -140,6 +148,23 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void red_cluster_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.relaxed.cluster.shared::cluster.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -170,18 +195,45 @@ __device__ __forceinline__ float fixup_amax(const int32_t (&cr)[kTopT], const ui
 }
 
 // 16 codes of one token row at columns k0..k0+15, from 16 fp16 values; outlier
-// columns and columns past K give 0 (prologue.cu semantics)
+// columns and columns past K give 0 (prologue.cu semantics). The token phase
+// runs at 8 warps per SM, so it is latency-bound: the 16 fast roundings are
+// straight-line, independent chains (code_fast without its branch), and the
+// exact f64 tie-break runs afterwards for the ~1e-4 of elements that need it.
+__device__ __noinline__ uint32_t codes16_fixup(uint32_t word, uint32_t bad, const uint4& lo, const uint4& hi,
+                                               int base, double s) {
+    for (int e = base; e < base + 4; ++e)
+        if ((bad >> e) & 1u) {
+            const float x = hbits_to_float(half_bits(e < 8 ? lo : hi, e & 7));
+            const uint32_t c = static_cast<uint32_t>(static_cast<int>(code_of(x, s))) & 0xFFu;
+            const int sh = (e - base) * 8;
+            word = (word & ~(0xFFu << sh)) | (c << sh);
+        }
+    return word;
+}
+
 __device__ __forceinline__ uint4 codes16(const uint4& lo, const uint4& hi, uint32_t mbits, int64_t k0,
                                          int64_t K, float s32, double s) {
-    uint32_t b[16];
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: t - kMagic = rint(pf)
+    const int lim = K - k0 < 16 ? static_cast<int>(K - k0) : 16;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    uint32_t bad = 0;
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-        const uint32_t h = half_bits(e < 8 ? lo : hi, e & 7);
-        const int c = (((mbits >> e) & 1u) || k0 + e >= K) ? 0 : code_fast(hbits_to_float(h), s32, s);
-        b[e] = static_cast<uint32_t>(c) & 0xFFu;
+        const float x = hbits_to_float(half_bits(e < 8 ? lo : hi, e & 7));
+        const float pf = x * s32;
+        const float t = pf + kMagic;
+        const float r = t - kMagic;
+        const bool zero = ((mbits >> e) & 1u) || e >= lim;
+        const uint32_t c = zero ? 0u : (static_cast<uint32_t>(__float_as_int(t) - 0x4B400000) & 0xFFu);
+        bad |= (!zero && !(fabsf(pf - r) < 0.5f - 6.103515625e-05f)) ? (1u << e) : 0u;
+        w[e >> 2] |= c << ((e & 3) * 8);
     }
-    return make_uint4(b[0] | b[1] << 8 | b[2] << 16 | b[3] << 24, b[4] | b[5] << 8 | b[6] << 16 | b[7] << 24,
-                      b[8] | b[9] << 8 | b[10] << 16 | b[11] << 24, b[12] | b[13] << 8 | b[14] << 16 | b[15] << 24);
+    if (bad) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if ((bad >> (q * 4)) & 0xFu) w[q] = codes16_fixup(w[q], bad, lo, hi, q * 4, s);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 struct __align__(8) Bars {
@@ -190,6 +242,7 @@ struct __align__(8) Bars {
     uint64_t tmem_full[2];
     uint64_t tmem_empty[2];
     uint64_t xbar;               // bulk copies of the X slice landed
+    uint64_t pbar;               // split-tile finisher: same-cluster contributors' partials added
     uint32_t tmem_slot;
     uint32_t nonfinite[CL];      // rank 0: every rank's NaN/Inf flag
     int32_t n_out;
@@ -211,19 +264,23 @@ struct Params {
     int num_kb, n_tiles;
     int s1, s2;          // weight stages before / after the X slice area is released
     int pre;             // weight tiles loaded before the token phase (<= s1)
+    int l2_prefetch;     // the CTA's remaining weight tiles are prefetched into L2 at the start
     int slots;           // panel slots (k-blocks of codes) per CTA
     int xs_cached;       // the X slice is kept in smem (the ring's stages s1..s2-1) for T2
     int64_t xs_ld;       // halves per cached X-slice row
     int64_t total_units;
     unsigned long long* dbg;  // per-CTA %globaltimer stamps (dev tool), nullable
-    int dbg_mode;             // dev build A/B: bit 0 local panel stores only, bit 1 no code math
+    int dbg_mode;             // dev build A/B: bit 0 local panel stores only, bit 1 no code math, bit 2 no Xq copy,
+                              // bit 3 no token phase at all
 };
 
-// dynamic shared memory after the weight ring and the panel
-__host__ __device__ inline size_t smem_tail(int64_t nwords) {
+// dynamic shared memory after the weight ring and the panel (kb_max: k-blocks a
+// rank owns, at most; their panel destinations are a kb_max x CL int16 table)
+__host__ __device__ inline size_t smem_tail(int64_t nwords, int64_t kb_max) {
     return static_cast<size_t>((nwords + 3) & ~int64_t(3)) * 4 + CL * MAX_M * 4 +
            MAX_M * (sizeof(double) + 3 * sizeof(float)) + MAX_M * WO_CAP * sizeof(float) +
-           TILE_N * MAX_M * sizeof(int32_t) + sizeof(Bars) + 64;
+           2 * TILE_N * MAX_M * sizeof(int32_t) + static_cast<size_t>((kb_max * CL + 3) & ~int64_t(3)) * 2 +
+           sizeof(Bars) + 64;
 }
 
 template <int EPI>
@@ -323,11 +380,11 @@ __device__ void compact_mask(const uint32_t* __restrict__ smask, int64_t nwords,
     if (threadIdx.x == THREADS - 1) bars->n_out = pos;
 }
 
-// 16 token columns of this thread's weight row: sum of the N_ACC accumulators
-__device__ __forceinline__ void tmem_row16(uint32_t taddr, uint32_t (&r)[16]) {
+// 16 token columns of this thread's weight row: sum of the n_used accumulators
+// the segment wrote (min(N_ACC, 4 x its units))
+__device__ __forceinline__ void tmem_row16(uint32_t taddr, int n_used, uint32_t (&r)[16]) {
     tmem_ld_32x32b_x16(taddr, r);
-#pragma unroll
-    for (int j = 1; j < N_ACC; ++j) {
+    for (int j = 1; j < n_used; ++j) {
         uint32_t t[16];
         tmem_ld_32x32b_x16(taddr + static_cast<uint32_t>(j * MPAD), t);
         tmem_ld_wait();
@@ -355,7 +412,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* samax = srow + MAX_M;                                        // row amax
     float* sxo = samax + MAX_M;                                         // [M][WO_CAP] x[:, O]
     int32_t* pdot = reinterpret_cast<int32_t*>(sxo + MAX_M * WO_CAP);    // [TILE_N][MAX_M]
-    Bars* bars = reinterpret_cast<Bars*>(pdot + TILE_N * MAX_M);
+    const int kb_max = (p.num_kb + CL - 1) / CL;
+    int32_t* racc = pdot + TILE_N * MAX_M;  // [MAX_M][TILE_N] same-cluster contributors' partial sums
+    int16_t* sdst = reinterpret_cast<int16_t*>(racc + TILE_N * MAX_M);  // [kb_max][CL] panel slot or -1
+    Bars* bars = reinterpret_cast<Bars*>(sdst + ((kb_max * CL + 3) & ~3));
     __half* xs = reinterpret_cast<__half*>(ring + static_cast<size_t>(p.s1) * A_BYTES);  // T1/T2 only
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -381,7 +441,24 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int64_t xs_ld = p.xs_ld;
 
     DSTAMP(p.dbg, 0);
-    // ================= setup + weight prefetch (independent of this call's tokens)
+    const bool bulk = cached && a.x_vec;
+    // split tile this CTA finishes (at most one: the last tile start in its range
+    // when that tile runs past the range), and its contributors: those in this
+    // cluster add their partials into racc (distributed shared memory), the
+    // others hand them over through the workspace
+    int fin_local = 0, fin_cross = 0;
+    {
+        const int t_last = (u_end - 1) / num_kb;
+        const int t0u = t_last * num_kb;
+        if (t0u >= u_begin && t0u + num_kb > u_end) {
+            const uint32_t cl = (static_cast<uint32_t>(t0u + num_kb) * Gu - 1) / T;
+            const uint32_t cl_in = min(cl, clu * CL + CL - 1);
+            fin_local = static_cast<int>(cl_in - blockIdx.x);
+            fin_cross = static_cast<int>(cl - cl_in);
+        }
+    }
+    // ================= setup: barriers, the weight prefetch (independent of this
+    // call's tokens), then the X slice (written by the preceding kernel) first
     if (tid == 0) {
         tma_prefetch_desc(&tmap_w);
         for (int s = 0; s < S2; ++s) {
@@ -393,6 +470,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&bars->tmem_empty[q], 4);
         }
         mbar_init(&bars->xbar, 1);
+        mbar_init(&bars->pbar, max(1, fin_local));
         fence_mbarrier_init();
         const uint64_t pol_w = l2_policy_evict_normal();
         for (int i = 0; i < min(p.pre, L); ++i) {
@@ -402,51 +480,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                         (u / num_kb) * TILE_N, pol_w);
         }
     }
-    if (tid < CL) {  // every rank's unit range: which panel slots its k-blocks land in
-        const uint32_t g = clu * CL + tid;
-        const int ub = static_cast<int>(T * g / Gu), ue = static_cast<int>(T * (g + 1) / Gu);
-        bars->peer_start[tid] = ub % num_kb;
-        bars->peer_len[tid] = ue - ub;
-    }
-    if (warp == 2) tmem_alloc<TMEM_COLS>(&bars->tmem_slot);
-    // cached per-column data of the first segments (immutable): loads in flight
-    // through the token phase, consumed by the epilogue warps
-    int32_t pre_cr[NSEG_PRE];
-    float pre_aw[NSEG_PRE];
-    if (warp >= 4) {
-        const int n_local = tid - 128;
-        int u = u_begin;
-#pragma unroll
-        for (int sg = 0; sg < NSEG_PRE; ++sg) {
-            const int tile = u / num_kb;
-            const int64_t n = static_cast<int64_t>(tile) * TILE_N + n_local;
-            const bool ok = u < u_end && n < N;
-            pre_cr[sg] = ok ? __ldg(a.cand_r + n) : -1;
-            pre_aw[sg] = ok ? __ldg(a.amax_full + n) : 127.0f;
-            u = min(u_end, (tile + 1) * num_kb);
-        }
-    }
-    // token rows M..15 of every panel slot stay zero
-    for (int i = tid; i < p.slots * (MPAD - static_cast<int>(M)) * 8; i += THREADS) {
-        const int per = (MPAD - static_cast<int>(M)) * 8;
-        const int sl = i / per, rr = i - sl * per;
-        *reinterpret_cast<uint4*>(panel + static_cast<size_t>(sl) * B_BYTES + (M + rr / 8) * BK + (rr & 7) * 16) =
-            make_uint4(0u, 0u, 0u, 0u);
-    }
-    for (int64_t w = w0 + tid; w < w1; w += THREADS) smask[w] = 0u;
-    cluster_arrive_relaxed();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = bars->tmem_slot;
+    if (tid == 0) DSTAMP(p.dbg, 19);
     // X and the workspace (written / read by the preceding kernels) after the wait
     pdl_wait();
     pdl_trigger();
-    DSTAMP(p.dbg, 1);
-
-    // ================= T1: X slice, outlier bits, row partials -> every rank
-    const uint32_t thr = a.thr_bits_dev != nullptr ? __ldcg(a.thr_bits_dev) : a.thr_bits;
-    const bool bulk = cached && a.x_vec;
+    if (tid == 0) DSTAMP(p.dbg, 20);
     if (bulk && tid == 0) {
         const uint32_t row_bytes = static_cast<uint32_t>(nfull) * 16u;
         if (row_bytes > 0) {
@@ -456,10 +494,89 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_arrive(&bars->xbar);
         }
     }
+    if (tid == 0) DSTAMP(p.dbg, 21);
+    // the rest of this CTA's weight tiles -> L2 now: a CTA's TMA engine keeps only
+    // a few tiles in flight, L2 prefetches have no such cap, so HBM streams the
+    // layer at full rate under the token phase and the ring's later loads hit L2
+    if (warp == 3 && p.l2_prefetch)
+        for (int i = min(p.pre, L) + lane; i < L; i += 32) {
+            const int u = u_begin + i;
+            tma_prefetch_l2_2d(&tmap_w, (u % num_kb) * BK, (u / num_kb) * TILE_N);
+        }
+    // panel destinations of this rank's k-blocks: slot in each rank's panel, or -1
+    for (int i = tid; i < (kb_hi - kb_lo) * CL; i += THREADS) {
+        const int kbi = i / CL, q = i - kbi * CL;
+        const uint32_t g = clu * CL + q;
+        const int ub = static_cast<int>(T * g / Gu), len = static_cast<int>(T * (g + 1) / Gu) - ub;
+        const int kb = kb_lo + kbi;
+        int slot;
+        if (len >= num_kb) {
+            slot = kb;
+        } else {
+            slot = kb - ub % num_kb;
+            if (slot < 0) slot += num_kb;
+            if (slot >= len) slot = -1;
+        }
+        sdst[i] = static_cast<int16_t>(slot);
+    }
+    if (tid == 0) DSTAMP(p.dbg, 22);
+    if (warp == 2) tmem_alloc<TMEM_COLS>(&bars->tmem_slot);
+    if (tid == 64) DSTAMP(p.dbg, 23);
+    // cached (immutable) candidates of the first segments' columns, in registers
+    // through the token phase: the column fixup needs no global round trip
+    int32_t pre_cr[NSEG_PRE][kTopT];
+    uint16_t pre_cv[NSEG_PRE][kTopT];
+    float pre_aw[NSEG_PRE];
+    if (warp >= 4) {
+        const int n_local = tid - 128;
+        int u = u_begin;
+#pragma unroll
+        for (int sg = 0; sg < NSEG_PRE; ++sg) {
+            const int tile = u / num_kb;
+            const int64_t n = static_cast<int64_t>(tile) * TILE_N + n_local;
+            const bool ok = u < u_end && n < N;
+#pragma unroll
+            for (int t = 0; t < kTopT; ++t) {
+                pre_cr[sg][t] = ok ? __ldg(a.cand_r + t * N + n) : -1;
+                pre_cv[sg][t] = ok && t > 0 ? __ldg(a.cand_v + t * N + n) : uint16_t(0);
+            }
+            pre_aw[sg] = ok ? __ldg(a.amax_full + n) : 127.0f;
+            u = min(u_end, (tile + 1) * num_kb);
+        }
+    }
+    if (tid == 128) DSTAMP(p.dbg, 24);
+    // token rows M..15 of every panel slot stay zero
+    for (int i = tid; i < p.slots * (MPAD - static_cast<int>(M)) * 8; i += THREADS) {
+        const int per = (MPAD - static_cast<int>(M)) * 8;
+        const int sl = i / per, rr = i - sl * per;
+        *reinterpret_cast<uint4*>(panel + static_cast<size_t>(sl) * B_BYTES + (M + rr / 8) * BK + (rr & 7) * 16) =
+            make_uint4(0u, 0u, 0u, 0u);
+    }
+    for (int64_t w = w0 + tid; w < w1; w += THREADS) smask[w] = 0u;
+    if (fin_local > 0)  // contributors add into it after cluster barrier 2
+        for (int i = tid; i < static_cast<int>(M) * TILE_N; i += THREADS) racc[i] = 0;
     if (bulk && nv > nfull)  // ragged last vector (K % 8 != 0): element loads
         for (int64_t m = tid; m < M; m += THREADS)
             *reinterpret_cast<uint4*>(xs + m * xs_ld + nfull * 8) = load8(a.x + m * a.ldx, c0 + nfull * 8, K, false);
+    if (tid == 0) DSTAMP(p.dbg, 25);
+    cluster_arrive_relaxed();
+    tc_fence_before();
     __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = bars->tmem_slot;
+    DSTAMP(p.dbg, 1);
+
+    // ================= T1: X slice, outlier bits, row partials -> every rank
+    if (kDevStamps && (p.dbg_mode & 8)) {  // A/B: no token phase (garbage panel): the stream alone
+        cluster_wait();
+        cluster_sync_all();
+        cluster_sync_all();
+        if (tid == 0) bars->n_out = 0;
+        __syncthreads();
+        goto roles;
+    }
+    {
+    const uint32_t thr = a.thr_bits_dev != nullptr ? __ldcg(a.thr_bits_dev) : a.thr_bits;
     if (bulk) mbar_wait(&bars->xbar, 0);
     DSTAMP(p.dbg, 2);
     uint32_t nf = 0;
@@ -527,12 +644,55 @@ __global__ void __launch_bounds__(THREADS, 1)
             a.ramax_bits[m] = mx;
         }
     }
-    __syncthreads();
+    compact_mask(smask, nwords, bars, lead && crank == 0 ? a.o_idx : nullptr);  // syncs
+    __syncthreads();  // o_s, n_out, row scales
     if (tid == 0) DSTAMP(p.dbg, 14);
+    if (warp >= 4) {
+        // the epilogue's global data, pulled into L2 while the codes are made:
+        // W[O, tile] (256 B per outlier row and segment) and, for each patched
+        // column, the cached q2 codes over the segment's k-range
+        const int et = tid - 128;
+        const int n_o0 = min(bars->n_out, WO_PRE_L2);
+        int u = u_begin;
+#pragma unroll
+        for (int sg = 0; sg < NSEG_PRE; ++sg) {
+            const int tile = u / num_kb;
+            const int seg_end = min(u_end, (tile + 1) * num_kb);
+            if (u < u_end) {
+                if (et < n_o0) {
+                    const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
+                    const int64_t cols = min(static_cast<int64_t>(TILE_N), N - n0);
+                    const uint32_t bytes = static_cast<uint32_t>(cols * 2) & ~15u;
+                    if (bytes && a.w_vec)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         a.w + static_cast<int64_t>(bars->o_s[et]) * a.ldw + n0),
+                                     "r"(bytes)
+                                     : "memory");
+                }
+                const int64_t n = static_cast<int64_t>(tile) * TILE_N + et;
+                if (n < N && pre_cr[sg][0] >= 0 && bit_of(smask, pre_cr[sg][0])) {
+                    int src;
+                    const float an = fixup_amax(pre_cr[sg], pre_cv[sg], smask, src);
+                    if (src == 1 && an != pre_aw[sg]) {
+                        const int k_lo = (u % num_kb) * BK, k_hi = min((seg_end - 1) % num_kb + 1, num_kb) * BK;
+                        if (k_hi > k_lo)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.q2 + n * a.ldq + k_lo),
+                                         "r"(static_cast<uint32_t>(k_hi - k_lo))
+                                         : "memory");
+                    }
+                }
+            }
+            u = seg_end;
+        }
+    }
     const int nkb = kb_hi - kb_lo;
-    for (int it = tid; it < nkb * static_cast<int>(M) * 8; it += THREADS) {
-        const int kbi = it / (static_cast<int>(M) * 8);
-        const int rem = it - kbi * static_cast<int>(M) * 8;
+    // codes of this rank's k-blocks: item = (k-block, row, 16-column chunk); row
+    // and chunk from a multiply-shift (exact for the ranges here: rest < 2^13)
+    const uint32_t m8 = static_cast<uint32_t>(M) * 8u;
+    const uint32_t inv_m8 = (1u << 20) / m8 + 1u;
+    for (int it = tid; it < nkb * static_cast<int>(m8); it += THREADS) {
+        const int kbi = static_cast<int>((static_cast<uint32_t>(it) * inv_m8) >> 20);
+        const int rem = it - kbi * static_cast<int>(m8);
         const int m = rem >> 3, ch = rem & 7;
         const int kb = kb_lo + kbi;
         const int64_t k0 = static_cast<int64_t>(kb) * BK + ch * 16;
@@ -548,20 +708,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             const uint32_t mbits = (smask[k0 >> 5] >> (k0 & 31)) & 0xFFFFu;
             code = codes16(lo, hi, mbits, k0, K, sscale32[m], sscale[m]);
-            if (lead) *reinterpret_cast<uint4*>(a.xq + m * a.ldq + k0) = code;  // workspace Xq (views)
+            if (lead && !(kDevStamps && (p.dbg_mode & 4)))
+                *reinterpret_cast<uint4*>(a.xq + m * a.ldq + k0) = code;  // workspace Xq (views)
         }
         const uint32_t off = static_cast<uint32_t>(m * BK + ((ch ^ (m & 7)) * 16));
+        const int16_t* dst = sdst + kbi * CL;
 #pragma unroll
         for (int q = 0; q < CL; ++q) {
-            const int len = bars->peer_len[q];
-            int slot;
-            if (len >= num_kb) {
-                slot = kb;
-            } else {
-                slot = kb - bars->peer_start[q];
-                if (slot < 0) slot += num_kb;
-                if (slot >= len) continue;
-            }
+            const int slot = dst[q];
+            if (slot < 0) continue;
             if (kDevStamps && (p.dbg_mode & 1))
                 *reinterpret_cast<uint4*>(panel + static_cast<size_t>(slot) * B_BYTES + off) = code;
             else
@@ -571,8 +726,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) DSTAMP(p.dbg, 15);
     asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");  // panels feed tcgen05.mma
     if (tid == 0) DSTAMP(p.dbg, 16);
-    compact_mask(smask, nwords, bars, lead && crank == 0 ? a.o_idx : nullptr);
-    if (tid == 0) DSTAMP(p.dbg, 17);
     if (lead) {
         for (int64_t w = w0 + tid; w < w1; w += THREADS) a.mask[w] = smask[w];
         if (crank == CL - 1) {  // Xq padding columns K..ldq (whole 16-column chunks)
@@ -592,50 +745,79 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int q = 0; q < CL; ++q) any |= bars->nonfinite[q];
         if (a.nonfinite != nullptr) *a.nonfinite = any ? 1 : 0;
     }
+    }
+roles:
     const int n_out = bars->n_out;
     const int n_o = n_out <= WO_CAP ? n_out : 0;  // x[:, O] factors staged in smem
     DSTAMP(p.dbg, 4);
 
+    // Producer and MMA loops keep their (tile, k-block, stage, phase) state
+    // incrementally: a runtime integer division is a ~20-instruction dependent
+    // chain, and at 4 small MMAs per unit it would pace the whole weight stream.
     if (warp == 0) {
         // ---------------- TMA producer: the remaining weight tiles
         if (lane == 0) {
             const uint64_t pol_w = l2_policy_evict_normal();
-            for (int i = min(p.pre, L); i < L; ++i) {
-                const int u = u_begin + i;
-                const int s = i % S2;
-                if (i >= S2) mbar_wait(&bars->empty[s], ((i / S2) & 1) ^ 1u);
+            const int i0 = min(p.pre, L);
+            int u = u_begin + i0;
+            int tile = u / num_kb, kb = u - tile * num_kb;
+            int s = i0 % S2;
+            uint32_t ph = static_cast<uint32_t>((i0 / S2) & 1);
+            for (int i = i0; i < L; ++i) {
+                if (i >= S2) mbar_wait(&bars->empty[s], ph ^ 1u);
                 mbar_arrive_expect_tx(&bars->full[s], A_BYTES);
-                tma_load_2d(&tmap_w, &bars->full[s], ring + static_cast<size_t>(s) * A_BYTES, (u % num_kb) * BK,
-                            (u / num_kb) * TILE_N, pol_w);
+                tma_load_2d(&tmap_w, &bars->full[s], ring + static_cast<size_t>(s) * A_BYTES, kb * BK, tile * TILE_N,
+                            pol_w);
+                if (++kb == num_kb) {
+                    kb = 0;
+                    ++tile;
+                }
+                if (++s == S2) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
+        // ---------------- MMA issuer. At N = 16 tokens a tcgen05.mma moves only 4 KB of
+        // weights, so the issue loop itself paces the stream: descriptors are
+        // precomputed (+2 per 32-byte K step, + one slot / stage stride per unit) and
+        // the accumulator rotates by mask (~60 cycles per MMA instead of ~240)
         const uint32_t idesc = idesc_i8(TILE_N, MPAD);
+        constexpr int KS = BK / UMMA_K;  // 4 K-steps per unit
+        const uint64_t a_base = smem_desc_k_sw128(smem_addr(ring));
+        const uint64_t b_base = smem_desc_k_sw128(smem_addr(panel));
+        int s = 0;
+        uint32_t ph = 0;
+        int kb = u_begin % num_kb;  // the unit's k-block; panel slot = kb (all_kb) or i
         int seg = 0;
         for (int u = u_begin; u < u_end; ++seg) {
-            const int tile = u / num_kb;
-            const int seg_end = min(u_end, (tile + 1) * num_kb);
+            const int seg_end = min(u_end, (u / num_kb + 1) * num_kb);
             const int acc = seg & 1;
             mbar_wait(&bars->tmem_empty[acc], ((seg >> 1) & 1) ^ 1u);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * N_ACC * MPAD);
             for (int kk = 0; u < seg_end; ++u, ++kk) {
-                const int i = u - u_begin, s = i % S2;
-                mbar_wait(&bars->full[s], (i / S2) & 1);
+                mbar_wait(&bars->full[s], ph);
                 tc_fence_after();
-                if (lane == 0 && u == u_begin) DSTAMP(p.dbg, 5);
                 if (lane == 0) {
-                    const int slot = all_kb ? u % num_kb : i;
-                    const uint32_t a0 = smem_addr(ring + static_cast<size_t>(s) * A_BYTES);
-                    const uint32_t b0 = smem_addr(panel + static_cast<size_t>(slot) * B_BYTES);
+                    if (u == u_begin) DSTAMP(p.dbg, 5);
+                    const int slot = all_kb ? kb : u - u_begin;
+                    const uint64_t ad = a_base + static_cast<uint64_t>(s * (A_BYTES >> 4));
+                    const uint64_t bd = b_base + static_cast<uint64_t>(slot * (B_BYTES >> 4));
+                    const uint32_t d = d_tmem + static_cast<uint32_t>(((kk * KS) & (N_ACC - 1)) * MPAD);
+                    const uint32_t accum = kk * KS >= N_ACC ? 1u : 0u;  // fresh on the first use
 #pragma unroll
-                    for (int k = 0; k < BK / UMMA_K; ++k)
-                        mma_i8(d_tmem + static_cast<uint32_t>(k * MPAD), smem_desc_k_sw128(a0 + k * UMMA_K),
-                               smem_desc_k_sw128(b0 + k * UMMA_K), idesc, kk > 0 ? 1u : 0u);
+                    for (int k = 0; k < KS; ++k)
+                        mma_i8(d + static_cast<uint32_t>(k * MPAD), ad + 2 * k, bd + 2 * k, idesc, accum);
                     mma_commit(&bars->empty[s]);
                 }
                 __syncwarp();
+                if (++kb == num_kb) kb = 0;
+                if (++s == S2) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
             if (lane == 0) mma_commit(&bars->tmem_full[acc]);
             __syncwarp();
@@ -660,13 +842,22 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int acc = seg & 1;
             const int64_t n = static_cast<int64_t>(tile) * TILE_N + n_local;
             const bool n_ok = n < N;
-            int32_t c0r;
+            int32_t cr[kTopT];
+            uint16_t cv[kTopT];
             float aw;
             if (seg < NSEG_PRE) {
-                c0r = seg == 0 ? pre_cr[0] : seg == 1 ? pre_cr[1] : pre_cr[2];
+#pragma unroll
+                for (int t = 0; t < kTopT; ++t) {
+                    cr[t] = seg == 0 ? pre_cr[0][t] : seg == 1 ? pre_cr[1][t] : pre_cr[2][t];
+                    cv[t] = seg == 0 ? pre_cv[0][t] : seg == 1 ? pre_cv[1][t] : pre_cv[2][t];
+                }
                 aw = seg == 0 ? pre_aw[0] : seg == 1 ? pre_aw[1] : pre_aw[2];
             } else {
-                c0r = n_ok ? __ldg(a.cand_r + n) : -1;
+#pragma unroll
+                for (int t = 0; t < kTopT; ++t) {
+                    cr[t] = n_ok ? __ldg(a.cand_r + t * N + n) : -1;
+                    cv[t] = n_ok && t > 0 ? __ldg(a.cand_v + t * N + n) : uint16_t(0);
+                }
                 aw = n_ok ? __ldg(a.amax_full + n) : 127.0f;
             }
             float wr[WO_CAP];
@@ -679,14 +870,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (et == 0) bars->n_ent = 0;
             bars->ent_of[n_local] = -1;
             named_bar_sync(1, 128);
-            if (n_ok && c0r >= 0 && bit_of(smask, c0r)) {
-                int32_t cr[kTopT];
-                uint16_t cv[kTopT];
-#pragma unroll
-                for (int t = 1; t < kTopT; ++t) {
-                    cr[t] = __ldg(a.cand_r + t * N + n);
-                    cv[t] = __ldg(a.cand_v + t * N + n);
-                }
+            if (n_ok && cr[0] >= 0 && bit_of(smask, cr[0])) {
                 int src;
                 const float a_new = fixup_amax(cr, cv, smask, src);
                 if (a_new < 0.0f || a_new != aw) {
@@ -698,6 +882,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             named_bar_sync(1, 128);
             const int n_ent = bars->n_ent;
+            if (kDevStamps && et == 0 && p.dbg != nullptr) p.dbg[blockIdx.x * 32 + 26 + min(seg, 2)] = n_ent;
             if (n_ent > 0) {
                 // every cached candidate an outlier row (rare): scan the column, warp per entry
                 for (int e = quad; e < n_ent; e += 4) {
@@ -709,6 +894,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             mx = max(mx, static_cast<uint32_t>(__half_as_ushort(a.w[k * a.ldw + j])) & 0x7FFFu);
 #pragma unroll
                     for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+                    __syncwarp();  // every lane has read ent_src[e]
                     if (lane == 0) {
                         const float an = hbits_to_float(mx);
                         bars->ent_a[e] = an;
@@ -785,19 +971,52 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t t0 = static_cast<uint32_t>(tile * num_kb), t1 = t0 + num_kb;
             const uint32_t cf = ((t0 + 1) * Gu - 1) / T;
             const uint32_t cl = (t1 * Gu - 1) / T;
+            // the finisher's cross-cluster partials: usually long ready (they are the
+            // next cluster's first segments), so fetched while this segment's MMAs run
+            uint32_t xpart[16];
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) xpart[jj] = 0u;
+            if (!full && cf == blockIdx.x && fin_cross > 0) {
+                if (et == 0) {
+                    // bounded: a workspace whose counters were never zeroed traps
+                    // instead of hanging the GPU
+                    for (uint32_t spin = 0; ld_acquire(a.tile_cnt + tile) < fin_cross; ++spin)
+                        if (spin > (1u << 22)) __trap();
+                    a.tile_cnt[tile] = 0;
+                }
+                named_bar_sync(1, 128);
+                __threadfence();
+                for (uint32_t c = cl - fin_cross + 1; c <= cl; ++c) {
+                    const int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj)
+                        if (jj < M) xpart[jj] += static_cast<uint32_t>(__ldcg(src + jj * TILE_N));
+                }
+            }
             mbar_wait(&bars->tmem_full[acc], (seg >> 1) & 1);
             tc_fence_after();
             if (et == 0 && seg == 0) DSTAMP(p.dbg, 7);
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * N_ACC * MPAD);
             uint32_t r[16];
-            tmem_row16(t_row, r);
+            tmem_row16(t_row, min(N_ACC, (seg_end - su0) * (BK / UMMA_K)), r);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->tmem_empty[acc]);
             if (my_ent >= 0) {
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) r[jj] = static_cast<uint32_t>(pdot[my_ent * MAX_M + jj]);
+            }
+            if (!full && cf != blockIdx.x && cf / CL == clu) {
+                // the finisher is in this cluster: add into its racc, then one
+                // release-arrive on its pbar per contributor CTA
+                const uint32_t dst = mapa_shared(racc + n_local, cf % CL);
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                    if (jj < M) red_cluster_add(dst + jj * TILE_N * 4, r[jj]);
+                named_bar_sync(1, 128);
+                if (et == 0) mbar_arrive_remote_release(mapa_shared(&bars->pbar, cf % CL));
+                continue;
             }
             if (!full && cf != blockIdx.x) {
                 int32_t* slotp = a.c32 + static_cast<int64_t>(blockIdx.x) * (MAX_M * TILE_N) + n_local;
@@ -809,22 +1028,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (et == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.tile_cnt + tile) : "memory");
                 continue;
             }
-            if (!full) {  // finisher: the other contributors' partials, then reset the counter
-                if (et == 0) {
-                    // bounded: a workspace whose counters were never zeroed traps
-                    // instead of hanging the GPU
-                    for (uint32_t spin = 0; ld_acquire(a.tile_cnt + tile) < static_cast<int>(cl - cf); ++spin)
-                        if (spin > (1u << 22)) __trap();
-                    a.tile_cnt[tile] = 0;
-                }
-                named_bar_sync(1, 128);
-                __threadfence();
-                for (uint32_t c = cf + 1; c <= cl; ++c) {
-                    const int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
+            if (kDevStamps && et == 0 && p.dbg != nullptr) p.dbg[blockIdx.x * 32 + 29 + min(seg, 2)] = full ? 2 : (cf != blockIdx.x ? 0 : 1);
+            if (!full) {  // finisher: the contributors' partials (this cluster's in racc, the others' global)
+                if (fin_local > 0) {
+                    mbar_wait_cluster(&bars->pbar, 0);
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj)
-                        if (jj < M) r[jj] += static_cast<uint32_t>(__ldcg(src + jj * TILE_N));
+                        if (jj < M) r[jj] += static_cast<uint32_t>(racc[jj * TILE_N + n_local]);
                 }
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) r[jj] += xpart[jj];
             }
             if (n_ok) {
 #pragma unroll
@@ -843,6 +1056,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
     }
+    // no CTA leaves while a cluster peer may still add into its racc / arrive on
+    // its pbar (the finisher's wait already implies it; this makes it explicit)
+    cluster_sync_all();
     DSTAMP(p.dbg, 9);
 }
 
@@ -909,7 +1125,7 @@ DecodeGeom decode_geom(int64_t M, int64_t K, int64_t N) {
         env_kb = (e && e[0]) ? atoi(e) : -1;
     }
     const size_t limit = env_kb > 0 ? static_cast<size_t>(env_kb) * 1024 : SMEM_LIMIT;
-    const size_t fixed = 1024 + static_cast<size_t>(g.slots) * B_BYTES + smem_tail(nwords);
+    const size_t fixed = 1024 + static_cast<size_t>(g.slots) * B_BYTES + smem_tail(nwords, kb_max);
     if (fixed + 2 * A_BYTES > limit) return g;
     int s2 = static_cast<int>((limit - fixed) / A_BYTES);
     if (s2 > MAX_STAGES) s2 = MAX_STAGES;
@@ -993,6 +1209,8 @@ cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st) {
     // weight tiles prefetched before the token phase (env I8MM_DECODE_PREFETCH, A/B)
     static const int env_pre = env_int_once("I8MM_DECODE_PREFETCH", -1);
     prm.pre = env_pre >= 0 && env_pre < g.s1 ? env_pre : g.s1;
+    static const int env_l2 = env_int_once("I8MM_DECODE_L2_PREFETCH", 0);
+    prm.l2_prefetch = env_l2;
     prm.slots = g.slots;
     prm.xs_cached = g.xs_cached;
     prm.xs_ld = g.xs_ld;

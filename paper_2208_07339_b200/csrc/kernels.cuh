@@ -208,6 +208,7 @@ struct DecodeArgs {
     int64_t ldq;
     const __half* w;      // K x N fp16 (resident)
     int64_t ldw;
+    int w_vec;            // W rows 16-byte aligned (ldw % 8 == 0, base aligned)
     const int8_t* wq_t;   // N x ldq cached codes
     const float* amax_full;
     const uint16_t* cand_v;

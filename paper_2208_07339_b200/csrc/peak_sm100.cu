@@ -114,8 +114,82 @@ static cudaError_t launch(int iters, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Dev micro-benchmark: issue cost of small swap-AB MMAs (decode shape, M = 128
+// weight rows, N = n_tok token rows, K = 32), cycling n_acc accumulators, one
+// commit every `per_commit` MMAs (the decode kernel's per-unit stage release).
+__global__ void __launch_bounds__(128, 1) mma_small_kernel(int iters, int n_tok, int n_acc, int per_commit,
+                                                           unsigned long long* cycles) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sa = base;
+    uint8_t* sb = base + STAGES * A_BYTES;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t tmem_slot;
+    uint32_t* w32 = reinterpret_cast<uint32_t*>(base);
+    for (int i = threadIdx.x; i < STAGES * (A_BYTES + 256 * 128) / 4; i += blockDim.x) w32[i] = 0x01010101u * (i & 7);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbarrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) tmem_alloc<512>(&tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (threadIdx.x == 0) {
+        const uint32_t idesc = idesc_i8(128, static_cast<uint32_t>(n_tok));
+        const uint64_t ad0 = smem_desc_k_sw128(smem_addr(sa)), bd0 = smem_desc_k_sw128(smem_addr(sb));
+        const unsigned long long t0 = clock64();
+        if (per_commit == 0) {  // lean: precomputed descriptors (+2 per 32 B), accumulator by mask
+            for (int it = 0; it < iters; ++it) {
+                const uint64_t ad = ad0 + static_cast<uint64_t>((it & 1) * (A_BYTES >> 4));
+                const uint64_t bd = bd0 + static_cast<uint64_t>((it & 1) * (2048 >> 4));
+                const uint32_t d = tmem + static_cast<uint32_t>(((it * 4) & (n_acc - 1)) * n_tok);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    mma_i8(d + static_cast<uint32_t>(k * n_tok), ad + 2 * k, bd + 2 * k, idesc, it > 0 ? 1u : 0u);
+                mma_commit(&bar);
+            }
+        } else {
+            const uint32_t a0 = smem_addr(sa), b0 = smem_addr(sb);
+            int j = 0, c = 0;
+            for (int it = 0; it < iters; ++it) {
+                for (int k = 0; k < 4; ++k, ++j) {
+                    const uint64_t ad = smem_desc_k_sw128(a0 + (it & 1) * A_BYTES + k * 32);
+                    const uint64_t bd = smem_desc_k_sw128(b0 + (it & 1) * 2048 + k * 32);
+                    mma_i8(tmem + static_cast<uint32_t>((j % n_acc) * n_tok), ad, bd, idesc, j >= n_acc ? 1u : 0u);
+                    if (++c == per_commit) {
+                        c = 0;
+                        mma_commit(&bar);
+                    }
+                }
+            }
+        }
+        const unsigned long long t1 = clock64();
+        mma_commit(&bar);
+        if (blockIdx.x == 0) cycles[0] = t1 - t0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
 }  // namespace peak
 }  // namespace i8mm
+
+extern "C" int i8mm_debug_mma_small(int iters, int n_tok, int n_acc, int per_commit, unsigned long long* cycles,
+                                    void* stream) {
+    using namespace i8mm::peak;
+    const size_t smem = 1024 + STAGES * (A_BYTES + 256 * 128);
+    cudaFuncSetAttribute(mma_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    mma_small_kernel<<<i8mm::num_sms(), 128, smem, static_cast<cudaStream_t>(stream)>>>(iters, n_tok, n_acc,
+                                                                                         per_commit, cycles);
+    return cudaGetLastError() == cudaSuccess ? I8MM_OK : I8MM_ERR_CUDA;
+}
 
 extern "C" int i8mm_peak_mma_launch(int cg, int iters, void* stream) {
     if ((cg != 1 && cg != 2) || iters <= 0) return I8MM_ERR_ARGUMENT;

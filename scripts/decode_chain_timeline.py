@@ -23,10 +23,29 @@ bufs = [torch.zeros(sms * 32, dtype=torch.int64, device="cuda") for _ in run.lay
 for _ in range(5):
     run.step()
 torch.cuda.synchronize()
-for mod, x, b in zip(run.mods, run.xs, bufs):
-    L.i8mm_debug_decode_timeline(b.data_ptr())
-    mod(x)
-L.i8mm_debug_decode_timeline(None)
+graph = len(sys.argv) > 1 and sys.argv[1] == "graph"
+if graph:  # the bench's form: one CUDA graph of the step (PDL edges between the layers)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for mod, x, b in zip(run.mods, run.xs, bufs):
+                L.i8mm_debug_decode_timeline(b.data_ptr())
+                mod(x)
+    L.i8mm_debug_decode_timeline(None)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for b in bufs:
+        b.zero_()
+    g.replay()
+else:
+    for mod, x, b in zip(run.mods, run.xs, bufs):
+        L.i8mm_debug_decode_timeline(b.data_ptr())
+        mod(x)
+    L.i8mm_debug_decode_timeline(None)
 torch.cuda.synchronize()
 G = [b.view(sms, 32).cpu().double() for b in bufs]
 t0 = G[0][:, 0][G[0][:, 0] > 0].min()
@@ -45,8 +64,28 @@ cols = [(0, "start", min), (0, "start (last CTA)", max), (1, "waited", max), (2,
         (10, "flags", max), (11, "cluster wait", max), (12, "partials pushed", max), (13, "mask pushed", max),
         (3, "cluster barrier 1", max), (14, "row scales", max), (15, "codes pushed", max), (16, "proxy fence", max),
         (17, "o-list", max), (18, "lead writes", max), (4, "panels ready", max), (5, "1st MMA", max),
-        (6, "MMA issued", max), (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]
+        (6, "MMA issued", max)] + [(19, "setup: bars+W", max), (20, "setup: pdl wait", max), (21, "setup: X issued", max),
+        (22, "setup: L2 pf+dst", max), (23, "setup: tmem alloc", max), (24, "setup: cand loads", max),
+        (25, "setup: zeroing", max)] + [ (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]
 print("us from layer q's prep start (min or max over CTAs)")
 print(f"{'':18s}" + "".join(f"{n:>8s}" for n in names))
+med = lambda v: v.median()
 for i, lab, f in cols:
-    print(f"{lab:18s}" + "".join(f"{stat(g, i, f):8.2f}" for g in G))
+    print(f"{lab:18s}" + "".join(f"{stat(g, i, f):8.2f}" for g in G) + "   med" +
+          "".join(f"{stat(g, i, med):8.2f}" for g in G))
+
+# the latest CTAs of each layer: what they did (patched entries per segment, role per segment: 0 contributor, 1 finisher, 2 full)
+for name, g in zip(names, G):
+    end = g[:, 9]
+    order = torch.argsort(end, descending=True)[:6]
+    rows = []
+    for c in order.tolist():
+        if end[c] <= 0:
+            continue
+        rows.append(f"cta {c:3d} end {(end[c] - t0) / 1e3:6.2f} 1st-tmem {(g[c, 7] - t0) / 1e3:6.2f} "
+                    f"ents {[int(g[c, 26 + k]) for k in range(3)]} roles {[int(g[c, 29 + k]) for k in range(3)]}")
+    print(name, "latest:"); [print("   ", r) for r in rows]
+    ents = g[:, 26:29].sum(1)
+    print("    median end (no patched) {:.2f} / (patched) {:.2f}".format(
+        float(((end[(ents == 0) & (end > 0)] - t0) / 1e3).median()) if ((ents == 0) & (end > 0)).any() else -1,
+        float(((end[(ents > 0) & (end > 0)] - t0) / 1e3).median()) if ((ents > 0) & (end > 0)).any() else -1))

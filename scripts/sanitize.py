@@ -60,14 +60,15 @@ def st_splitk():  # M <= 128, K >= 8192: split-K partial sums + counters
     check("split-K exact", lin.matmul(x16, exact=True).cpu().numpy(), ref.output)
 
 
-def st_decode():  # cooperative decode kernel (grid barriers, stream-K, patch tile)
-    x, w = case(4, 8, 2048, 640, heavy=2)
-    ref = orc.c_llm_int8_matmul(x, w, 6.0)
-    lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
-    assert lin.uses_decode(8)
-    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
-    check("decode exact", lin.matmul(x16, exact=True).cpu().numpy(), ref.output)
-    lin(x16)
+def st_decode():  # decode kernel: 8-CTA clusters, DSMEM token side + partials, stream-K, patched dots
+    for seed, m, k, n, heavy in ((4, 8, 2048, 640, 2), (6, 13, 1001, 2000, 6), (7, 3, 5120, 1280, 1)):
+        x, w = case(seed, m, k, n, heavy=heavy)
+        ref = orc.c_llm_int8_matmul(x, w, 6.0)
+        lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+        assert lin.uses_decode(m)
+        x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+        check(f"decode exact {m}x{k}x{n}", lin.matmul(x16, exact=True).cpu().numpy(), ref.output)
+        lin(x16)
 
 
 def st_peers():  # fused all-gather epilogue stores into (emulated) peer buffers
