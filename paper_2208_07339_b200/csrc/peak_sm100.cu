@@ -141,7 +141,6 @@ __global__ void __launch_bounds__(128, 1) mma_small_kernel(int iters, int n_tok,
     if (threadIdx.x == 0) {
         const uint32_t idesc = idesc_i8(128, static_cast<uint32_t>(n_tok));
         const uint64_t ad0 = smem_desc_k_sw128(smem_addr(sa)), bd0 = smem_desc_k_sw128(smem_addr(sb));
-        const unsigned long long t0 = clock64();
         if (per_commit == 0) {  // lean: precomputed descriptors (+2 per 32 B), accumulator by mask
             for (int it = 0; it < iters; ++it) {
                 const uint64_t ad = ad0 + static_cast<uint64_t>((it & 1) * (A_BYTES >> 4));
@@ -167,9 +166,8 @@ __global__ void __launch_bounds__(128, 1) mma_small_kernel(int iters, int n_tok,
                 }
             }
         }
-        const unsigned long long t1 = clock64();
         mma_commit(&bar);
-        if (blockIdx.x == 0) cycles[0] = t1 - t0;
+        if (blockIdx.x == 0) cycles[0] = static_cast<unsigned long long>(iters);  // wall time is taken on the host
     }
     __syncthreads();
     if (threadIdx.x < 32) {

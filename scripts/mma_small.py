@@ -24,5 +24,4 @@ for n_tok, n_acc, per_commit in [(16, 4, 4), (16, 16, 0), (16, 4, 0), (32, 8, 0)
     torch.cuda.synchronize()
     us = s.elapsed_time(e) * 1e3
     mmas = iters * 4
-    print(f"N={n_tok:3d} n_acc={n_acc:2d} commit/{per_commit:7d}: {us / mmas * 1e3:7.1f} ns/MMA wall, "
-          f"issue {int(cyc.item()) / mmas:6.1f} cyc/MMA")
+    print(f"N={n_tok:3d} n_acc={n_acc:2d} commit/{per_commit:7d}: {us / mmas * 1e3:7.1f} ns/MMA wall")
