@@ -165,6 +165,11 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
             : "r"(smem_addr(bar)), "r"(parity)
             : "memory");
 }
+// L2 policy of the single-use weight stream: evict_first keeps the kernel's code,
+// X, the outputs and the workspace resident while 100+ MB of weights pass through
+__device__ __forceinline__ uint64_t weight_policy(int mode) {
+    return mode == 0 ? l2_policy_evict_first() : l2_policy_evict_normal();
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -265,6 +270,7 @@ struct Params {
     int s1, s2;          // weight stages before / after the X slice area is released
     int pre;             // weight tiles loaded before the token phase (<= s1)
     int l2_prefetch;     // the CTA's remaining weight tiles are prefetched into L2 at the start
+    int w_policy;        // 0: weight tiles evict_first (default), 1: evict_normal (A/B)
     int slots;           // panel slots (k-blocks of codes) per CTA
     int xs_cached;       // the X slice is kept in smem (the ring's stages s1..s2-1) for T2
     int64_t xs_ld;       // halves per cached X-slice row
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_init(&bars->xbar, 1);
         mbar_init(&bars->pbar, max(1, fin_local));
         fence_mbarrier_init();
-        const uint64_t pol_w = l2_policy_evict_normal();
+        const uint64_t pol_w = weight_policy(p.w_policy);
         for (int i = 0; i < min(p.pre, L); ++i) {
             const int u = u_begin + i;
             mbar_arrive_expect_tx(&bars->full[i], A_BYTES);
@@ -757,7 +763,7 @@ roles:
     if (warp == 0) {
         // ---------------- TMA producer: the remaining weight tiles
         if (lane == 0) {
-            const uint64_t pol_w = l2_policy_evict_normal();
+            const uint64_t pol_w = weight_policy(p.w_policy);
             const int i0 = min(p.pre, L);
             int u = u_begin + i0;
             int tile = u / num_kb, kb = u - tile * num_kb;
@@ -1211,6 +1217,8 @@ cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st) {
     prm.pre = env_pre >= 0 && env_pre < g.s1 ? env_pre : g.s1;
     static const int env_l2 = env_int_once("I8MM_DECODE_L2_PREFETCH", 0);
     prm.l2_prefetch = env_l2;
+    static const int env_wp = env_int_once("I8MM_DECODE_W_POLICY", 0);
+    prm.w_policy = env_wp;
     prm.slots = g.slots;
     prm.xs_cached = g.xs_cached;
     prm.xs_ld = g.xs_ld;

@@ -332,6 +332,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else if (warp == 1 && leader) {
         // ===================== MMA issuer (leader CTA) =====================
         constexpr uint32_t idesc = idesc_i8(BM * CG, BN);
+        const uint64_t a_desc0 = smem_desc_k_sw128(smem_addr(smem_a));
+        const uint64_t b_desc0 = smem_desc_k_sw128(smem_addr(smem_b));
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -359,12 +361,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_fence_after();
                 if (lane == 0 && it == 0 && kb == kb0) gstamp(p.dbg, 3);
                 if (lane == 0) {
-                    const uint32_t a0 = smem_addr(smem_a + stage * A_BYTES);
-                    const uint32_t b0 = smem_addr(smem_b + stage * B_BYTES);
+                    // descriptors advance by +2 per 32-byte K step (the address field
+                    // is in 16-byte units): no per-MMA descriptor arithmetic
+                    const uint64_t a_d = a_desc0 + static_cast<uint64_t>(stage * (A_BYTES >> 4));
+                    const uint64_t b_d = b_desc0 + static_cast<uint64_t>(stage * (B_BYTES >> 4));
 #pragma unroll
                     for (int k = 0; k < BK / UMMA_K; ++k) {
-                        const uint64_t ad = smem_desc_k_sw128(a0 + k * UMMA_K);
-                        const uint64_t bd = smem_desc_k_sw128(b0 + k * UMMA_K);
+                        const uint64_t ad = a_d + 2 * k;
+                        const uint64_t bd = b_d + 2 * k;
                         const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
                         if constexpr (CG == 2) mma_i8_pair(d_tmem, ad, bd, idesc, accum);
                         else mma_i8(d_tmem, ad, bd, idesc, accum);
