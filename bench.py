@@ -8,9 +8,10 @@ each layer of the workload through the public module ``Int8Linear`` (or
 ``ShardedInt8Linear`` under torchrun: W split along its output dimension,
 outputs all-gathered). The default workload is the north-star target
 (BASELINE.json / north_star): OPT-175B fc1 12288 -> 49152 on 16384 fp16
-tokens (configs[4] at 1 GPU), planted outlier columns x20, alpha 6.0. cfg5 fc2
-and cfg2 (configs[1], OPT-6.7B FFN) are measured in the same run and reported
-under ``extra_workloads``.
+tokens (configs[4] at 1 GPU), planted outlier columns x20, alpha 6.0. cfg5 fc2,
+cfg2 (configs[1], OPT-6.7B FFN), cfg4 fc1 (configs[3], OPT-66B, 1 GPU) and the
+cfg3 decode step (configs[2], OPT-13B projections at 8 tokens, CUDA-graph
+replay) are measured in the same run and reported under ``extra_workloads``.
 
 ``value`` = algorithmic int8 tera-ops/s (2*M*N*K summed over the layers) of
 the whole job, device-timed with inputs resident in HBM, max over ranks.
@@ -48,7 +49,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "LLM.int8() matmul TOPS and tokens/s at OPT FFN shapes; % of INT8 tensor peak"
 INT8_PEAK_NOMINAL_TOPS = 4500.0  # B200 dense INT8 (datasheet; 9 POPS is the 2:4-sparse figure)
 DEFAULT_WORKLOAD = "cfg5_fc1"
-DEFAULT_EXTRAS = ("cfg5_fc2", "cfg2")
+DEFAULT_EXTRAS = ("cfg5_fc2", "cfg2", "cfg4_fc1", "cfg3_decode")
 
 WORKLOADS = {
     "cfg5_fc1": {
@@ -662,10 +663,14 @@ def run_ours(args) -> None:
             if name == args.workload or name not in WORKLOADS:
                 continue
             r = WorkloadRun(name, dev, dist_on, args.nccl_gather)
+            step_x = r.step
+            if r.wl.get("decode") and not args.no_graph:  # as the main line: a CUDA graph of the step
+                g_call = pkg.GraphedCall(lambda *xx, _r=r: [m(x) for m, x in zip(_r.mods, xx)], *r.xs)
+                step_x = g_call.replay
             for _ in range(args.warmup):
-                r.step()
-            ms_x = timed(r.step, args.steps, dev, dist_on) / args.steps
-            g_x = gemm_marked_ms(r, max(1, min(args.steps, 20)))
+                step_x()
+            ms_x = timed(step_x, args.steps, dev, dist_on) / args.steps
+            g_x = ms_x if r.wl.get("decode") else gemm_marked_ms(r, max(1, min(args.steps, 20)))
             ent = {"value": r.ops / (ms_x * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": ms_x,
                    "tokens_per_s": r.layers[0][0] / (ms_x * 1e-3),
                    "config": config_dict(name, dist_on, world),

@@ -46,10 +46,13 @@ constexpr int A_BYTES = BM * BK;
 // TS: fp16 output through per-warp shared-memory staging tiles and TMA bulk
 // stores (full 64-byte row segments per box row instead of 32 scattered
 // 16-byte stores per warp instruction); costs one operand stage of smem.
-template <int CG, int MC = 1, bool TS = false>
+// NW: N=256 MMA halves per tile (2: the pair tile is 256 x 512 with one 512-column
+// accumulator -- each A panel feeds twice the outputs, 0.75x the L2 -> SM bytes)
+template <int CG, int MC = 1, bool TS = false, int NW = 1>
 struct Cfg {
-    static constexpr int STAGES = CG == 1 ? 4 : (TS ? 5 : 6);
-    static constexpr int B_ROWS = BN / CG;        // WqT rows resident in each CTA
+    static constexpr int TBN = BN * NW;           // output columns per (pair) tile
+    static constexpr int STAGES = NW == 2 ? (TS ? 3 : 4) : (CG == 1 ? 4 : (TS ? 5 : 6));
+    static constexpr int B_ROWS = TBN / CG;       // WqT rows resident in each CTA
     static constexpr int B_LOAD_ROWS = B_ROWS / MC;  // rows each CTA fetches (then multicasts)
     static constexpr int B_BYTES = B_ROWS * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -63,7 +66,6 @@ constexpr int EPI_WARP0 = 4;
 constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half of BN
 constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
-constexpr int COLS_PER_EPI_WARP = BN / (EPI_WARPS / 4);
 constexpr uint32_t TMEM_COLS = 2 * BN;
 
 struct __align__(8) Barriers {
@@ -74,14 +76,19 @@ struct __align__(8) Barriers {
     uint32_t tmem_slot;
 };
 
-constexpr size_t SMEM_WO = static_cast<size_t>(WO_CAP) * BN * sizeof(float);
-constexpr size_t SMEM_COLS = static_cast<size_t>(BN) * sizeof(double);
+// outlier rows of W staged per tile (the 512-wide tile stages up to 8; more take
+// the global-load path) and the per-column factors
+__host__ __device__ constexpr int wo_cap_of(int nw) { return nw == 2 ? 8 : WO_CAP; }
+__host__ __device__ constexpr size_t smem_wo_of(int nw) {
+    return static_cast<size_t>(wo_cap_of(nw)) * BN * nw * sizeof(float);
+}
+__host__ __device__ constexpr size_t smem_cols_of(int nw) { return static_cast<size_t>(BN) * nw * sizeof(double); }
 constexpr int STG_BYTES = 32 * 32 * 2;  // one 32 x 32 fp16 staging tile
 constexpr size_t SMEM_STG = static_cast<size_t>(EPI_WARPS) * 2 * STG_BYTES;  // double-buffered per warp
-template <int CG, int MC, bool TS = false>
+template <int CG, int MC, bool TS = false, int NW = 1>
 constexpr size_t smem_total() {
-    return 1024 /*align slack*/ + Cfg<CG, MC, TS>::SMEM_OPERANDS + (TS ? SMEM_STG : 0) + SMEM_WO +
-           SMEM_COLS + sizeof(Barriers) + 64;
+    return 1024 /*align slack*/ + Cfg<CG, MC, TS, NW>::SMEM_OPERANDS + (TS ? SMEM_STG : 0) + smem_wo_of(NW) +
+           smem_cols_of(NW) + sizeof(Barriers) + 64;
 }
 
 struct Params {
@@ -114,6 +121,7 @@ struct Params {
     int dbg_epi;    // A/B knob (I8MM_DBG_EPI): bit 0 skips the outlier FMAs, bit 1 the stores
     int tma_y;      // tmap_y is valid (fp16 Y, 16-byte aligned rows)
     int group_m;    // raster: m-tiles per group sharing each B panel in L2
+    int l2_pol;     // raster L2 policy (A/B): bit 0 A panels evict_last, bit 1 B panels evict_first
     // split-K (CG = 1 only): ksplit units per tile, each over a K-block range;
     // partials are added into c32 (column-major, c32_rows rows: one red per
     // lane covers 32 consecutive rows), the last unit of a tile runs the epilogue
@@ -153,9 +161,9 @@ struct TileSpace {
     int n_tiles, main_total, patch_n, total;
 };
 
-__device__ __forceinline__ TileSpace tile_space(const Params& p) {
+__device__ __forceinline__ TileSpace tile_space(const Params& p, int tbn) {
     TileSpace ts;
-    ts.n_tiles = static_cast<int>((p.N + BN - 1) / BN);
+    ts.n_tiles = static_cast<int>((p.N + tbn - 1) / tbn);
     ts.main_total = p.m_tiles * ts.n_tiles;
     int64_t pn = 0;
     if (p.patch_count != nullptr) {
@@ -163,7 +171,7 @@ __device__ __forceinline__ TileSpace tile_space(const Params& p) {
         pn = pn < p.N ? pn : p.N;
     }
     ts.patch_n = static_cast<int>(pn);
-    ts.total = ts.main_total + p.m_tiles * static_cast<int>((pn + BN - 1) / BN);
+    ts.total = ts.main_total + p.m_tiles * static_cast<int>((pn + tbn - 1) / tbn);
     return ts;
 }
 
@@ -194,12 +202,12 @@ __device__ __forceinline__ float amax_or_127(float a) { return a == 0.0f ? 127.0
 // widened to f32 once per tile: staging them as fp16 halves the shared-memory
 // wavefronts but costs two conversions per pair in every chunk (+58 M warp
 // instructions on fc1, +31 %, which a power-capped part pays in clock)
-template <int NO>
+template <int NO, int TBN>
 __device__ __forceinline__ void outlier_fma(float2* v2, const float* xo_r, const float* wrow) {
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
         const float2 xv2 = make_float2(xo_r[o], xo_r[o]);
-        const float4* wr = reinterpret_cast<const float4*>(wrow + o * BN);
+        const float4* wr = reinterpret_cast<const float4*>(wrow + o * TBN);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const float4 f = wr[u];
@@ -209,14 +217,19 @@ __device__ __forceinline__ void outlier_fma(float2* v2, const float* xo_r, const
     }
 }
 
-template <int EPI, int CG, int MC>
+template <int EPI, int CG, int MC, int NW>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_i8_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ CUtensorMap tmap_p,
                    const __grid_constant__ CUtensorMap tmap_y, const Params p) {
     constexpr bool TS = EPI == EPI_F16 && CG == 2;
-    using C = Cfg<CG, MC, TS>;
+    using C = Cfg<CG, MC, TS, NW>;
+    constexpr int TBN = C::TBN;
+    constexpr int WOC = wo_cap_of(NW);
+    constexpr int COLS_PER_WARP = TBN / (EPI_WARPS / 4);
+    constexpr size_t SMEM_WO = smem_wo_of(NW);
+    constexpr size_t SMEM_COLS = smem_cols_of(NW);
     constexpr int STAGES = C::STAGES;
     constexpr int B_BYTES = C::B_BYTES;
     constexpr size_t SMEM_OPERANDS = C::SMEM_OPERANDS;
@@ -271,13 +284,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     pdl_trigger();
     // the live tile count reads the patch counter written by the prologue:
     // only after the dependency wait
-    const TileSpace ts = tile_space(p);
+    const TileSpace ts = tile_space(p, TBN);
     if (threadIdx.x == 0) gstamp(p.dbg, 1);
 
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
             const uint64_t pol = l2_policy_evict_normal();
+            // the group's A panels stay in L2 while the B panels stream past them
+            const uint64_t pol_a = (p.l2_pol & 1) ? l2_policy_evict_last() : pol;
+            const uint64_t pol_b = (p.l2_pol & 2) ? l2_policy_evict_first() : pol;
             int stage = 0;
             uint32_t phase = 0;
             long long w_empty = 0;
@@ -289,8 +305,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const CUtensorMap* map_b = is_patch ? &tmap_p : &tmap_b;
                 const int a_row = m_blk * C::TILE_M + static_cast<int>(pair) * (BM * CG) +
                                   static_cast<int>(crank) * BM;
-                const int b_row = n_blk * BN + static_cast<int>(crank) * C::B_ROWS +
-                                  static_cast<int>(pair) * C::B_LOAD_ROWS;
+                // N-half h of the tile: rows n_blk*TBN + h*BN + crank*(BN/CG) (+ this pair's share)
+                const int b_row = n_blk * TBN + static_cast<int>(crank) * (BN / CG) +
+                                  static_cast<int>(pair) * (C::B_LOAD_ROWS / NW);
                 // this CTA's B piece is multicast to the CTAs of equal crank in every pair
                 uint16_t b_mask = 0;
 #pragma unroll
@@ -307,19 +324,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                         // the pair leader's full barrier counts every byte landing in the pair
                         if (leader) mbar_arrive_expect_tx(&bars->full[stage], CG * C::STAGE_BYTES);
                         tma_load_2d_pair(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES,
-                                         kb * BK, a_row, pol);
+                                         kb * BK, a_row, pol_a);
                         uint8_t* bdst = smem_b + stage * B_BYTES + pair * (C::B_LOAD_ROWS * BK);
                         if constexpr (MC > 1)
                             tma_load_2d_pair_mc(map_b, &bars->full[stage], bdst, kb * BK, b_row,
-                                                b_mask, pol);
+                                                b_mask, pol_b);
                         else
-                            tma_load_2d_pair(map_b, &bars->full[stage], bdst, kb * BK, b_row, pol);
+#pragma unroll
+                            for (int h = 0; h < NW; ++h)  // the tile's N-halves, 16 KB each
+                                tma_load_2d_pair(map_b, &bars->full[stage], bdst + h * (BN / CG) * BK, kb * BK,
+                                                 b_row + h * BN, pol_b);
                     } else {
                         mbar_arrive_expect_tx(&bars->full[stage], C::STAGE_BYTES);
                         tma_load_2d(&tmap_a, &bars->full[stage], smem_a + stage * A_BYTES, kb * BK,
-                                    a_row, pol);
+                                    a_row, pol_a);
                         tma_load_2d(map_b, &bars->full[stage], smem_b + stage * B_BYTES, kb * BK,
-                                    b_row, pol);
+                                    b_row, pol_b);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -341,8 +361,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int u = cluster_id; u < ts.total * p.ksplit; u += n_clusters, ++it) {
             const int sl = u % p.ksplit;
             const int kb0 = sl * p.num_kb / p.ksplit, kb1 = (sl + 1) * p.num_kb / p.ksplit;
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
+            // NW == 1: two 256-column accumulators alternate; NW == 2: one 512-column
+            const int acc = NW == 1 ? (it & 1) : 0;
+            const uint32_t acc_phase = NW == 1 ? ((it >> 1) & 1) : (it & 1);
             if ((kDev && p.dbg != nullptr)) {
                 const long long c0 = clock64();
                 mbar_wait(&bars->tmem_empty[acc], acc_phase ^ 1u);
@@ -368,10 +389,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < BK / UMMA_K; ++k) {
                         const uint64_t ad = a_d + 2 * k;
-                        const uint64_t bd = b_d + 2 * k;
                         const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
-                        if constexpr (CG == 2) mma_i8_pair(d_tmem, ad, bd, idesc, accum);
-                        else mma_i8(d_tmem, ad, bd, idesc, accum);
+#pragma unroll
+                        for (int h = 0; h < NW; ++h) {  // N-half h: B rows h*BN/CG.., TMEM columns h*BN..
+                            const uint64_t bd = b_d + static_cast<uint64_t>(h * ((BN / CG * BK) >> 4)) + 2 * k;
+                            if constexpr (CG == 2) mma_i8_pair(d_tmem + h * BN, ad, bd, idesc, accum);
+                            else mma_i8(d_tmem + h * BN, ad, bd, idesc, accum);
+                        }
                     }
                     // frees the smem slot (in both CTAs of a pair) when the MMAs finish
                     // (with MC > 1 the slot also holds B pieces written by the other
@@ -406,13 +430,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int et = threadIdx.x - EPI_WARP0 * 32;     // 0 .. EPI_THREADS-1
         int n_out = 0;
         if constexpr (EPI != EPI_I32) n_out = p.o_count ? *p.o_count : 0;
-        const bool wo_fast = n_out <= WO_CAP && p.wo != nullptr && n_out <= p.wo_cap;
-        const bool xo_fast = n_out <= WO_CAP && p.xo != nullptr && n_out <= p.o_cap;
-        const bool stage_wo = n_out > 0 && n_out <= WO_CAP;
+        const bool wo_fast = n_out <= WOC && p.wo != nullptr && n_out <= p.wo_cap;
+        const bool xo_fast = n_out <= WOC && p.xo != nullptr && n_out <= p.o_cap;
+        const bool stage_wo = n_out > 0 && n_out <= WOC;
         // staged outlier rows are padded with zeros to a class of 4 / 6 / 8 / 16 so the
         // FMA loop is straight-line code (per-outlier guards made the compiler
         // shuffle the 32 accumulators between registers at every join)
-        const int n_cls = n_out <= 4 ? 4 : (n_out <= 6 ? 6 : (n_out <= 8 ? 8 : WO_CAP));
+        const int n_cls = n_out <= 4 ? 4 : (n_out <= 6 ? 6 : (n_out <= 8 ? 8 : WOC));
         uint32_t stg_cnt = 0;  // TS: output boxes issued by this warp
         __shared__ int split_last;
         long long w_tf = 0;
@@ -421,14 +445,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int t = u / p.ksplit;
             int m_blk, n_blk;
             const bool is_patch = tile_coords(p, ts, t, m_blk, n_blk);
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
+            const int acc = NW == 1 ? (it & 1) : 0;
+            const uint32_t acc_phase = NW == 1 ? ((it >> 1) & 1) : (it & 1);
             const int64_t n_live = is_patch ? ts.patch_n : p.N;
             const float* camax = is_patch ? p.patch_amax : p.col_amax;
             const int32_t* cmap = p.patch_idx;
             const int64_t row = static_cast<int64_t>(m_blk) * C::TILE_M + pair * (BM * CG) +
                                 crank * BM + quad * 32 + lane;
-            const int64_t col0 = static_cast<int64_t>(n_blk) * BN;
+            const int64_t col0 = static_cast<int64_t>(n_blk) * TBN;
             const bool row_ok = row < p.M;
             const bool mapped = is_patch;
 
@@ -438,7 +462,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if constexpr (EPI != EPI_I32) {
                 // ---- stage per-tile column factors and outlier W rows in smem
                 named_bar_sync(1, EPI_THREADS);  // previous tile's readers are done
-                for (int j = et; j < BN; j += EPI_THREADS) {
+                for (int j = et; j < TBN; j += EPI_THREADS) {
                     const int64_t c = col0 + j;
                     const float aw = c < n_live ? amax_or_127(camax[c]) : 127.0f;
                     if constexpr (EPI == EPI_F32_EXACT)
@@ -447,22 +471,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                         reinterpret_cast<float*>(smem_col)[j] = aw * (1.0f / 16129.0f);
                 }
                 if (stage_wo) {
-                    if (wo_fast && !mapped && col0 + BN <= n_live && (p.ldwo % 8) == 0) {
+                    if (wo_fast && !mapped && col0 + TBN <= n_live && (p.ldwo % 8) == 0) {
                         // 16-byte vector loads of the compact outlier rows
-                        for (int i = et; i < n_cls * (BN / 8); i += EPI_THREADS) {
-                            const int o = i / (BN / 8), v = i % (BN / 8);
+                        for (int i = et; i < n_cls * (TBN / 8); i += EPI_THREADS) {
+                            const int o = i / (TBN / 8), v = i % (TBN / 8);
                             const uint4 q = o < n_out ? *reinterpret_cast<const uint4*>(
                                 p.wo + static_cast<int64_t>(o) * p.ldwo + col0 + v * 8) : make_uint4(0, 0, 0, 0);
                             const __half2* h2 = reinterpret_cast<const __half2*>(&q);
-                            float4* dst = reinterpret_cast<float4*>(smem_wo + o * BN + v * 8);
+                            float4* dst = reinterpret_cast<float4*>(smem_wo + o * TBN + v * 8);
                             const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]);
                             const float2 f2 = __half22float2(h2[2]), f3 = __half22float2(h2[3]);
                             dst[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
                             dst[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
                         }
                     } else {
-                        for (int i = et; i < n_cls * BN; i += EPI_THREADS) {
-                            const int o = i / BN, j = i % BN;
+                        for (int i = et; i < n_cls * TBN; i += EPI_THREADS) {
+                            const int o = i / TBN, j = i % TBN;
                             const int64_t c = col0 + j;
                             float v = 0.0f;
                             if (c < n_live && o < n_out) {
@@ -470,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 v = wo_fast ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + gc])
                                             : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + gc]);
                             }
-                            smem_wo[o * BN + j] = v;
+                            smem_wo[o * TBN + j] = v;
                         }
                     }
                 }
@@ -480,7 +504,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 sx = 127.0 / static_cast<double>(ax);
                 if (stage_wo) {
 #pragma unroll
-                    for (int o = 0; o < WO_CAP; ++o) {
+                    for (int o = 0; o < WOC; ++o) {
                         float v = 0.0f;
                         if (o < n_out && row_ok)
                             v = xo_fast ? __half2float(p.xo[row * p.o_cap + o])
@@ -569,10 +593,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (n_out > 0 && !(kDev && (p.dbg_epi & 1))) {
                             if (stage_wo) {
                                 const float* wrow = smem_wo + ch * 32;
-                                if (n_cls == 4) outlier_fma<4>(v2, xo_r, wrow);
-                                else if (n_cls == 6) outlier_fma<6>(v2, xo_r, wrow);
-                                else if (n_cls == 8) outlier_fma<8>(v2, xo_r, wrow);
-                                else outlier_fma<WO_CAP>(v2, xo_r, wrow);
+                                if (n_cls == 4) outlier_fma<4, TBN>(v2, xo_r, wrow);
+                                else if (n_cls == 6) outlier_fma<6, TBN>(v2, xo_r, wrow);
+                                else if (n_cls == 8) outlier_fma<8, TBN>(v2, xo_r, wrow);
+                                else outlier_fma<WOC, TBN>(v2, xo_r, wrow);
                             } else {
                                 for (int o = 0; o < n_out; ++o) {
                                     const int64_t k = p.o_idx[o];
@@ -688,8 +712,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t c32_col = (is_patch ? static_cast<int64_t>(ts.n_tiles) * BN : 0) +
                                     static_cast<int64_t>(n_blk) * BN;
 #pragma unroll 1
-            for (int cc = 0; cc < COLS_PER_EPI_WARP / 32; ++cc) {
-                const int ch = half * (COLS_PER_EPI_WARP / 32) + cc;
+            for (int cc = 0; cc < COLS_PER_WARP / 32; ++cc) {
+                const int ch = half * (COLS_PER_WARP / 32) + cc;
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(t_row + ch * 32, r);
                 tmem_ld_wait();
@@ -720,8 +744,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (split_last) {
                         __threadfence();
 #pragma unroll 1
-                        for (int cc = 0; cc < COLS_PER_EPI_WARP / 32; ++cc) {
-                            const int ch = half * (COLS_PER_EPI_WARP / 32) + cc;
+                        for (int cc = 0; cc < COLS_PER_WARP / 32; ++cc) {
+                            const int ch = half * (COLS_PER_WARP / 32) + cc;
                             uint32_t r[32];
                             int32_t* cr = p.c32 + (c32_col + ch * 32) * p.c32_rows + (row_ok ? row : 0);
 #pragma unroll
@@ -809,14 +833,15 @@ static bool make_tmap_f16_out(CUtensorMap* map, void* base, int64_t rows, int64_
     return r == CUDA_SUCCESS;
 }
 
-template <int EPI, int CG, int MC>
+template <int EPI, int CG, int MC, int NW>
 static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tp,
                               const CUtensorMap& ty, const Params& p, int64_t max_tiles,
                               cudaStream_t st) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     static int max_clusters = 0;
-    constexpr size_t smem = smem_total<CG, MC, EPI == EPI_F16 && CG == 2>();
+    constexpr size_t smem = smem_total<CG, MC, EPI == EPI_F16 && CG == 2, NW>();
+    static_assert(smem <= 227 * 1024, "shared memory");
     constexpr int CL = CG * MC;
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(THREADS);
@@ -832,7 +857,7 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(gemm_i8_kernel<EPI, CG, MC>,
+        attr_err = cudaFuncSetAttribute(gemm_i8_kernel<EPI, CG, MC, NW>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem));
         // how many clusters of this shape the GPC layout can co-schedule
@@ -840,7 +865,7 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
         q.gridDim = dim3(static_cast<unsigned>(num_sms() / CL * CL));
         int n = 0;
         if (attr_err == cudaSuccess &&
-            cudaOccupancyMaxActiveClusters(&n, gemm_i8_kernel<EPI, CG, MC>, &q) == cudaSuccess && n > 0)
+            cudaOccupancyMaxActiveClusters(&n, gemm_i8_kernel<EPI, CG, MC, NW>, &q) == cudaSuccess && n > 0)
             max_clusters = n;
         else
             max_clusters = num_sms() / CL;
@@ -858,7 +883,7 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
     }
     cfg.gridDim = dim3(static_cast<unsigned>(clusters * CL));
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC>, ta, tb, tp, ty, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_i8_kernel<EPI, CG, MC, NW>, ta, tb, tp, ty, p);
     count_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -867,10 +892,11 @@ static cudaError_t launch_epi(const CUtensorMap& ta, const CUtensorMap& tb, cons
 template <int EPI>
 static cudaError_t launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tp,
                              const CUtensorMap& ty, const Params& p, int64_t max_tiles, int cg,
-                             int mc, cudaStream_t st) {
-    if (cg == 2 && mc == 2) return launch_epi<EPI, 2, 2>(ta, tb, tp, ty, p, max_tiles, st);
-    if (cg == 2) return launch_epi<EPI, 2, 1>(ta, tb, tp, ty, p, max_tiles, st);
-    return launch_epi<EPI, 1, 1>(ta, tb, tp, ty, p, max_tiles, st);
+                             int mc, int nw, cudaStream_t st) {
+    if (cg == 2 && mc == 2) return launch_epi<EPI, 2, 2, 1>(ta, tb, tp, ty, p, max_tiles, st);
+    if (cg == 2 && nw == 2) return launch_epi<EPI, 2, 1, 2>(ta, tb, tp, ty, p, max_tiles, st);
+    if (cg == 2) return launch_epi<EPI, 2, 1, 1>(ta, tb, tp, ty, p, max_tiles, st);
+    return launch_epi<EPI, 1, 1, 1>(ta, tb, tp, ty, p, max_tiles, st);
 }
 
 }  // namespace gemm
@@ -912,6 +938,17 @@ static int gemm_mc_override() {
     if (g_mc_override < 0) g_mc_override = env_int("I8MM_GEMM_MC");
     return g_mc_override;
 }
+// 512-wide pair tiles: env I8MM_GEMM_WIDE = 1 forces, 2 forbids; default by shape
+static bool gemm_wide_mode(int64_t M, int64_t N, int64_t K) {
+    const int e = env_int("I8MM_GEMM_WIDE");
+    if (e == 1) return true;
+    if (e == 2) return false;
+    // its epilogue cannot overlap the next tile's MMAs (one 512-column accumulator),
+    // so it pays only when the K loop is long (measured, scripts/gemm_wide_ab.sh:
+    // cfg5 fc2 K = 49152 +15 %, cfg5 fc1 K = 12288 -4 %, cfg4 fc1 K = 9216 -8 %)
+    return M >= 2048 && N >= 2 * BN && K >= 32768;
+}
+
 void set_gemm_variant(int cg, int mc) {
     g_cg_override = cg;
     g_mc_override = mc;
@@ -961,6 +998,11 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     // (profiles/) it does not beat plain pairs, so it is opt-in (I8MM_GEMM_MC=2).
     const int cg = (a.M > BM && gemm_cg_override() != 1) ? 2 : 1;
     const int mc = (cg == 2 && a.M >= 2048 && gemm_mc_override() == 2) ? 2 : 1;
+    // 256 x 512 pair tiles (two N=256 MMAs share each A panel: 0.75x the L2 -> SM
+    // bytes of 256 x 256, the ceiling of this GEMM at full clock) when the
+    // layer is big enough in N and K for one accumulator without epilogue overlap
+    const int nw = (cg == 2 && mc == 1 && gemm_wide_mode(a.M, a.N, a.K)) ? 2 : 1;
+    const int tbn = BN * nw;
     CUtensorMap ta, tb;
     const int64_t kdim = a.K > 0 ? a.K : 16;
     if (!make_tmap_i8(&ta, a.a, a.M, kdim, a.lda, BM)) return cudaErrorInvalidValue;
@@ -978,7 +1020,7 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     p.m_tiles = static_cast<int>((a.M + BM * cg * mc - 1) / (BM * cg * mc));
     // upper bound on tiles (patches at most double the N-tiles); the kernel
     // computes the live count on the device
-    const int64_t max_tiles = static_cast<int64_t>(p.m_tiles) * ((a.N + BN - 1) / BN) *
+    const int64_t max_tiles = static_cast<int64_t>(p.m_tiles) * ((a.N + tbn - 1) / tbn) *
                               (a.patch_count != nullptr ? 2 : 1);
     p.y = a.y;
     p.ldy = a.ldy;
@@ -1032,7 +1074,7 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
         // A panels (GROUP_M x TILE_M x K bytes) stay within ~32 MB of L2 while
         // the B panels stream past them.
         const int gm_env = env_int("I8MM_GROUP_M");
-        const int64_t n_tiles = (a.N + BN - 1) / BN;
+        const int64_t n_tiles = (a.N + tbn - 1) / tbn;
         const int64_t wave = num_sms() / (cg * mc);
         int gm;
         if (n_tiles * 2 <= wave) {
@@ -1044,16 +1086,20 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
             while (gm * 2 <= g && gm < 32) gm *= 2;
         }
         p.group_m = gm_env > 0 ? gm_env : gm;
+        const int pol_env = env_int("I8MM_GEMM_L2POL");
+        // bit 0: A panels evict_last, bit 1: B panels evict_first (measured: B panels
+        // are reused by the group's m-tiles, evict_first on them costs ~10 %)
+        p.l2_pol = pol_env > 0 ? pol_env : 0;
     }
     CUtensorMap ty = ta;
     p.tma_y = 0;
     if (epi == EPI_F16 && p.vec_store && env_int("I8MM_NO_TMA_STORE") != 1)
         p.tma_y = make_tmap_f16_out(&ty, a.y, a.M, a.N, a.ldy) ? 1 : 0;
     switch (epi) {
-        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
-        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
-        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
-        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, tp, ty, p, max_tiles, cg, mc, st);
+        case EPI_I32: return launch_cg<EPI_I32>(ta, tb, tp, ty, p, max_tiles, cg, mc, nw, st);
+        case EPI_F16: return launch_cg<EPI_F16>(ta, tb, tp, ty, p, max_tiles, cg, mc, nw, st);
+        case EPI_F32: return launch_cg<EPI_F32>(ta, tb, tp, ty, p, max_tiles, cg, mc, nw, st);
+        case EPI_F32_EXACT: return launch_cg<EPI_F32_EXACT>(ta, tb, tp, ty, p, max_tiles, cg, mc, nw, st);
         default: return cudaErrorInvalidValue;
     }
 }
