@@ -946,7 +946,7 @@ static bool gemm_wide_mode(int64_t M, int64_t N, int64_t K) {
     // its epilogue cannot overlap the next tile's MMAs (one 512-column accumulator),
     // so it pays only when the K loop is long (measured, scripts/gemm_wide_ab.sh:
     // cfg5 fc2 K = 49152 +15 %, cfg5 fc1 K = 12288 -4 %, cfg4 fc1 K = 9216 -8 %)
-    return M >= 2048 && N >= 2 * BN && K >= 32768;
+    return M >= 2048 && N >= 2 * gemm::BN && K >= 32768;
 }
 
 void set_gemm_variant(int cg, int mc) {
