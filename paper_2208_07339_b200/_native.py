@@ -196,6 +196,8 @@ def load_library(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    if path is None and os.environ.get("I8MM_LIB_ALT"):  # dev A/B against another build
+        path = os.environ["I8MM_LIB_ALT"]
     p = Path(path) if path else LIB_PATH
     if not p.exists():
         raise NativeLibraryError(

@@ -389,13 +389,20 @@ __device__ void compact_mask(const uint32_t* __restrict__ smask, int64_t nwords,
 // 16 token columns of this thread's weight row: sum of the n_used accumulators
 // the segment wrote (min(N_ACC, 4 x its units))
 __device__ __forceinline__ void tmem_row16(uint32_t taddr, int n_used, uint32_t (&r)[16]) {
-    tmem_ld_32x32b_x16(taddr, r);
-    for (int j = 1; j < n_used; ++j) {
-        uint32_t t[16];
-        tmem_ld_32x32b_x16(taddr + static_cast<uint32_t>(j * MPAD), t);
+    // accumulator pairs (32 consecutive columns) per load, one wait per pair: a
+    // wait per accumulator made the sum a chain of n_used TMEM round trips
+    if (n_used & 1) {
+        tmem_ld_32x32b_x16(taddr, r);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] = 0u;
+    }
+    for (int j = n_used & 1; j < n_used; j += 2) {
+        uint32_t t[32];
+        tmem_ld_32x32b_x32(taddr + static_cast<uint32_t>(j * MPAD), t);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) r[e] += t[e];
+        for (int e = 0; e < 16; ++e) r[e] += t[e] + t[16 + e];
     }
     tmem_ld_wait();
 }

@@ -19,7 +19,8 @@ from . import _native as nat
 
 
 class GraphedCall:
-    def __init__(self, fn: Callable, *static_inputs: torch.Tensor, warmup: int = 3) -> None:
+    def __init__(self, fn: Callable, *static_inputs: torch.Tensor, warmup: int = 3,
+                 keep_graph: bool = False) -> None:
         self.fn = fn
         self.static_inputs = static_inputs
         side = torch.cuda.Stream()
@@ -29,9 +30,13 @@ class GraphedCall:
                 fn(*static_inputs)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
+        self.graph = torch.cuda.CUDAGraph(keep_graph=keep_graph)  # keep: raw_cuda_graph() (tests)
         n0 = nat.launch_count()
-        with torch.cuda.graph(self.graph):
+        # captured on the warm-up stream: per-stream state the warm-up created
+        # (decode workspaces, initialised once) is reused, so no initialisation
+        # node (a memset between two kernels breaks their programmatic edge)
+        # lands in the graph
+        with torch.cuda.graph(self.graph, stream=side):
             self.output = fn(*static_inputs)
         self.kernels = nat.launch_count() - n0  # library kernels replayed per call
 

@@ -139,7 +139,10 @@ class Int8Linear(torch.nn.Module):
         """A workspace for an M-row call. Prefill routing: a fresh buffer.
         Decode routing: cached per (M, stream), initialised once
         (``i8mm_linear_workspace_init``: its per-tile arrival counters must be
-        zero on first use; every decode call leaves them zero)."""
+        zero on first use; every decode call leaves them zero). A workspace
+        first created while a CUDA graph is being captured puts that
+        initialisation into the graph; ``GraphedCall`` captures on its warm-up
+        stream so the graph holds only the layer kernels."""
         L = nat.lib()
         k, n = self.weight.shape
         if not self.uses_decode(m):

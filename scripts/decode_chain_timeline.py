@@ -29,6 +29,8 @@ if graph:  # the bench's form: one CUDA graph of the step (PDL edges between the
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
+        for _ in range(2):  # this stream's decode workspaces exist before the capture
+            run.step()
         with torch.cuda.graph(g, stream=s):
             for mod, x, b in zip(run.mods, run.xs, bufs):
                 L.i8mm_debug_decode_timeline(b.data_ptr())
@@ -67,7 +69,7 @@ cols = [(0, "start", min), (0, "start (last CTA)", max), (1, "waited", max), (2,
         (6, "MMA issued", max)] + [(19, "setup: bars+W", max), (20, "setup: pdl wait", max), (21, "setup: X issued", max),
         (22, "setup: L2 pf+dst", max), (23, "setup: tmem alloc", max), (24, "setup: cand loads", max),
         (25, "setup: zeroing", max)] + [ (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]
-print("us from layer q's prep start (min or max over CTAs)")
+print("us from layer q's prep start (min or max over CTAs); CTAs per layer:", [int((g[:, 0] > 0).sum()) for g in G])
 print(f"{'':18s}" + "".join(f"{n:>8s}" for n in names))
 med = lambda v: v.median()
 for i, lab, f in cols:
