@@ -276,6 +276,7 @@ struct Params {
     int64_t xs_ld;       // halves per cached X-slice row
     int64_t total_units;
     unsigned long long* dbg;  // per-CTA %globaltimer stamps (dev tool), nullable
+    int end_sync;             // A/B (I8MM_DECODE_END_SYNC=1): closing cluster barrier
     int dbg_mode;             // dev build A/B: bit 0 local panel stores only, bit 1 no code math, bit 2 no Xq copy,
                               // bit 3 no token phase at all
 };
@@ -1069,9 +1070,12 @@ roles:
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
     }
-    // no CTA leaves while a cluster peer may still add into its racc / arrive on
-    // its pbar (the finisher's wait already implies it; this makes it explicit)
-    cluster_sync_all();
+    // No closing cluster barrier: after barrier 2 the only distributed-shared-
+    // memory traffic is contributors adding into a finisher's racc and arriving
+    // on its pbar, and the finisher leaves only after that wait. The other CTAs
+    // of the cluster leave as soon as they are done, so the next layer's
+    // clusters (programmatic dependent launch) find free SMs earlier.
+    if (p.end_sync) cluster_sync_all();
     DSTAMP(p.dbg, 9);
 }
 
@@ -1229,6 +1233,8 @@ cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st) {
     prm.slots = g.slots;
     prm.xs_cached = g.xs_cached;
     prm.xs_ld = g.xs_ld;
+    static const int env_es = env_int_once("I8MM_DECODE_END_SYNC", 0);
+    prm.end_sync = env_es;
     prm.dbg = g_dbg;
     static const int env_dbg = env_int_once("I8MM_DECODE_DBG_MODE", 0);
     prm.dbg_mode = env_dbg;

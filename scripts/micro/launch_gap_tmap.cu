@@ -35,6 +35,7 @@ __device__ __forceinline__ void body(const void* map, unsigned long long* t, int
     if (mode & 1) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        if (threadIdx.x == 0) atomicMax(&t[32 + which], gt());
     }
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar)), "r"(16384) : "memory");
@@ -104,6 +105,7 @@ int main(int argc, char** argv) {
             cudaGraphExec_t ge;
             unsigned long long init[16];
             for (int i = 0; i < 16; ++i) init[i] = (i % 2 == 0) ? ~0ull : 0ull;
+            cudaMemset(t + 32, 0, 8 * 8);
             cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
             for (int wi = 0; wi < 6; ++wi) {
                 cudaLaunchConfig_t cfg{};
@@ -141,6 +143,12 @@ int main(int argc, char** argv) {
             cudaMemcpy(h, t, sizeof(h), cudaMemcpyDeviceToHost);
             printf("%s pdl %d: gaps us:", variant == 1 ? "global tmap" : variant == 2 ? "param+1.2KB" : "param tmap ", mode);
             for (int wi = 1; wi < 6; ++wi) printf(" %.2f", (double)((long long)h[2 * wi] - (long long)h[2 * wi - 1]) / 1e3);
+            if (mode) {
+                unsigned long long h2[8];
+                cudaMemcpy(h2, t + 32, sizeof(h2), cudaMemcpyDeviceToHost);
+                printf("  | wait released after prev end (max over CTAs) us:");
+                for (int wi = 1; wi < 6; ++wi) printf(" %.2f", (double)((long long)h2[wi] - (long long)h[2 * wi - 1]) / 1e3);
+            }
             printf("  err=%s\n", cudaGetErrorString(cudaGetLastError()));
         }
 }
