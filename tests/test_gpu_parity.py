@@ -440,7 +440,9 @@ def decode_max(p):
     (13, 13, 1001, 257, 4, 1), (14, 12, 4096, 1024, 8, 3), (15, 16, 768, 2050, 6, 0),
     (16, 9, 512, 600, 20, 5), (17, 15, 1536, 768, 6, 2), (18, 3, 256, 520, 70, 0),
     (19, 11, 8192, 136, 2, 2), (20, 14, 1024, 2000, 6, 6), (21, 2, 20480, 384, 6, 1),
-    (22, 7, 130, 4000, 3, 2)])
+    (22, 7, 130, 4000, 3, 2),
+    # more n-tiles than clusters, >= 8 k-blocks, ragged K
+    (23, 8, 2048, 4000, 6, 3), (24, 16, 3000, 5000, 8, 2), (25, 1, 1024, 1920, 6, 4)])
 def test_decode_path_vs_oracle_and_prefill(p, oracle_mod, decode_max, case):
     """The decode kernel (8-CTA clusters: token side in distributed shared
     memory + swap-AB stream-K tcgen05 GEMM): exact output bit-identical to the
