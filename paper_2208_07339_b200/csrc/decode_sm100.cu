@@ -494,29 +494,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                         (u / num_kb) * TILE_N, pol_w);
         }
     }
-    if (tid == 0) DSTAMP(p.dbg, 19);
-    // X and the workspace (written / read by the preceding kernels) after the wait
-    pdl_wait();
-    pdl_trigger();
-    if (tid == 0) DSTAMP(p.dbg, 20);
-    if (bulk && tid == 0) {
-        const uint32_t row_bytes = static_cast<uint32_t>(nfull) * 16u;
-        if (row_bytes > 0) {
-            mbar_arrive_expect_tx(&bars->xbar, row_bytes * static_cast<uint32_t>(M));
-            for (int64_t m = 0; m < M; ++m) bulk_load_1d(xs + m * xs_ld, a.x + m * a.ldx + c0, row_bytes, &bars->xbar);
-        } else {
-            mbar_arrive(&bars->xbar);
-        }
-    }
-    if (tid == 0) DSTAMP(p.dbg, 21);
-    // the rest of this CTA's weight tiles -> L2 now: a CTA's TMA engine keeps only
-    // a few tiles in flight, L2 prefetches have no such cap, so HBM streams the
-    // layer at full rate under the token phase and the ring's later loads hit L2
-    if (warp == 3 && p.l2_prefetch)
-        for (int i = min(p.pre, L) + lane; i < L; i += 32) {
-            const int u = u_begin + i;
-            tma_prefetch_l2_2d(&tmap_w, (u % num_kb) * BK, (u / num_kb) * TILE_N);
-        }
+    // Everything up to the dependency wait touches only this call's immutable
+    // inputs (the cached codes and candidates, written by i8mm_linear_prepare,
+    // whose kernels never trigger early) and shared memory, so it overlaps the
+    // preceding kernel's tail: CTAs of this grid start on SMs as they free up.
     // panel destinations of this rank's k-blocks: slot in each rank's panel, or -1
     for (int i = tid; i < (kb_hi - kb_lo) * CL; i += THREADS) {
         const int kbi = i / CL, q = i - kbi * CL;
@@ -559,16 +540,34 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     if (tid == 128) DSTAMP(p.dbg, 24);
-    // token rows M..15 of every panel slot stay zero
-    for (int i = tid; i < p.slots * (MPAD - static_cast<int>(M)) * 8; i += THREADS) {
-        const int per = (MPAD - static_cast<int>(M)) * 8;
-        const int sl = i / per, rr = i - sl * per;
-        *reinterpret_cast<uint4*>(panel + static_cast<size_t>(sl) * B_BYTES + (M + rr / 8) * BK + (rr & 7) * 16) =
-            make_uint4(0u, 0u, 0u, 0u);
-    }
+    // (token rows M..15 of the panel slots are left as they are: they only feed
+    // accumulator columns m >= M, which no path reads)
     for (int64_t w = w0 + tid; w < w1; w += THREADS) smask[w] = 0u;
     if (fin_local > 0)  // contributors add into it after cluster barrier 2
         for (int i = tid; i < static_cast<int>(M) * TILE_N; i += THREADS) racc[i] = 0;
+    if (tid == 0) DSTAMP(p.dbg, 19);
+    // X and the workspace (written / read by the preceding kernels) after the wait
+    pdl_wait();
+    pdl_trigger();
+    if (tid == 0) DSTAMP(p.dbg, 20);
+    if (bulk && tid == 0) {
+        const uint32_t row_bytes = static_cast<uint32_t>(nfull) * 16u;
+        if (row_bytes > 0) {
+            mbar_arrive_expect_tx(&bars->xbar, row_bytes * static_cast<uint32_t>(M));
+            for (int64_t m = 0; m < M; ++m) bulk_load_1d(xs + m * xs_ld, a.x + m * a.ldx + c0, row_bytes, &bars->xbar);
+        } else {
+            mbar_arrive(&bars->xbar);
+        }
+    }
+    if (tid == 0) DSTAMP(p.dbg, 21);
+    // the rest of this CTA's weight tiles -> L2 now: a CTA's TMA engine keeps only
+    // a few tiles in flight, L2 prefetches have no such cap, so HBM streams the
+    // layer at full rate under the token phase and the ring's later loads hit L2
+    if (warp == 3 && p.l2_prefetch)
+        for (int i = min(p.pre, L) + lane; i < L; i += 32) {
+            const int u = u_begin + i;
+            tma_prefetch_l2_2d(&tmap_w, (u % num_kb) * BK, (u / num_kb) * TILE_N);
+        }
     if (bulk && nv > nfull)  // ragged last vector (K % 8 != 0): element loads
         for (int64_t m = tid; m < M; m += THREADS)
             *reinterpret_cast<uint4*>(xs + m * xs_ld + nfull * 8) = load8(a.x + m * a.ldx, c0 + nfull * 8, K, false);
@@ -699,6 +698,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             u = seg_end;
         }
     }
+    if (tid == 128) DSTAMP(p.dbg, 17);  // warps 4-7 done with the L2 prefetches
     const int nkb = kb_hi - kb_lo;
     // codes of this rank's k-blocks: item = (k-block, row, 16-column chunk); row
     // and chunk from a multiply-shift (exact for the ranges here: rest < 2^13)
@@ -738,6 +738,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     if (tid == 0) DSTAMP(p.dbg, 15);
+    if (tid == 128) DSTAMP(p.dbg, 28);  // warp 4 codes done (dev: slot shared with the 3rd segment entry count)
     asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");  // panels feed tcgen05.mma
     if (tid == 0) DSTAMP(p.dbg, 16);
     if (lead) {

@@ -65,7 +65,7 @@ names = ["q", "k", "v", "o", "fc1", "fc2"]
 cols = [(0, "start", min), (0, "start (last CTA)", max), (1, "waited", max), (2, "X landed", max),
         (10, "flags", max), (11, "cluster wait", max), (12, "partials pushed", max), (13, "mask pushed", max),
         (3, "cluster barrier 1", max), (14, "row scales", max), (15, "codes pushed", max), (16, "proxy fence", max),
-        (17, "o-list", max), (18, "lead writes", max), (4, "panels ready", max), (5, "1st MMA", max),
+        (17, "w4 prefetch done", max), (28, "w4 codes done", max), (18, "lead writes", max), (4, "panels ready", max), (5, "1st MMA", max),
         (6, "MMA issued", max)] + [(19, "setup: bars+W", max), (20, "setup: pdl wait", max), (21, "setup: X issued", max),
         (22, "setup: L2 pf+dst", max), (23, "setup: tmem alloc", max), (24, "setup: cand loads", max),
         (25, "setup: zeroing", max)] + [ (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]
