@@ -196,7 +196,7 @@ void i8mm_debug_set_decode_max_m(int max_m);
    (same as I8MM_PDL=0); for A/B measurements. */
 void i8mm_debug_set_pdl(int on);
 int i8mm_linear_uses_decode(int64_t M, int64_t K, int64_t N);
-/* Dev tool: per-CTA %globaltimer stamps of the decode kernel (32 u64 per CTA,
+/* Dev tool: per-CTA %globaltimer stamps of the decode kernel (64 u64 per CTA,
  * device buffer sized for one CTA per SM; NULL disables). */
 void i8mm_debug_decode_timeline(void* stamps);
 /* Fused output all-gather for N-sharded layers (fp16 out): like

@@ -108,7 +108,7 @@ constexpr bool kDevStamps = false;
 #endif
 #define DSTAMP(ptr, i)                                                                 \
     do {                                                                               \
-        if (kDevStamps && (ptr) != nullptr) (ptr)[blockIdx.x * 32 + (i)] = gtimer(); \
+        if (kDevStamps && (ptr) != nullptr) (ptr)[blockIdx.x * 64 + (i)] = gtimer(); \
     } while (0)
 
 // 8 consecutive fp16 of a row starting at `col` (zeros past K); 16-byte load
@@ -204,8 +204,8 @@ __device__ __forceinline__ float fixup_amax(const int32_t (&cr)[kTopT], const ui
 // runs at 8 warps per SM, so it is latency-bound: the 16 fast roundings are
 // straight-line, independent chains (code_fast without its branch), and the
 // exact f64 tie-break runs afterwards for the ~1e-4 of elements that need it.
-__device__ __noinline__ uint32_t codes16_fixup(uint32_t word, uint32_t bad, const uint4& lo, const uint4& hi,
-                                               int base, double s) {
+__device__ __noinline__ uint32_t codes16_fixup(uint32_t word, uint32_t bad, uint4 lo, uint4 hi, int base,
+                                               double s) {  // by value: no stack copy of lo / hi per item
     for (int e = base; e < base + 4; ++e)
         if ((bad >> e) & 1u) {
             const float x = hbits_to_float(half_bits(e < 8 ? lo : hi, e & 7));
@@ -704,7 +704,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     // and chunk from a multiply-shift (exact for the ranges here: rest < 2^13)
     const uint32_t m8 = static_cast<uint32_t>(M) * 8u;
     const uint32_t inv_m8 = (1u << 20) / m8 + 1u;
+    // every rank's panel base in the cluster window, computed once: a store is
+    // then base + slot offset, with no per-store address translation
+    uint32_t peer_panel[CL];
+#pragma unroll
+    for (int q = 0; q < CL; ++q) peer_panel[q] = mapa_shared(panel, static_cast<uint32_t>(q));
     for (int it = tid; it < nkb * static_cast<int>(m8); it += THREADS) {
+        if (tid == 0 && it == 0) DSTAMP(p.dbg, 32);
+        if (tid == 0 && it == THREADS) DSTAMP(p.dbg, 34);
         const int kbi = static_cast<int>((static_cast<uint32_t>(it) * inv_m8) >> 20);
         const int rem = it - kbi * static_cast<int>(m8);
         const int m = rem >> 3, ch = rem & 7;
@@ -722,19 +729,28 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             const uint32_t mbits = (smask[k0 >> 5] >> (k0 & 31)) & 0xFFFFu;
             code = codes16(lo, hi, mbits, k0, K, sscale32[m], sscale[m]);
+            if (tid == 0 && it == 0) DSTAMP(p.dbg, 33);
             if (lead && !(kDevStamps && (p.dbg_mode & 4)))
                 *reinterpret_cast<uint4*>(a.xq + m * a.ldq + k0) = code;  // workspace Xq (views)
         }
         const uint32_t off = static_cast<uint32_t>(m * BK + ((ch ^ (m & 7)) * 16));
-        const int16_t* dst = sdst + kbi * CL;
+        // the k-block's destination slots, read once (CL int16 = one 16-byte row
+        // for CL = 8): the stores below carry no memory clobber, so nothing
+        // forces a re-read between them (the proxy fence and cluster barrier 2
+        // order them before any use)
+        int16_t dsl[CL];
+#pragma unroll
+        for (int q = 0; q < CL; ++q) dsl[q] = sdst[kbi * CL + q];
 #pragma unroll
         for (int q = 0; q < CL; ++q) {
-            const int slot = dst[q];
+            const int slot = dsl[q];
             if (slot < 0) continue;
             if (kDevStamps && (p.dbg_mode & 1))
                 *reinterpret_cast<uint4*>(panel + static_cast<size_t>(slot) * B_BYTES + off) = code;
             else
-                st_cluster_v4(mapa_shared(panel + static_cast<size_t>(slot) * B_BYTES + off, q), code);
+                asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                 peer_panel[q] + static_cast<uint32_t>(slot) * B_BYTES + off),
+                             "r"(code.x), "r"(code.y), "r"(code.z), "r"(code.w));
         }
     }
     if (tid == 0) DSTAMP(p.dbg, 15);
@@ -897,7 +913,7 @@ roles:
             }
             named_bar_sync(1, 128);
             const int n_ent = bars->n_ent;
-            if (kDevStamps && et == 0 && p.dbg != nullptr) p.dbg[blockIdx.x * 32 + 26 + min(seg, 2)] = n_ent;
+            if (kDevStamps && et == 0 && p.dbg != nullptr) p.dbg[blockIdx.x * 64 + 26 + min(seg, 2)] = n_ent;
             if (n_ent > 0) {
                 // every cached candidate an outlier row (rare): scan the column, warp per entry
                 for (int e = quad; e < n_ent; e += 4) {
@@ -1043,7 +1059,7 @@ roles:
                 if (et == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.tile_cnt + tile) : "memory");
                 continue;
             }
-            if (kDevStamps && et == 0 && p.dbg != nullptr) p.dbg[blockIdx.x * 32 + 29 + min(seg, 2)] = full ? 2 : (cf != blockIdx.x ? 0 : 1);
+            if (kDevStamps && et == 0 && p.dbg != nullptr) p.dbg[blockIdx.x * 64 + 29 + min(seg, 2)] = full ? 2 : (cf != blockIdx.x ? 0 : 1);
             if (!full) {  // finisher: the contributors' partials (this cluster's in racc, the others' global)
                 if (fin_local > 0) {
                     mbar_wait_cluster(&bars->pbar, 0);

@@ -19,7 +19,7 @@ import bench  # noqa: E402
 L = nat.lib()
 run = bench.WorkloadRun("cfg3_decode", "cuda", False)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-bufs = [torch.zeros(sms * 32, dtype=torch.int64, device="cuda") for _ in run.layers]
+bufs = [torch.zeros(sms * 64, dtype=torch.int64, device="cuda") for _ in run.layers]
 for _ in range(5):
     run.step()
 torch.cuda.synchronize()
@@ -49,7 +49,7 @@ else:
         mod(x)
     L.i8mm_debug_decode_timeline(None)
 torch.cuda.synchronize()
-G = [b.view(sms, 32).cpu().double() for b in bufs]
+G = [b.view(sms, 64).cpu().double() for b in bufs]
 t0 = G[0][:, 0][G[0][:, 0] > 0].min()
 
 
@@ -65,7 +65,7 @@ names = ["q", "k", "v", "o", "fc1", "fc2"]
 cols = [(0, "start", min), (0, "start (last CTA)", max), (1, "waited", max), (2, "X landed", max),
         (10, "flags", max), (11, "cluster wait", max), (12, "partials pushed", max), (13, "mask pushed", max),
         (3, "cluster barrier 1", max), (14, "row scales", max), (15, "codes pushed", max), (16, "proxy fence", max),
-        (17, "w4 prefetch done", max), (28, "w4 codes done", max), (18, "lead writes", max), (4, "panels ready", max), (5, "1st MMA", max),
+        (17, "w4 prefetch done", max), (28, "w4 codes done", max), (32, "t0 item0 start", max), (33, "t0 item0 codes", max), (34, "t0 item1 start", max), (18, "lead writes", max), (4, "panels ready", max), (5, "1st MMA", max),
         (6, "MMA issued", max)] + [(19, "setup: bars+W", max), (20, "setup: pdl wait", max), (21, "setup: X issued", max),
         (22, "setup: L2 pf+dst", max), (23, "setup: tmem alloc", max), (24, "setup: cand loads", max),
         (25, "setup: zeroing", max)] + [ (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]

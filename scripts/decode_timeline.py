@@ -23,7 +23,7 @@ L.i8mm_debug_set_decode_max_m(256)
 x, w, _ = planted_pair_device(m, k, n, 6, 20.0, seed=3, device="cuda")
 lin = pkg.Int8Linear(w, 6.0, check_finite=False)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-g = torch.zeros(sms * 32, dtype=torch.int64, device="cuda")
+g = torch.zeros(sms * 64, dtype=torch.int64, device="cuda")
 for _ in range(3):
     lin(x)
 torch.cuda.synchronize()
@@ -34,7 +34,7 @@ L.i8mm_debug_decode_timeline(g.data_ptr())
 lin(x)
 torch.cuda.synchronize()
 L.i8mm_debug_decode_timeline(None)
-G = g.view(sms, 32).cpu().double()
+G = g.view(sms, 64).cpu().double()
 t0 = G[:, 0][G[:, 0] > 0].min()
 
 
