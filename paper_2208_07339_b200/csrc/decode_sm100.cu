@@ -145,6 +145,9 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, const uint4& v) {
 __device__ __forceinline__ void cluster_arrive_relaxed() {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive_release() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
@@ -276,7 +279,6 @@ struct Params {
     int64_t xs_ld;       // halves per cached X-slice row
     int64_t total_units;
     unsigned long long* dbg;  // per-CTA %globaltimer stamps (dev tool), nullable
-    int end_sync;             // A/B (I8MM_DECODE_END_SYNC=1): closing cluster barrier
     int dbg_mode;             // dev build A/B: bit 0 local panel stores only, bit 1 no code math, bit 2 no Xq copy,
                               // bit 3 no token phase at all
 };
@@ -863,6 +865,17 @@ roles:
             const int m = i / n_o, o = i - m * n_o;
             sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
         }
+        // closing barrier, split: a CTA adds into a peer's shared memory only in its
+        // first segment, and only when that segment continues a tile an earlier CTA of
+        // this cluster started; every other epilogue thread arrives right away (the
+        // wait is at the very end)
+        bool arrived = true;
+        {
+            const uint32_t t0 = static_cast<uint32_t>(u_begin / num_kb * num_kb);
+            const uint32_t cf0 = ((t0 + 1) * Gu - 1) / T;
+            if (L > 0 && static_cast<uint32_t>(u_begin) != t0 && cf0 / CL == clu) arrived = false;
+        }
+        if (arrived) cluster_arrive_release();
         int seg = 0;
         for (int u = u_begin; u < u_end; ++seg) {
             const int tile = u / num_kb;
@@ -1047,6 +1060,10 @@ roles:
                     if (jj < M) red_cluster_add(dst + jj * TILE_N * 4, r[jj]);
                 named_bar_sync(1, 128);
                 if (et == 0) mbar_arrive_remote_release(mapa_shared(&bars->pbar, cf % CL));
+                if (!arrived) {
+                    cluster_arrive_release();
+                    arrived = true;
+                }
                 continue;
             }
             if (!full && cf != blockIdx.x) {
@@ -1079,20 +1096,24 @@ roles:
                 }
             }
         }
+        if (!arrived) cluster_arrive_release();
         if (et == 0) DSTAMP(p.dbg, 8);
     }
+    if (warp < 4) cluster_arrive_release();
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
     }
-    // No closing cluster barrier: after barrier 2 the only distributed-shared-
-    // memory traffic is contributors adding into a finisher's racc and arriving
-    // on its pbar, and the finisher leaves only after that wait. The other CTAs
-    // of the cluster leave as soon as they are done, so the next layer's
-    // clusters (programmatic dependent launch) find free SMs earlier.
-    if (p.end_sync) cluster_sync_all();
+    // Closing cluster barrier, split. After barrier 2 the only distributed-shared-
+    // memory traffic is contributors adding into a finisher's racc and arriving on
+    // its pbar, all in the contributors' first segment; every thread arrives once
+    // its part of that is done (warps 0-3 after their roles, the epilogue after its
+    // first segment), so no CTA leaves while a peer may still write its shared
+    // memory, and a CTA waits only for its peers' first segments, not for the
+    // cluster's slowest finisher (a full barrier here cost ~4 us per layer).
+    cluster_wait();
     DSTAMP(p.dbg, 9);
 }
 
@@ -1250,8 +1271,6 @@ cudaError_t launch_decode(const DecodeArgs& a, int epi, cudaStream_t st) {
     prm.slots = g.slots;
     prm.xs_cached = g.xs_cached;
     prm.xs_ld = g.xs_ld;
-    static const int env_es = env_int_once("I8MM_DECODE_END_SYNC", 0);
-    prm.end_sync = env_es;
     prm.dbg = g_dbg;
     static const int env_dbg = env_int_once("I8MM_DECODE_DBG_MODE", 0);
     prm.dbg_mode = env_dbg;
