@@ -1186,9 +1186,15 @@ DecodeGeom decode_geom(int64_t M, int64_t K, int64_t N) {
     if (s2 > MAX_STAGES) s2 = MAX_STAGES;
     const size_t xs_bytes = static_cast<size_t>(M * g.xs_ld) * 2;
     const int xs_stages = static_cast<int>((xs_bytes + A_BYTES - 1) / A_BYTES);
-    // keep the X slice in the ring's last stages while T1/T2 run when at least
-    // two weight stages stay free for the prefetch; else T2 re-reads X
-    g.xs_cached = s2 - xs_stages >= 2 ? 1 : 0;
+    // the X slice lives in the ring's last stages while T1/T2 run
+    // keep the X slice in the ring whenever it fits, even if no stage is left for
+    // the weight prefetch: re-reading X from global in T1/T2 costs more (fc2 M = 16:
+    // 67.6 -> 57.4 us, profiles/r2/decode/notes_r2.md); I8MM_DECODE_XS_MIN_FREE for A/B
+    static const int min_free = [] {
+        const char* e = getenv("I8MM_DECODE_XS_MIN_FREE");
+        return (e && e[0]) ? atoi(e) : 0;
+    }();
+    g.xs_cached = s2 - xs_stages >= min_free ? 1 : 0;
     g.s2 = s2;
     g.s1 = g.xs_cached ? s2 - xs_stages : s2;
     g.smem = fixed + static_cast<size_t>(s2) * A_BYTES;
