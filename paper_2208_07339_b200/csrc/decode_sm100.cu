@@ -346,34 +346,35 @@ __device__ __forceinline__ float epi_value(const DecodeArgs& a, const int32_t* o
     }
 }
 
-// one block: sorted outlier columns from the full mask in shared memory: the
-// first WO_CAP to o_s, all of them to o_idx when non-null, the count to n_out
+// sorted outlier columns from the full mask in shared memory, by the nthr
+// threads t = 0..nthr-1 (whole warps, synchronised on named barrier bar_id):
+// the first WO_CAP to o_s, all of them to o_idx when non-null, the count to n_out
 __device__ void compact_mask(const uint32_t* __restrict__ smask, int64_t nwords, Bars* bars,
-                             int32_t* __restrict__ o_idx) {
-    const int64_t per = (nwords + THREADS - 1) / THREADS;
-    const int64_t w0 = threadIdx.x * per;
+                             int32_t* __restrict__ o_idx, int t, int nthr, uint32_t bar_id) {
+    const int64_t per = (nwords + nthr - 1) / nthr;
+    const int64_t w0 = t * per;
     const int64_t w1 = w0 + per < nwords ? w0 + per : nwords;
     int32_t local = 0;
     for (int64_t w = w0; w < w1; ++w) local += __popc(smask[w]);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = t & 31, wid = t >> 5, nw = nthr >> 5;
     int32_t incl = local;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        const int32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += t;
+        const int32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
     }
     if (lane == 31) bars->warp_sums[wid] = incl;
-    __syncthreads();
+    named_bar_sync(bar_id, nthr);
     if (wid == 0) {
-        int32_t s = lane < NWARPS ? bars->warp_sums[lane] : 0;
+        int32_t v = lane < nw ? bars->warp_sums[lane] : 0;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int32_t t = __shfl_up_sync(0xffffffffu, s, d);
-            if (lane >= d) s += t;
+            const int32_t u = __shfl_up_sync(0xffffffffu, v, d);
+            if (lane >= d) v += u;
         }
-        if (lane < NWARPS) bars->warp_sums[lane] = s;
+        if (lane < nw) bars->warp_sums[lane] = v;
     }
-    __syncthreads();
+    named_bar_sync(bar_id, nthr);
     int32_t pos = incl - local + (wid > 0 ? bars->warp_sums[wid - 1] : 0);
     for (int64_t w = w0; w < w1; ++w) {
         uint32_t m = smask[w];
@@ -386,7 +387,8 @@ __device__ void compact_mask(const uint32_t* __restrict__ smask, int64_t nwords,
             ++pos;
         }
     }
-    if (threadIdx.x == THREADS - 1) bars->n_out = pos;
+    if (t == nthr - 1) bars->n_out = pos;
+    named_bar_sync(bar_id, nthr);
 }
 
 // 16 token columns of this thread's weight row: sum of the n_used accumulators
@@ -437,6 +439,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t crank = cluster_ctarank();
     const uint32_t clu = blockIdx.x / CL;
+    const bool lead = clu == 0;  // cluster 0 also publishes the call's token-side results
     // unit indices fit 32 bits (decode_fits bounds T * G < 2^31): 32-bit division on
     // the producer / MMA / finisher paths (a 64-bit one is a ~100-instruction call)
     const uint32_t T = static_cast<uint32_t>(p.total_units);
@@ -582,14 +585,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     DSTAMP(p.dbg, 1);
 
     // ================= T1: X slice, outlier bits, row partials -> every rank
-    if (kDevStamps && (p.dbg_mode & 8)) {  // A/B: no token phase (garbage panel): the stream alone
-        cluster_wait();
-        cluster_sync_all();
-        cluster_sync_all();
-        if (tid == 0) bars->n_out = 0;
-        __syncthreads();
-        goto roles;
-    }
     {
     const uint32_t thr = a.thr_bits_dev != nullptr ? __ldcg(a.thr_bits_dev) : a.thr_bits;
     if (bulk) mbar_wait(&bars->xbar, 0);
@@ -643,7 +638,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     DSTAMP(p.dbg, 3);
 
     // ================= T2: row scales, outlier list, codes -> every rank's panel
-    const bool lead = clu == 0;  // cluster 0 also publishes the call's token-side results
     for (int m = tid; m < static_cast<int>(M); m += THREADS) {
         uint32_t mx = 0;
 #pragma unroll
@@ -659,48 +653,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             a.ramax_bits[m] = mx;
         }
     }
-    compact_mask(smask, nwords, bars, lead && crank == 0 ? a.o_idx : nullptr);  // syncs
-    __syncthreads();  // o_s, n_out, row scales
+    __syncthreads();  // row scales (O is compacted by the epilogue warps after barrier 2)
     if (tid == 0) DSTAMP(p.dbg, 14);
-    if (warp >= 4) {
-        // the epilogue's global data, pulled into L2 while the codes are made:
-        // W[O, tile] (256 B per outlier row and segment) and, for each patched
-        // column, the cached q2 codes over the segment's k-range
-        const int et = tid - 128;
-        const int n_o0 = min(bars->n_out, WO_PRE_L2);
-        int u = u_begin;
-#pragma unroll
-        for (int sg = 0; sg < NSEG_PRE; ++sg) {
-            const int tile = u / num_kb;
-            const int seg_end = min(u_end, (tile + 1) * num_kb);
-            if (u < u_end) {
-                if (et < n_o0) {
-                    const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
-                    const int64_t cols = min(static_cast<int64_t>(TILE_N), N - n0);
-                    const uint32_t bytes = static_cast<uint32_t>(cols * 2) & ~15u;
-                    if (bytes && a.w_vec)
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                         a.w + static_cast<int64_t>(bars->o_s[et]) * a.ldw + n0),
-                                     "r"(bytes)
-                                     : "memory");
-                }
-                const int64_t n = static_cast<int64_t>(tile) * TILE_N + et;
-                if (n < N && pre_cr[sg][0] >= 0 && bit_of(smask, pre_cr[sg][0])) {
-                    int src;
-                    const float an = fixup_amax(pre_cr[sg], pre_cv[sg], smask, src);
-                    if (src == 1 && an != pre_aw[sg]) {
-                        const int k_lo = (u % num_kb) * BK, k_hi = min((seg_end - 1) % num_kb + 1, num_kb) * BK;
-                        if (k_hi > k_lo)
-                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.q2 + n * a.ldq + k_lo),
-                                         "r"(static_cast<uint32_t>(k_hi - k_lo))
-                                         : "memory");
-                    }
-                }
-            }
-            u = seg_end;
-        }
-    }
-    if (tid == 128) DSTAMP(p.dbg, 17);  // warps 4-7 done with the L2 prefetches
     const int nkb = kb_hi - kb_lo;
     // codes of this rank's k-blocks: item = (k-block, row, 16-column chunk); row
     // and chunk from a multiply-shift (exact for the ranges here: rest < 2^13)
@@ -772,16 +726,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) DSTAMP(p.dbg, 18);
     cluster_sync_all();  // 2: every panel complete; the X slice area becomes weight stages
     fence_proxy_async_smem();
-    if (lead && crank == 0 && tid == 0) {
-        *a.o_count = bars->n_out;
-        uint32_t any = 0;
-        for (int q = 0; q < CL; ++q) any |= bars->nonfinite[q];
-        if (a.nonfinite != nullptr) *a.nonfinite = any ? 1 : 0;
     }
-    }
-roles:
-    const int n_out = bars->n_out;
-    const int n_o = n_out <= WO_CAP ? n_out : 0;  // x[:, O] factors staged in smem
     DSTAMP(p.dbg, 4);
 
     // Producer and MMA loops keep their (tile, k-block, stage, phase) state
@@ -859,6 +804,53 @@ roles:
     } else if (warp >= 4) {
         // ---------------- epilogue: thread = weight row n of the tile
         const int et = tid - 128;
+        // the sorted outlier list (only the epilogue reads it): off the token
+        // phase's critical path, while the producer and the MMA warp start
+        compact_mask(smask, nwords, bars, lead && crank == 0 ? a.o_idx : nullptr, et, 128, 1);
+        if (lead && crank == 0 && et == 0) {
+            *a.o_count = bars->n_out;
+            uint32_t any = 0;  // every rank's NaN/Inf flag landed before barrier 1
+            for (int q = 0; q < CL; ++q) any |= bars->nonfinite[q];
+            if (a.nonfinite != nullptr) *a.nonfinite = any ? 1 : 0;
+        }
+        const int n_out = bars->n_out;
+        const int n_o = n_out <= WO_CAP ? n_out : 0;  // x[:, O] factors staged in smem
+    // the epilogue's global data, pulled into L2 while the first MMAs run:
+    // W[O, tile] (256 B per outlier row and segment) and, for each patched
+    // column, the cached q2 codes over the segment's k-range
+    const int n_o0 = min(bars->n_out, WO_PRE_L2);
+    int u = u_begin;
+#pragma unroll
+    for (int sg = 0; sg < NSEG_PRE; ++sg) {
+        const int tile = u / num_kb;
+        const int seg_end = min(u_end, (tile + 1) * num_kb);
+        if (u < u_end) {
+            if (et < n_o0) {
+                const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
+                const int64_t cols = min(static_cast<int64_t>(TILE_N), N - n0);
+                const uint32_t bytes = static_cast<uint32_t>(cols * 2) & ~15u;
+                if (bytes && a.w_vec)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     a.w + static_cast<int64_t>(bars->o_s[et]) * a.ldw + n0),
+                                 "r"(bytes)
+                                 : "memory");
+            }
+            const int64_t n = static_cast<int64_t>(tile) * TILE_N + et;
+            if (n < N && pre_cr[sg][0] >= 0 && bit_of(smask, pre_cr[sg][0])) {
+                int src;
+                const float an = fixup_amax(pre_cr[sg], pre_cv[sg], smask, src);
+                if (src == 1 && an != pre_aw[sg]) {
+                    const int k_lo = (u % num_kb) * BK, k_hi = min((seg_end - 1) % num_kb + 1, num_kb) * BK;
+                    if (k_hi > k_lo)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.q2 + n * a.ldq + k_lo),
+                                     "r"(static_cast<uint32_t>(k_hi - k_lo))
+                                     : "memory");
+                }
+            }
+        }
+        u = seg_end;
+    }
+
         const int n_local = et;
         const int quad = warp & 3;
         for (int i = et; i < static_cast<int>(M) * n_o; i += 128) {
