@@ -1020,8 +1020,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (spin > (1u << 22)) __trap();
                     a.tile_cnt[tile] = 0;
                 }
+                // thread 0's acquire + the barrier order every thread's loads after the
+                // contributors' release (no per-thread fence)
                 named_bar_sync(1, 128);
-                __threadfence();
                 for (uint32_t c = cl - fin_cross + 1; c <= cl; ++c) {
                     const int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
 #pragma unroll
@@ -1063,7 +1064,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj)
                     if (jj < M) __stcg(slotp + jj * TILE_N, static_cast<int32_t>(r[jj]));
-                __threadfence();
+                // the barrier orders every thread's stores before thread 0's release
+                // (cumulativity), as a per-thread fence would, at one GPU-scope op
                 named_bar_sync(1, 128);
                 if (et == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.tile_cnt + tile) : "memory");
                 continue;
