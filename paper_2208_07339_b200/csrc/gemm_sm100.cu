@@ -735,14 +735,22 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             if constexpr (CG == 1) {
                 if (split) {  // the tile's last K-range to arrive runs the epilogue on the sums
-                    __threadfence();
+                    // every thread's reductions are ordered before thread 0's acq_rel
+                    // count by the barrier (cumulativity), and the last arriver's loads
+                    // after it by the second barrier: no per-thread GPU-scope fence
                     named_bar_sync(2, EPI_THREADS);
                     if (et == 0 && it == 0) gstamp(p.dbg, 9);
-                    if (et == 0) split_last = atomicAdd(p.c32_cnt + t, 1) == p.ksplit - 1;
+                    if (et == 0) {
+                        int old;
+                        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                                     : "=r"(old)
+                                     : "l"(p.c32_cnt + t)
+                                     : "memory");
+                        split_last = old == p.ksplit - 1;
+                    }
                     named_bar_sync(2, EPI_THREADS);
                     if (et == 0 && it == 0) gstamp(p.dbg, 10);
                     if (split_last) {
-                        __threadfence();
 #pragma unroll 1
                         for (int cc = 0; cc < COLS_PER_WARP / 32; ++cc) {
                             const int ch = half * (COLS_PER_WARP / 32) + cc;
