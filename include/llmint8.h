@@ -192,6 +192,10 @@ int i8mm_linear_workspace_init(void* workspace, size_t workspace_bytes, int64_t 
 int i8mm_linear_patch_stats(const void* w, int64_t ldw, const void* wbuf, int64_t M, int64_t K, int64_t N,
                             void* workspace, size_t workspace_bytes, void* stream);
 void i8mm_debug_set_decode_max_m(int max_m);
+/* Test / A-B hook: route weight-stationary prefill calls with 17 <= M <= 128 through
+ * the swap-AB stream-K GEMM (1, default; env I8MM_SWAPAB=0 disables) or the row-tile
+ * GEMM (0). Workspaces sized under one setting must be used under the same one. */
+void i8mm_debug_set_swapab(int on);
 /* Programmatic dependent launch on the prefill path: 1 on (default), 0 off
    (same as I8MM_PDL=0); for A/B measurements. */
 void i8mm_debug_set_pdl(int on);

@@ -23,7 +23,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB_NAME = "libllmint8_sm100.so"
 SOURCES = ["capi.cu", "prologue.cu", "weights.cu", "gemm_sm100.cu", "decode_sm100.cu", "siblings.cu",
-           "peak_sm100.cu", "f32path.cu"]
+           "peak_sm100.cu", "f32path.cu", "swapab_sm100.cu"]
 HEADERS = ["kernels.cuh", "sm100_ptx.cuh", "quant_common.cuh", "percall_dev.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

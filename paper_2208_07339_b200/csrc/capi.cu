@@ -258,6 +258,9 @@ struct Workspace {
     void* rp_scratch;    // prefill: per-row group maxima + f64 row scales (launch_row_prologue)
     int32_t* sk_c32;     // prefill M <= 128 (linear): split-K partial sums, then tile counters
     int64_t sk_ld, sk_words;
+    int32_t* sab_c32;    // prefill M = 17..128 (linear): swap-AB partial slots, then tile counters
+    int32_t* sab_cnt;
+    int64_t sab_cnt_words;
     int64_t ldq, o_cap;
     size_t bytes;
 };
@@ -329,7 +332,11 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
         }
     }
     if (!w.decode) w.rp_scratch = reinterpret_cast<void*>(take(row_prologue_scratch_bytes(M > 0 ? M : 1, K)));
-    if (linear && !w.decode && gemm_split_factor(M, N, K) > 1) {
+    if (linear && !w.decode && swapab_route(M, K, N)) {
+        w.sab_c32 = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(swapab_c32_words(M))));
+        w.sab_cnt_words = swapab_cnt_words(N);
+        w.sab_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(w.sab_cnt_words)));
+    } else if (linear && !w.decode && gemm_split_factor(M, N, K) > 1) {
         w.sk_ld = gemm_split_cols(N, true);  // column-major partials: sk_ld columns x M rows
         w.sk_words = M * w.sk_ld + gemm_split_tiles(N, true);
         w.sk_c32 = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(w.sk_words)));
@@ -418,6 +425,8 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
 
 // ---------------------------------------------------------------- linear layer
 void i8mm_debug_set_pdl(int on) { g_pdl = on ? 1 : 0; }
+
+void i8mm_debug_set_swapab(int on) { set_swapab(on); }
 
 void i8mm_debug_set_decode_max_m(int max_m) {
     g_decode_max_m = max_m < 0 ? 0 : (max_m > kDecodeMaxM ? kDecodeMaxM : max_m);
@@ -528,7 +537,10 @@ int i8mm_linear_prologue(const void* x, int64_t ldx, int64_t M, const void* w, i
     if (ws.decode) return cuda_status(launch_set_word(ws.thr_word, alpha_threshold_bits(alpha), st));
     // row side (+ the fixup counters zeroed in the same first launch), then
     // W[O, :] gather + column fixup in one launch, then the patched codes
-    const PerCallFix fix{ws.sk_c32, ws.sk_c32 != nullptr ? ws.sk_words : 0, wh, K, N, ldw, ws.wo, round_up(N, 8),
+    // zeroed with the mask: the split-K scratch, or the swap-AB GEMM's tile counters
+    const PerCallFix fix{ws.sab_cnt != nullptr ? ws.sab_cnt : ws.sk_c32,
+                         ws.sab_cnt != nullptr ? ws.sab_cnt_words : (ws.sk_c32 != nullptr ? ws.sk_words : 0), wh, K,
+                         N, ldw, ws.wo, round_up(N, 8),
                          b.col_amax, b.cand_v, b.cand_r, b.q2, ws.p_count, ws.p_idx, ws.p_amax, ws.p_src,
                          ws.wq_p};
     if (launch_row_prologue(xh, M, K, ldx, alpha, ws.mask, ws.o_idx, ws.o_count, ws.xq, ws.ldq,
@@ -609,6 +621,9 @@ static int linear_gemm_rows_impl(const void* x, int64_t ldx, int64_t M, const vo
         g.peer_ldy = peers->ldy;
         g.peer_col = peers->col;
     }
+    // mid-size M, whole call: the swap-AB stream-K GEMM (swapab_sm100.cu)
+    if (ws.sab_cnt != nullptr && row0 == 0 && rows == M && g.n_peer == 0 && (epi == EPI_F16 || epi == EPI_F32))
+        return cuda_status(launch_swapab(g, ws.sab_c32, ws.sab_cnt, epi, static_cast<cudaStream_t>(stream)));
     if (ws.sk_c32 != nullptr && row0 == 0 && rows == M) {  // split-K scratch (zeroed by the prologue)
         g.c32 = ws.sk_c32;
         g.c32_rows = M;

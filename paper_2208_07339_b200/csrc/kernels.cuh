@@ -184,6 +184,12 @@ constexpr int kMaxPeers = 8;
 int64_t gemm_split_cols(int64_t N, bool patches);
 int gemm_split_factor(int64_t M, int64_t N, int64_t K);  // 1 = no split
 int64_t gemm_split_tiles(int64_t N, bool patches);
+// swap-AB stream-K GEMM for M = 17..128 (swapab_sm100.cu)
+bool swapab_route(int64_t M, int64_t K, int64_t N);
+void set_swapab(int on);
+int64_t swapab_c32_words(int64_t M);
+int64_t swapab_cnt_words(int64_t N);
+cudaError_t launch_swapab(const GemmArgs& a, int32_t* c32, int32_t* tile_cnt, int epi, cudaStream_t st);
 
 cudaError_t launch_gemm_sm100(const GemmArgs& args, int epi, cudaStream_t st);
 

@@ -52,12 +52,30 @@ def st_module():  # weight-stationary prefill: fused prologue, fixup, patches, C
     lin(x16)
 
 
-def st_splitk():  # M <= 128, K >= 8192: split-K partial sums + counters
+def st_splitk():  # M <= 128, K >= 8192: split-K partial sums + counters (row-tile GEMM)
+    from paper_2208_07339_b200 import _native as nat
     x, w = case(3, 64, 8192, 512, heavy=3)
     ref = orc.c_llm_int8_matmul(x, w, 6.0)
     lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
     x16 = torch.from_numpy(x.astype(np.float16)).cuda()
-    check("split-K exact", lin.matmul(x16, exact=True).cpu().numpy(), ref.output)
+    nat.lib().i8mm_debug_set_swapab(0)
+    try:
+        check("split-K exact", lin.matmul(x16, exact=True).cpu().numpy(), ref.output)
+        lin(x16)
+    finally:
+        nat.lib().i8mm_debug_set_swapab(1)
+
+
+def st_swapab():  # 17 <= M <= 64: swap-AB stream-K GEMM, split tiles, patch tiles
+    for seed, m, k, n, heavy in ((8, 40, 2048, 1000, 3), (9, 64, 8192, 512, 2), (10, 17, 1024, 2050, 6)):
+        x, w = case(seed, m, k, n, heavy=heavy)
+        ref = orc.c_llm_int8_matmul(x, w, 6.0)
+        lin = p.Int8Linear(torch.from_numpy(w.astype(np.float16)).cuda())
+        x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+        y = lin(x16).float().cpu().numpy()
+        err = float(np.abs(y - ref.output).max())
+        assert err <= 2.0 ** -10 * float(np.abs(ref.output).max()) + 1e-3, err
+        print(f"[ok] swap-AB M={m} K={k} N={n} max err {err:.3g}", flush=True)
 
 
 def st_decode():  # decode kernel: 8-CTA clusters, DSMEM token side + partials, stream-K, patched dots

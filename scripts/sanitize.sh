@@ -4,7 +4,7 @@
 O=gpurun_out/sanitize; mkdir -p $O
 : > $O/summary.txt
 for tool in memcheck racecheck synccheck initcheck; do
-  for st in functional module splitk decode peers siblings f32 peak; do
+  for st in functional module splitk swapab decode peers siblings f32 peak; do
     timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize.py $st > $O/${tool}_${st}.log 2>&1
     rc=$?
     s=$(grep -E "ERROR SUMMARY|RACECHECK SUMMARY" $O/${tool}_${st}.log | tail -1)

@@ -918,3 +918,43 @@ def test_graphed_decode_step_has_only_kernel_nodes(p):
     torch.cuda.synchronize()
     for mod, x, y in zip(mods, static, outs):
         assert torch.equal(y, mod(x))
+
+
+@pytest.mark.parametrize("case", [
+    # seed, m, k, n, planted outlier cols, heavy outlier rows of W
+    (70, 17, 1024, 1000, 6, 2), (71, 32, 5120, 640, 6, 0), (72, 48, 2048, 384, 6, 6),
+    (73, 64, 1008, 257, 4, 1), (74, 100, 4096, 2050, 8, 3), (75, 128, 768, 4000, 20, 5),
+    (76, 33, 8192, 136, 2, 2), (77, 80, 2048, 1536, 6, 0)])
+def test_swapab_mid_m_vs_row_tile_gemm_and_oracle(p, oracle_mod, case):
+    """Weight-stationary prefill at 17 <= M <= 128 runs the swap-AB stream-K GEMM
+    (swapab_sm100.cu): fp16 and fast f32 outputs bitwise equal to the row-tile
+    GEMM on the same prologue, fp16 within tolerance of the oracle; ragged N and
+    K, > 16 outliers (the slow outlier loop), patched columns (extra tiles),
+    tiles split over many CTAs."""
+    from paper_2208_07339_b200 import _native as nat
+
+    seed, m, k, n, n_out, heavy = case
+    x, w = _ws_case(seed, m, k, n, n_out, heavy)
+    ref = oracle_mod.c_llm_int8_matmul(x, w, 6.0)
+    w16 = torch.from_numpy(w.astype(np.float16)).cuda()
+    lin = p.Int8Linear(w16, alpha=6.0)
+    lin32 = p.Int8Linear(w16, alpha=6.0, out_dtype=torch.float32)
+    x16 = torch.from_numpy(x.astype(np.float16)).cuda()
+    L = nat.lib()
+    try:
+        L.i8mm_debug_set_swapab(1)
+        y_sab = lin(x16)
+        y32_sab = lin32(x16)
+        st = lin.last_stats()
+        L.i8mm_debug_set_swapab(0)
+        y_row = lin(x16)
+        y32_row = lin32(x16)
+    finally:
+        L.i8mm_debug_set_swapab(1)
+    assert torch.equal(y_sab, y_row), "swap-AB and row-tile GEMMs must agree bitwise (fp16)"
+    assert torch.equal(y32_sab, y32_row), "swap-AB and row-tile GEMMs must agree bitwise (f32)"
+    err_ok = np.abs(_np(y_sab).astype(np.float64) - ref.output) <= _golden.fp16_tolerance(ref.output)
+    assert err_ok.all(), f"{(~err_ok).sum()} fp16 outputs outside the stated tolerance"
+    assert st["decomposed_cols"] == len(ref.dims)
+    if heavy:
+        assert st["patched_cols"] > 0
