@@ -196,6 +196,9 @@ void i8mm_debug_set_decode_max_m(int max_m);
  * the swap-AB stream-K GEMM (1, default; env I8MM_SWAPAB=0 disables) or the row-tile
  * GEMM (0). Workspaces sized under one setting must be used under the same one. */
 void i8mm_debug_set_swapab(int on);
+/* Dev tool: per-CTA %globaltimer stamps of the swap-AB GEMM (16 u64 per CTA, dev
+ * build only; NULL disables). */
+void i8mm_debug_swapab_timeline(void* stamps);
 /* Programmatic dependent launch on the prefill path: 1 on (default), 0 off
    (same as I8MM_PDL=0); for A/B measurements. */
 void i8mm_debug_set_pdl(int on);

@@ -71,6 +71,7 @@ EXPORTED_SYMBOLS = (
     "i8mm_linear_patch_stats",
     "i8mm_debug_set_decode_max_m",
     "i8mm_debug_set_swapab",
+    "i8mm_debug_swapab_timeline",
     "i8mm_debug_set_pdl",
     "i8mm_linear_uses_decode",
     "i8mm_debug_decode_timeline",
@@ -122,6 +123,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_debug_set_gemm_variant": ([I32, I32], None),
         "i8mm_debug_set_decode_max_m": ([I32], None),
         "i8mm_debug_set_swapab": ([I32], None),
+        "i8mm_debug_swapab_timeline": ([P], None),
         "i8mm_debug_set_pdl": ([I32], None),
         "i8mm_linear_uses_decode": ([I64, I64, I64], I32),
         "i8mm_debug_decode_timeline": ([P], None),

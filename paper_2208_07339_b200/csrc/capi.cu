@@ -428,6 +428,10 @@ void i8mm_debug_set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
 void i8mm_debug_set_swapab(int on) { set_swapab(on); }
 
+void i8mm_debug_swapab_timeline(void* stamps) {
+    set_swapab_timeline(static_cast<unsigned long long*>(stamps));
+}
+
 void i8mm_debug_set_decode_max_m(int max_m) {
     g_decode_max_m = max_m < 0 ? 0 : (max_m > kDecodeMaxM ? kDecodeMaxM : max_m);
 }

@@ -187,6 +187,7 @@ int64_t gemm_split_tiles(int64_t N, bool patches);
 // swap-AB stream-K GEMM for M = 17..128 (swapab_sm100.cu)
 bool swapab_route(int64_t M, int64_t K, int64_t N);
 void set_swapab(int on);
+void set_swapab_timeline(unsigned long long* stamps);
 int64_t swapab_c32_words(int64_t M);
 int64_t swapab_cnt_words(int64_t N);
 cudaError_t launch_swapab(const GemmArgs& a, int32_t* c32, int32_t* tile_cnt, int epi, cudaStream_t st);

@@ -71,7 +71,23 @@ struct Params {
     int num_kb, n_tiles, stages;
     int32_t* c32;       // [grid][MP][TILE_N] partial sums of split tiles
     int32_t* tile_cnt;  // [n_tiles + patch tiles] arrival counters (zeroed)
+    unsigned long long* dbg;  // dev build: 16 %globaltimer stamps per CTA, nullable
 };
+
+#ifdef I8MM_GEMM_DEVTOOLS
+constexpr bool kStamps = true;
+#else
+constexpr bool kStamps = false;
+#endif
+__device__ __forceinline__ void stamp(const Params& p, int i) {
+    if constexpr (kStamps) {
+        if (p.dbg != nullptr) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.dbg[blockIdx.x * 16 + i] = t;
+        }
+    }
+}
 
 struct __align__(8) Bars {
     uint64_t full[MAX_STAGES];
@@ -135,9 +151,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = bars->tmem_slot;
+    if (tid == 0) stamp(p, 0);
     // everything below reads the prologue's outputs
     pdl_wait();
     pdl_trigger();
+    if (tid == 0) stamp(p, 1);
     const int n_patch = min(static_cast<int>(*p.patch_count), static_cast<int>(p.N));
     const int n_pt = (n_patch + TILE_N - 1) / TILE_N;
     const uint32_t T = static_cast<uint32_t>((p.n_tiles + n_pt) * num_kb);
@@ -207,6 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             if (lane == 0) mma_commit(&bars->tmem_full[acc]);
             __syncwarp();
+            if (lane == 0 && seg < 3) stamp(p, 2 + seg);  // MMAs of segment issued
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: thread = weight row n of the tile
@@ -258,6 +277,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t cf = ((t0 + 1) * G - 1) / T;
             const uint32_t cl = (t1 * G - 1) / T;
             const bool finisher = !full && cf == blockIdx.x;
+            if (et == 0 && seg < 3) stamp(p, 5 + seg);  // epilogue reaches the segment
             if (finisher) {
                 if (et == 0) {
                     for (uint32_t spin = 0; ld_acquire(p.tile_cnt + tile) < static_cast<int>(cl - cf); ++spin)
@@ -266,8 +286,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 named_bar_sync(1, 128);
             }
+            if (et == 0 && seg < 3) stamp(p, 8 + seg);  // finisher's partials ready (or no wait)
             mbar_wait(&bars->tmem_full[acc], (seg >> 1) & 1);
             tc_fence_after();
+            if (et == 0 && seg < 3) stamp(p, 11 + seg);  // accumulator ready
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                                    static_cast<uint32_t>(acc * NACC * MP);
             const int n_used = min(NACC, (seg_end - su0) * KS);
@@ -333,8 +355,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     }
+    if (tid == 128) stamp(p, 15);  // epilogue done (before the closing barrier; timer reads
+                                   // right after a BAR.SYNC can complete before it resolves)
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) stamp(p, 14);
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<512>(tmem_base);
@@ -351,6 +376,7 @@ int sab_stages(int mp) {
     return s > sab::MAX_STAGES ? sab::MAX_STAGES : s;
 }
 int g_swapab = -1;  // -1: env I8MM_SWAPAB (default on)
+unsigned long long* g_sab_dbg = nullptr;
 }  // namespace
 
 int swapab_mp(int64_t M) { return M <= 32 ? 32 : (M <= 64 ? 64 : 128); }
@@ -375,6 +401,8 @@ bool swapab_route(int64_t M, int64_t K, int64_t N) {
 }
 
 void set_swapab(int on) { g_swapab = on; }
+
+void set_swapab_timeline(unsigned long long* stamps) { g_sab_dbg = stamps; }
 
 int64_t swapab_c32_words(int64_t M) { return static_cast<int64_t>(num_sms()) * swapab_mp(M) * sab::TILE_N; }
 
@@ -436,6 +464,7 @@ cudaError_t launch_swapab(const GemmArgs& a, int32_t* c32, int32_t* tile_cnt, in
     prm.stages = sab_stages(mp);
     prm.c32 = c32;
     prm.tile_cnt = tile_cnt;
+    prm.dbg = g_sab_dbg;
     CUtensorMap tw, tp, tx;
     if (!make_tmap_i8_rows(&tw, a.b, a.N, a.K, a.ldb, sab::TILE_N)) return cudaErrorInvalidValue;
     if (!make_tmap_i8_rows(&tp, a.b_patch, a.N, a.K, a.ldb, sab::TILE_N)) return cudaErrorInvalidValue;
