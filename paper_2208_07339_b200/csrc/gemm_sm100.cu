@@ -994,9 +994,73 @@ int gemm_split_factor(int64_t M, int64_t N, int64_t K) {
     return sk >= 2 ? static_cast<int>(sk) : 1;
 }
 
+// m-tiles per raster group (see launch_gemm_one)
+static int raster_group_m(int64_t N, int64_t K, int cg, int mc, int tbn) {
+    using namespace gemm;
+    const int gm_env = env_int("I8MM_GROUP_M");
+    if (gm_env > 0) return gm_env;
+    const int64_t n_tiles = (N + tbn - 1) / tbn;
+    const int64_t wave = num_sms() / (cg * mc);
+    if (n_tiles * 2 <= wave) return 1;
+    const int64_t panel = static_cast<int64_t>(BM) * cg * mc * (K > 0 ? K : 1);
+    const int64_t g = (32LL << 20) / panel;
+    int gm = 1;
+    while (gm * 2 <= g && gm < 32) gm *= 2;
+    return gm;
+}
+
+static cudaError_t launch_gemm_one(const GemmArgs& a, int epi, cudaStream_t st);
+
+// Row chunks (measured, profiles/r2/gemm_chunk_ab.txt): a persistent launch over
+// many raster groups lets its clusters drift apart by several tiles, so the
+// tiles in flight span more than one group and the L2 stops holding the group's
+// panels: cfg5 fc1 read 18.5 GB of DRAM for 0.8 GB of operands. One launch per
+// chunk of whole groups (>= 8 waves of tiles, so the last wave's idle SMs stay a
+// small share) resets the drift: 6.75 GB, and the power-capped SM clock rises
+// 1.29 -> 1.48 GHz (+8-12 % on the bench line). I8MM_GEMM_CHUNK_WAVES=0 disables.
 cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     using namespace gemm;
     if (a.M <= 0 || a.N <= 0) return cudaSuccess;
+    static const int chunk_waves = [] {
+        const char* e = getenv("I8MM_GEMM_CHUNK_WAVES");
+        return (e && e[0]) ? atoi(e) : 8;
+    }();
+    if (chunk_waves > 0 && a.M > BM && a.c32 == nullptr) {
+        const int cg = gemm_cg_override() != 1 ? 2 : 1;
+        const int mc = (cg == 2 && a.M >= 2048 && gemm_mc_override() == 2) ? 2 : 1;
+        const int nw = (cg == 2 && mc == 1 && gemm_wide_mode(a.M, a.N, a.K)) ? 2 : 1;
+        const int tbn = BN * nw;
+        const int gm = raster_group_m(a.N, a.K, cg, mc, tbn);
+        const int64_t group_rows = static_cast<int64_t>(gm) * BM * cg * mc;
+        const int64_t n_tiles = (a.N + tbn - 1) / tbn;
+        const int64_t wave = num_sms() / (cg * mc);
+        const int64_t groups_per_chunk = (chunk_waves * wave + gm * n_tiles - 1) / (gm * n_tiles);
+        const int64_t chunk = group_rows * (groups_per_chunk > 0 ? groups_per_chunk : 1);
+        if (gm > 1 && a.M > chunk + group_rows / 2) {
+            const int elt = epi == EPI_F16 ? 2 : 4;
+            for (int64_t r0 = 0; r0 < a.M; r0 += chunk) {
+                // a short tail joins the previous chunk
+                const int64_t rows = (a.M - r0 < chunk + group_rows / 2) ? a.M - r0 : chunk;
+                GemmArgs c = a;
+                c.a = a.a + r0 * a.lda;
+                c.M = rows;
+                c.y = static_cast<char*>(a.y) + r0 * a.ldy * elt;
+                if (a.row_amax) c.row_amax = a.row_amax + r0;
+                if (a.x) c.x = a.x + r0 * a.ldx;
+                if (a.xo) c.xo = a.xo + r0 * a.o_cap;
+                for (int q = 0; q < a.n_peer; ++q)
+                    c.y_peer[q] = static_cast<char*>(a.y_peer[q]) + r0 * a.peer_ldy * 2;
+                if (cudaError_t e = launch_gemm_one(c, epi, st)) return e;
+                if (rows != chunk) break;
+            }
+            return cudaSuccess;
+        }
+    }
+    return launch_gemm_one(a, epi, st);
+}
+
+static cudaError_t launch_gemm_one(const GemmArgs& a, int epi, cudaStream_t st) {
+    using namespace gemm;
     if ((a.lda % 16) || (a.ldb % 16) || (reinterpret_cast<uintptr_t>(a.a) & 15) ||
         (reinterpret_cast<uintptr_t>(a.b) & 15))
         return cudaErrorInvalidValue;
@@ -1081,19 +1145,7 @@ cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
         // wave -> row-major (group 1); otherwise group GROUP_M m-tiles so their
         // A panels (GROUP_M x TILE_M x K bytes) stay within ~32 MB of L2 while
         // the B panels stream past them.
-        const int gm_env = env_int("I8MM_GROUP_M");
-        const int64_t n_tiles = (a.N + tbn - 1) / tbn;
-        const int64_t wave = num_sms() / (cg * mc);
-        int gm;
-        if (n_tiles * 2 <= wave) {
-            gm = 1;
-        } else {
-            const int64_t panel = static_cast<int64_t>(BM) * cg * mc * (a.K > 0 ? a.K : 1);
-            int64_t g = (32LL << 20) / panel;
-            gm = 1;
-            while (gm * 2 <= g && gm < 32) gm *= 2;
-        }
-        p.group_m = gm_env > 0 ? gm_env : gm;
+        p.group_m = raster_group_m(a.N, a.K, cg, mc, tbn);
         const int pol_env = env_int("I8MM_GEMM_L2POL");
         // bit 0: A panels evict_last, bit 1: B panels evict_first (measured: B panels
         // are reused by the group's m-tiles, evict_first on them costs ~10 %)
