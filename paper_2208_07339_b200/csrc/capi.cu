@@ -669,20 +669,6 @@ int i8mm_linear_forward_peers(const void* x, int64_t ldx, int64_t M, const void*
 int i8mm_linear_gemm(const void* x, int64_t ldx, int64_t M, const void* w, int64_t ldw,
                      const void* wbuf, int64_t K, int64_t N, void* y, int64_t ldy, int out_kind,
                      void* workspace, size_t workspace_bytes, void* stream) {
-    // A/B (I8MM_GEMM_CHUNK=rows): one launch per row chunk
-    static const int64_t chunk = [] {
-        const char* e = getenv("I8MM_GEMM_CHUNK");
-        return static_cast<int64_t>((e && e[0]) ? atoll(e) : 0);
-    }();
-    if (chunk > 0 && M > chunk && !uses_decode(M, K, N)) {
-        for (int64_t r0 = 0; r0 < M; r0 += chunk) {
-            const int64_t rows = M - r0 < chunk ? M - r0 : chunk;
-            if (int s = linear_gemm_rows_impl(x, ldx, M, w, ldw, wbuf, K, N, y, ldy, out_kind, workspace,
-                                              workspace_bytes, r0, rows, stream))
-                return s;
-        }
-        return I8MM_OK;
-    }
     return linear_gemm_rows_impl(x, ldx, M, w, ldw, wbuf, K, N, y, ldy, out_kind, workspace,
                                  workspace_bytes, 0, M, stream);
 }
