@@ -1021,10 +1021,8 @@ static cudaError_t launch_gemm_one(const GemmArgs& a, int epi, cudaStream_t st);
 cudaError_t launch_gemm_sm100(const GemmArgs& a, int epi, cudaStream_t st) {
     using namespace gemm;
     if (a.M <= 0 || a.N <= 0) return cudaSuccess;
-    static const int chunk_waves = [] {
-        const char* e = getenv("I8MM_GEMM_CHUNK_WAVES");
-        return (e && e[0]) ? atoi(e) : 8;
-    }();
+    const char* cw_env = getenv("I8MM_GEMM_CHUNK_WAVES");  // read per call (tests set it)
+    const int chunk_waves = (cw_env && cw_env[0]) ? atoi(cw_env) : 8;
     if (chunk_waves > 0 && a.M > BM && a.c32 == nullptr) {
         const int cg = gemm_cg_override() != 1 ? 2 : 1;
         const int mc = (cg == 2 && a.M >= 2048 && gemm_mc_override() == 2) ? 2 : 1;

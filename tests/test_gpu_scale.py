@@ -76,6 +76,8 @@ MULTIWAVE = [
     ("all_tiles_one_pair_group2", (43, 700, 520, 1500, 4, 2),
      {"I8MM_GEMM_MAX_CLUSTERS": "1", "I8MM_GROUP_M": "2"}),
     ("cg1_many_tiles", (44, 128, 2048, 6000, 6, 6), {"I8MM_GEMM_MAX_CLUSTERS": "2"}),
+    # one launch per chunk of raster groups, with a short tail folded into the last chunk
+    ("chunked_launches", (46, 2900, 1024, 3000, 6, 3), {"I8MM_GROUP_M": "2", "I8MM_GEMM_CHUNK_WAVES": "1"}),
 ]
 
 
