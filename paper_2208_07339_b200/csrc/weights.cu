@@ -42,14 +42,27 @@ __global__ void col_amax_vec_kernel(const __half* __restrict__ w, int64_t K, int
     if (v >= (N >> 3)) return;
     uint32_t m[4] = {0, 0, 0, 0};
     const __half* p = w + (v << 3);
-    for (int64_t k = k0; k < k1; ++k) {
-        if (row_is_out(row_mask, k)) continue;
-        const uint4 q = ld_stream_u4(p + k * ldw);
+    auto fold = [&](const uint4& q) {
         m[0] = __vmaxu2(m[0], q.x & 0x7FFF7FFFu);
         m[1] = __vmaxu2(m[1], q.y & 0x7FFF7FFFu);
         m[2] = __vmaxu2(m[2], q.z & 0x7FFF7FFFu);
         m[3] = __vmaxu2(m[3], q.w & 0x7FFF7FFFu);
+    };
+    // 8 rows per step: the loads are issued unconditionally (an outlier row's is
+    // discarded), so they are in flight together instead of each waiting on the
+    // row-mask lookup that decides whether to load it
+    constexpr int U = 8;
+    int64_t k = k0;
+    for (; k + U <= k1; k += U) {
+        uint4 q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) q[u] = ld_stream_u4(p + (k + u) * ldw);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (!row_is_out(row_mask, k + u)) fold(q[u]);
     }
+    for (; k < k1; ++k)
+        if (!row_is_out(row_mask, k)) fold(ld_stream_u4(p + k * ldw));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         if (m[i] & 0xFFFFu) atomicMax(amax_bits + (v << 3) + 2 * i, m[i] & 0xFFFFu);
@@ -337,7 +350,10 @@ cudaError_t launch_col_amax(const __half* w, int64_t K, int64_t N, int64_t ldw,
     const bool vec = (N % 8 == 0) && (ldw % 8 == 0) && aligned16(w);
     if (vec) {
         const int64_t cb = ((N >> 3) + 127) / 128;
-        const int rb = grid_rows_chunk(K, cb, static_cast<int64_t>(num_sms()) * 16, &rpb);
+        // ~2 blocks per SM, each thread over many rows: 16x fewer row chunks than the
+        // 16-per-SM split (each chunk costs one atomicMax per column; at 4096 x 4096
+        // they serialised in the L2: 62 us for 32 MB)
+        const int rb = grid_rows_chunk(K, cb, static_cast<int64_t>(num_sms()) * 2, &rpb);
         col_amax_vec_kernel<<<dim3(static_cast<unsigned>(cb), rb), 128, 0, st>>>(w, K, N, ldw, row_mask,
                                                                                    rpb, bits);
     } else {
