@@ -126,6 +126,12 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
                          int64_t K, int64_t N, float alpha, void* y, int64_t ldy, int out_kind,
                          void* workspace, size_t workspace_bytes, int32_t* o_count_dev,
                          void* stream);
+/* Same, plus the reference's NaN/Inf rejection of X and W (tensors.py:47-48):
+ * *nonfinite_dev (device int32, nullable) ends non-zero when either holds NaN/Inf. */
+int i8mm_llm_int8_matmul_checked(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M,
+                                 int64_t K, int64_t N, float alpha, void* y, int64_t ldy, int out_kind,
+                                 void* workspace, size_t workspace_bytes, int32_t* o_count_dev,
+                                 int32_t* nonfinite_dev, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Int8 linear module (weight-stationary). Replaces the reference's module

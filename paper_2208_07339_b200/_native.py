@@ -55,6 +55,7 @@ EXPORTED_SYMBOLS = (
     "i8mm_transpose_i8",
     "i8mm_llm_int8_workspace_size",
     "i8mm_llm_int8_matmul",
+    "i8mm_llm_int8_matmul_checked",
     "i8mm_gather_outlier_rows",
     "i8mm_linear_weight_bytes",
     "i8mm_linear_prepare_scratch_bytes",
@@ -158,6 +159,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "i8mm_llm_int8_workspace_size": ([I64, I64, I64], ctypes.c_size_t),
         "i8mm_llm_int8_matmul": ([P, I64, P, I64, I64, I64, I64, F32, P, I64, I32, P,
                                   ctypes.c_size_t, P, P], I32),
+        "i8mm_llm_int8_matmul_checked": ([P, I64, P, I64, I64, I64, I64, F32, P, I64, I32, P,
+                                          ctypes.c_size_t, P, P, P], I32),
         "i8mm_tensor_stats": ([P, I64, I64, I64, P, P, P], I32),
         "i8mm_absmax_quantize": ([P, I64, I64, I64, P, P, I64, I32, P], I32),
         "i8mm_zeropoint_params": ([F32, F32, P, P, P], I32),

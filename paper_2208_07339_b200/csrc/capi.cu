@@ -423,6 +423,24 @@ int i8mm_llm_int8_matmul(const void* x, int64_t ldx, const void* w, int64_t ldw,
     return I8MM_OK;
 }
 
+// The whole call plus the reference's NaN/Inf rejection of both operands
+// (tensors.py:47-48) as one device word: X's flag from the scan, W's from one
+// check pass (OR). One entry instead of a host round trip per stage.
+int i8mm_llm_int8_matmul_checked(const void* x, int64_t ldx, const void* w, int64_t ldw, int64_t M,
+                                 int64_t K, int64_t N, float alpha, void* y, int64_t ldy, int out_kind,
+                                 void* workspace, size_t workspace_bytes, int32_t* o_count_dev,
+                                 int32_t* nonfinite_dev, void* stream) {
+    int s = i8mm_llm_int8_matmul(x, ldx, w, ldw, M, K, N, alpha, y, ldy, out_kind, workspace, workspace_bytes,
+                                 o_count_dev, stream);
+    if (s || nonfinite_dev == nullptr) return s;
+    void* base = reinterpret_cast<void*>(round_up(reinterpret_cast<intptr_t>(workspace), 256));
+    const Workspace ws = carve(base, M, K, N);
+    if (cudaMemcpyAsync(nonfinite_dev, ws.nonfinite, sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                        static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return I8MM_ERR_CUDA;
+    return i8mm_f16_check(w, K, N, ldw, nonfinite_dev, stream);
+}
+
 // ---------------------------------------------------------------- linear layer
 void i8mm_debug_set_pdl(int on) { g_pdl = on ? 1 : 0; }
 

@@ -389,6 +389,22 @@ def llm_int8_matmul(x, w, alpha: float = 6.0, out_dtype: torch.dtype = torch.flo
                                              ws.data_ptr(), ws.numel(), status.data_ptr(),
                                              stream_handle()), "llm_int8_matmul_f32")
         return MatmulResult(_f32_output(y, out_dtype, exact), "llm_int8", status[0:1], k)
+    if _timer is None:
+        # the whole call in one native entry (scan, row / column quantization, gathers,
+        # GEMM + dequant + outlier term, NaN/Inf flags): one host round trip
+        L = nat.lib()
+        kind, dt = _out_kind(out_dtype, exact)
+        ws = torch.empty((L.i8mm_llm_int8_workspace_size(m, k, n),), dtype=torch.uint8, device=xt.device)
+        y = torch.empty((m, n), dtype=dt, device=xt.device)
+        cnt = torch.empty((2,), dtype=torch.int32, device=xt.device)  # [|O|, nonfinite]
+        nat.check(L.i8mm_llm_int8_matmul_checked(xt.data_ptr(), xt.stride(0), wt.data_ptr(), wt.stride(0), m, k,
+                                                 n, float(alpha), y.data_ptr(), n, kind, ws.data_ptr(),
+                                                 ws.numel(), cnt.data_ptr(),
+                                                 cnt.data_ptr() + 4 if validate else None, stream_handle()),
+                  "llm_int8_matmul")
+        if validate:
+            raise_for_flags(nat.FLAG_NONFINITE if int(cnt[1].item()) else 0)
+        return MatmulResult(y, "llm_int8", cnt[0:1], k)
     scan = scan_outliers(xt, alpha)  # gemm.py:225 (+ the X NaN/Inf flag)
     if validate:
         _f16_check(wt, scan.nonfinite)
