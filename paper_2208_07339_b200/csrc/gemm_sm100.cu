@@ -559,7 +559,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 __ddiv_rn(static_cast<double>(static_cast<int32_t>(r[j])), d);
                             v[j] = __double2float_rn(q);
                         }
-                        if (n_out > 0) {
+                        if (n_out > 0 && stage_wo) {
+                            // the staged fp16 values (exact in f32 and f64): x[row, O] in
+                            // registers, W[O, tile] in shared memory, same ascending order
+                            const float* wrow = smem_wo + ch * 32;
+                            for (int j = 0; j < 32; ++j) {
+                                if (cbase + j >= n_live) break;
+                                double hacc = 0.0;
+                                for (int o = 0; o < n_out; ++o)
+                                    hacc = __dadd_rn(hacc, __dmul_rn(static_cast<double>(xo_r[o]),
+                                                                     static_cast<double>(wrow[o * TBN + j])));
+                                v[j] = __double2float_rn(__dadd_rn(static_cast<double>(v[j]), hacc));
+                            }
+                        } else if (n_out > 0) {
                             for (int j = 0; j < 32; ++j) {
                                 const int64_t c = cbase + j;
                                 if (c >= n_live) break;
