@@ -280,7 +280,8 @@ int decode_max_m() {
 }
 
 bool uses_decode(int64_t M, int64_t K, int64_t N) {
-    return M > 0 && M <= decode_max_m() && decode_fits(M, K, N);
+    // small weight matrices at 12 <= M <= 16 run faster through the swap-AB GEMM
+    return M > 0 && M <= decode_max_m() && decode_fits(M, K, N) && !swapab_route(M, K, N);
 }  // compacted outlier slice width (wider |O| reads X directly)
 
 // Per-call workspace. `linear` = weight-stationary layout: no WqT (it lives in

@@ -392,10 +392,14 @@ bool swapab_route(int64_t M, int64_t K, int64_t N) {
         g_swapab = (e && e[0] == '0') ? 0 : 1;
         const char* lo = getenv("I8MM_SWAPAB_MIN_M");  // A/B
         const char* hi = getenv("I8MM_SWAPAB_MAX_M");
-        min_m = (lo && lo[0]) ? atoi(lo) : 17;
+        min_m = (lo && lo[0]) ? atoi(lo) : 0;
         max_m = (hi && hi[0]) ? atoi(hi) : 64;
     }
-    if (g_swapab != 1 || M < min_m || M > max_m || M > 128 || K < sab::BK || N < 1 || (K % 16) != 0) return false;
+    // below 17 rows only small weight matrices (<= 32 MiB of codes), from 12 rows:
+    // measured against the decode kernel (qkvo 5120 x 5120: M = 12 / 16: 37.9 / 41.8 ->
+    // 36.9 us; fc1 / fc2 (105 MB) stay faster on the decode kernel up to M = 16)
+    const int64_t lo_m = min_m > 0 ? min_m : (K * N <= (32LL << 20) ? 12 : 17);
+    if (g_swapab != 1 || M < lo_m || M > max_m || M > 128 || K < sab::BK || N < 1 || (K % 16) != 0) return false;
     if (M <= 32 || max_m > 64) return true;
     return (N + 255) / 256 < num_sms() / 2;
 }

@@ -426,12 +426,16 @@ def decode_max(p):
     from paper_2208_07339_b200 import _native as nat
 
     L = nat.lib()
+    # the decode kernel itself (small weight matrices at 12 <= M <= 16 otherwise route
+    # to the swap-AB GEMM), and the row-tile GEMM when decode is switched off
+    L.i8mm_debug_set_swapab(0)
 
     def set_max(m):
         L.i8mm_debug_set_decode_max_m(m)
 
     yield set_max
     L.i8mm_debug_set_decode_max_m(16)
+    L.i8mm_debug_set_swapab(1)
 
 
 @pytest.mark.parametrize("case", [
