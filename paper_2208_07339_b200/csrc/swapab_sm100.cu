@@ -110,17 +110,12 @@ template <int MP>
 constexpr int b_bytes() { return MP * BK; }
 template <int MP>
 constexpr int stage_bytes() { return A_BYTES + b_bytes<MP>(); }
-template <int MP>
-constexpr size_t fixed_smem() {
-    return 1024 + static_cast<size_t>(MP) * (WO_CAP + 1) * sizeof(float) + sizeof(Bars) + 64;
-}
 
 template <int MP, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     swapab_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_p,
                   const __grid_constant__ CUtensorMap tmap_x, const Params p) {
     constexpr int NACC = n_acc<MP>();
-    constexpr int B_BYTES = b_bytes<MP>();
     constexpr int STAGE = stage_bytes<MP>();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
