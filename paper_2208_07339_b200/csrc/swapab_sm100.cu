@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* ring = smem;  // stage s: A (weights) then B (tokens)
     float* sxo = reinterpret_cast<float*>(ring + static_cast<size_t>(S) * STAGE);  // [MP][WO_CAP]
     float* srow = sxo + MP * WO_CAP;                                                 // [MP]
-    Bars* bars = reinterpret_cast<Bars*>(srow + MP);
+    float* swo = srow + MP;  // [WO_CAP][TILE_N] W[O, tile] of the current segment
+    Bars* bars = reinterpret_cast<Bars*>(swo + WO_CAP * TILE_N);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int num_kb = p.num_kb;
 
@@ -262,11 +263,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
             float wr[WO_CAP];
+            const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
+            if (!patch && n_o > 0 && n_o <= p.wo_cap && n0 + TILE_N <= p.N && (p.ldwo % 8) == 0) {
+                // W[O, tile] staged with 16-byte loads (two per thread), then read from
+                // shared memory: one load round trip instead of one per outlier row
+                named_bar_sync(1, 128);  // the previous segment's readers are done
+                for (int i = et; i < n_o * (TILE_N / 8); i += 128) {
+                    const int o = i / (TILE_N / 8), c8 = i - o * (TILE_N / 8);
+                    const uint4 q = *reinterpret_cast<const uint4*>(p.wo + static_cast<int64_t>(o) * p.ldwo + n0 + c8 * 8);
+                    const __half2* h2 = reinterpret_cast<const __half2*>(&q);
+                    float4* dst = reinterpret_cast<float4*>(swo + o * TILE_N + c8 * 8);
+                    const float2 f0 = __half22float2(h2[0]), f1 = __half22float2(h2[1]);
+                    const float2 f2 = __half22float2(h2[2]), f3 = __half22float2(h2[3]);
+                    dst[0] = make_float4(f0.x, f0.y, f1.x, f1.y);
+                    dst[1] = make_float4(f2.x, f2.y, f3.x, f3.y);
+                }
+                named_bar_sync(1, 128);
 #pragma unroll
-            for (int o = 0; o < WO_CAP; ++o)
-                wr[o] = (o < n_o && n_ok) ? (o < p.wo_cap ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + n])
-                                                          : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + n]))
-                                          : 0.0f;
+                for (int o = 0; o < WO_CAP; ++o) wr[o] = (o < n_o && n_ok) ? swo[o * TILE_N + et] : 0.0f;
+            } else {
+#pragma unroll
+                for (int o = 0; o < WO_CAP; ++o)
+                    wr[o] = (o < n_o && n_ok) ? (o < p.wo_cap ? __half2float(p.wo[static_cast<int64_t>(o) * p.ldwo + n])
+                                                              : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + n]))
+                                              : 0.0f;
+            }
             // split tile: first-unit holder finishes, the others hand over partials
             const uint32_t t0 = static_cast<uint32_t>(tile * num_kb), t1 = t0 + num_kb;
             const uint32_t cf = ((t0 + 1) * G - 1) / T;
@@ -366,7 +387,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 namespace {
 int sab_stages(int mp) {
     const size_t stage = static_cast<size_t>(sab::A_BYTES) + static_cast<size_t>(mp) * sab::BK;
-    const size_t fixed = 1024 + static_cast<size_t>(mp) * (sab::WO_CAP + 1) * sizeof(float) + sizeof(sab::Bars) + 64;
+    const size_t fixed = 1024 + static_cast<size_t>(mp) * (sab::WO_CAP + 1) * sizeof(float) +
+                         static_cast<size_t>(sab::WO_CAP) * sab::TILE_N * sizeof(float) + sizeof(sab::Bars) + 64;
     int s = static_cast<int>((sab::SMEM_LIMIT - fixed) / stage);
     return s > sab::MAX_STAGES ? sab::MAX_STAGES : s;
 }
@@ -472,7 +494,8 @@ cudaError_t launch_swapab(const GemmArgs& a, int32_t* c32, int32_t* tile_cnt, in
     const int64_t units = static_cast<int64_t>(prm.n_tiles) * prm.num_kb;
     const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
     const size_t smem = 1024 + static_cast<size_t>(prm.stages) * (sab::A_BYTES + mp * sab::BK) +
-                        static_cast<size_t>(mp) * (sab::WO_CAP + 1) * sizeof(float) + sizeof(sab::Bars) + 64;
+                        static_cast<size_t>(mp) * (sab::WO_CAP + 1) * sizeof(float) +
+                        static_cast<size_t>(sab::WO_CAP) * sab::TILE_N * sizeof(float) + sizeof(sab::Bars) + 64;
     switch (mp * 4 + epi) {
         case 32 * 4 + EPI_F16: return launch_sab<32, EPI_F16>(tw, tp, tx, prm, grid, smem, st);
         case 64 * 4 + EPI_F16: return launch_sab<64, EPI_F16>(tw, tp, tx, prm, grid, smem, st);
