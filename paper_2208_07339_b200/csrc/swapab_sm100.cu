@@ -403,14 +403,17 @@ int swapab_mp(int64_t M) { return M <= 32 ? 32 : (M <= 64 ? 64 : 128); }
 // row-tile GEMM would have fewer 256-column tiles than half the SMs; above that
 // the row-tile GEMM's overlapped epilogue wins. M <= 16 stays on the decode kernel.
 bool swapab_route(int64_t M, int64_t K, int64_t N) {
-    static int min_m = -1, max_m = -1;
+    static const int min_m = [] {  // A/B overrides, read once (independently of set_swapab)
+        const char* lo = getenv("I8MM_SWAPAB_MIN_M");
+        return (lo && lo[0]) ? atoi(lo) : 0;
+    }();
+    static const int max_m = [] {
+        const char* hi = getenv("I8MM_SWAPAB_MAX_M");
+        return (hi && hi[0]) ? atoi(hi) : 64;
+    }();
     if (g_swapab < 0) {
         const char* e = getenv("I8MM_SWAPAB");
         g_swapab = (e && e[0] == '0') ? 0 : 1;
-        const char* lo = getenv("I8MM_SWAPAB_MIN_M");  // A/B
-        const char* hi = getenv("I8MM_SWAPAB_MAX_M");
-        min_m = (lo && lo[0]) ? atoi(lo) : 0;
-        max_m = (hi && hi[0]) ? atoi(hi) : 64;
     }
     // below 17 rows only small weight matrices (<= 32 MiB of codes), from 12 rows:
     // measured against the decode kernel (qkvo 5120 x 5120: M = 12 / 16: 37.9 / 41.8 ->
