@@ -897,10 +897,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                 aw = n_ok ? __ldg(a.amax_full + n) : 127.0f;
             }
             float wr[WO_CAP];
+            const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
+            if (EPI != EPI_F32_EXACT && n_o > 0 && a.w_vec && n0 + TILE_N <= N) {
+                // W[O, tile] staged through the (idle) pdot area with 16-byte loads: one
+                // load round trip instead of one per outlier row
+                __half* sw = reinterpret_cast<__half*>(pdot);  // [WO_CAP][TILE_N]
+                named_bar_sync(1, 128);  // the previous segment's pdot readers are done
+                for (int i = et; i < n_o * (TILE_N / 8); i += 128) {
+                    const int o = i / (TILE_N / 8), c8 = i - o * (TILE_N / 8);
+                    *reinterpret_cast<uint4*>(sw + o * TILE_N + c8 * 8) = *reinterpret_cast<const uint4*>(
+                        a.w + static_cast<int64_t>(bars->o_s[o]) * a.ldw + n0 + c8 * 8);
+                }
+                named_bar_sync(1, 128);
 #pragma unroll
-            for (int o = 0; o < WO_CAP; ++o)
-                wr[o] = (EPI != EPI_F32_EXACT && o < n_o && n_ok)
-                            ? __half2float(a.w[static_cast<int64_t>(bars->o_s[o]) * a.ldw + n]) : 0.0f;
+                for (int o = 0; o < WO_CAP; ++o) wr[o] = (o < n_o && n_ok) ? __half2float(sw[o * TILE_N + n_local]) : 0.0f;
+            } else {
+#pragma unroll
+                for (int o = 0; o < WO_CAP; ++o)
+                    wr[o] = (EPI != EPI_F32_EXACT && o < n_o && n_ok)
+                                ? __half2float(a.w[static_cast<int64_t>(bars->o_s[o]) * a.ldw + n]) : 0.0f;
+            }
             // -- column fixup: patched when the cached maximiser row is an outlier row
             //    and the keep-row amax differs (weights.cu fixup_kernel semantics)
             if (et == 0) bars->n_ent = 0;
