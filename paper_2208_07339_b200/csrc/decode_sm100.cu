@@ -221,20 +221,44 @@ __device__ __noinline__ uint32_t codes16_fixup(uint32_t word, uint32_t bad, uint
 
 __device__ __forceinline__ uint4 codes16(const uint4& lo, const uint4& hi, uint32_t mbits, int64_t k0,
                                          int64_t K, float s32, double s) {
+    // packed f32x2 arithmetic (FMUL2 / FADD2, round-to-nearest per lane: the same
+    // values as the scalar form), code bytes gathered with byte permutes: the low
+    // byte of t = pf + 1.5 * 2^23 is rint(pf) as two's complement
     constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: t - kMagic = rint(pf)
+    constexpr float kTie = 0.5f - 6.103515625e-05f;
     const int lim = K - k0 < 16 ? static_cast<int>(K - k0) : 16;
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    uint32_t zmask = mbits & 0xFFFFu;  // bit e: code e is 0 (outlier column or past K)
+    if (lim < 16) zmask |= (0xFFFFu << (lim > 0 ? lim : 0)) & 0xFFFFu;
+    const uint32_t hw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    const float2 s2 = make_float2(s32, s32), mg = make_float2(kMagic, kMagic), nmg = make_float2(-kMagic, -kMagic);
+    uint32_t tb[16];
     uint32_t bad = 0;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-        const float x = hbits_to_float(half_bits(e < 8 ? lo : hi, e & 7));
-        const float pf = x * s32;
-        const float t = pf + kMagic;
-        const float r = t - kMagic;
-        const bool zero = ((mbits >> e) & 1u) || e >= lim;
-        const uint32_t c = zero ? 0u : (static_cast<uint32_t>(__float_as_int(t) - 0x4B400000) & 0xFFu);
-        bad |= (!zero && !(fabsf(pf - r) < 0.5f - 6.103515625e-05f)) ? (1u << e) : 0u;
-        w[e >> 2] |= c << ((e & 3) * 8);
+    for (int q = 0; q < 8; ++q) {
+        const float2 x2 = __half22float2(*reinterpret_cast<const __half2*>(&hw[q]));
+        const float2 pf = __fmul2_rn(x2, s2);
+        const float2 t = __fadd2_rn(pf, mg);
+        const float2 r = __fadd2_rn(t, nmg);
+        const float2 d = __fadd2_rn(pf, make_float2(-r.x, -r.y));
+        tb[2 * q] = __float_as_uint(t.x);
+        tb[2 * q + 1] = __float_as_uint(t.y);
+        bad |= (fabsf(d.x) < kTie ? 0u : 1u) << (2 * q);
+        bad |= (fabsf(d.y) < kTie ? 0u : 1u) << (2 * q + 1);
+    }
+    bad &= ~zmask;
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t p01 = __byte_perm(tb[4 * q], tb[4 * q + 1], 0x0040);
+        const uint32_t p23 = __byte_perm(tb[4 * q + 2], tb[4 * q + 3], 0x0040);
+        w[q] = __byte_perm(p01, p23, 0x5410);
+    }
+    if (zmask) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t z4 = (zmask >> (4 * q)) & 0xFu;
+            w[q] &= ~(((z4 * 0x00204081u) & 0x01010101u) * 0xFFu);
+        }
     }
     if (bad) {
 #pragma unroll
