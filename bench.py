@@ -1,7 +1,7 @@
 """Benchmark of the B200 LLM.int8() linear layer (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cfg5_fc1|cfg5_fc2|cfg5_ffn|cfg2|cfg4_fc1|cfg3_decode|cfg1]
+                    [--workload cfg5_fc1|cfg5_fc2|cfg5_ffn|cfg2|cfg4_fc1|cfg3_decode|cfg3_decode_qkv|cfg1]
 
 A step is one pass of the hot path over one batch: the LLM.int8() matmul of
 each layer of the workload through the public module ``Int8Linear`` (or
@@ -49,7 +49,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "LLM.int8() matmul TOPS and tokens/s at OPT FFN shapes; % of INT8 tensor peak"
 INT8_PEAK_NOMINAL_TOPS = 4500.0  # B200 dense INT8 (datasheet; 9 POPS is the 2:4-sparse figure)
 DEFAULT_WORKLOAD = "cfg5_fc1"
-DEFAULT_EXTRAS = ("cfg5_fc2", "cfg2", "cfg4_fc1", "cfg3_decode")
+DEFAULT_EXTRAS = ("cfg5_fc2", "cfg2", "cfg4_fc1", "cfg3_decode", "cfg3_decode_qkv")
 
 WORKLOADS = {
     "cfg5_fc1": {
@@ -88,6 +88,14 @@ WORKLOADS = {
                 "configs[2]): q, k, v, o 5120->5120, fc1 5120->20480, fc2 20480->5120; M = 8 "
                 "(single-launch decode kernel), weights 314 MB > L2",
         "layers": [(8, 5120, 5120)] * 4 + [(8, 5120, 20480), (8, 20480, 5120)],
+        "decode": True,
+    },
+    "cfg3_decode_qkv": {
+        "desc": "the cfg3 decode step with q, k, v as one 5120->15360 weight-stationary layer "
+                "(they read the same hidden state, so one call computes the same outlier set, "
+                "row scales and bitwise the same outputs as three; "
+                "test_fused_qkv_matches_three_projections): qkv, o, fc1, fc2 at M = 8",
+        "layers": [(8, 5120, 15360), (8, 5120, 5120), (8, 5120, 20480), (8, 20480, 5120)],
         "decode": True,
     },
 }

@@ -234,3 +234,24 @@ def test_cfg3_decode_projections_vs_oracle(p, oracle_mod, proj, m):
     assert np.array_equal(_np(lin.matmul(x16, exact=True)), ref.output)
     assert lin.last_stats()["decomposed_cols"] == len(ref.dims)
     _check_fp16(_np(lin(x16)), ref.output)
+
+
+@pytest.mark.parametrize("m", [1, 8, 16])
+def test_fused_qkv_matches_three_projections(p, m):
+    """bench.py's cfg3_decode_qkv workload: q, k, v read the same hidden state, so
+    one layer over the concatenated weight [W_q | W_k | W_v] (5120 -> 15360)
+    computes the same outlier set and row scales as three calls, and per-column
+    weight scales are independent of the neighbours: the outputs are bitwise the
+    three separate layers' (fp16 and exact mode, decode kernel at every M here)."""
+    from paper_2208_07339_b200.synthetic import planted_pair_device
+
+    k, n = 5120, 5120
+    x, _, _ = planted_pair_device(m, k, 8, 6, 20.0, seed=11)
+    ws = [planted_pair_device(1, k, n, 0, 1.0, seed=20 + i)[1] for i in range(3)]
+    fused = p.Int8Linear(torch.cat(ws, dim=1), alpha=6.0)
+    sep = [p.Int8Linear(w, alpha=6.0) for w in ws]
+    y = fused(x)
+    y_ex = fused.matmul(x, exact=True)
+    for i, lin in enumerate(sep):
+        assert torch.equal(y[:, i * n:(i + 1) * n], lin(x))
+        assert torch.equal(y_ex[:, i * n:(i + 1) * n], lin.matmul(x, exact=True))
