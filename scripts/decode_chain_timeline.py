@@ -68,7 +68,7 @@ cols = [(0, "start", min), (0, "start (last CTA)", max), (1, "waited", max), (2,
         (17, "w4 prefetch done", max), (28, "w4 codes done", max), (32, "t0 item0 start", max), (33, "t0 item0 codes", max), (34, "t0 item1 start", max), (18, "lead writes", max), (4, "panels ready", max), (5, "1st MMA", max),
         (6, "MMA issued", max)] + [(19, "setup: bars+W", max), (20, "setup: pdl wait", max), (21, "setup: X issued", max),
         (22, "setup: L2 pf+dst", max), (23, "setup: tmem alloc", max), (24, "setup: cand loads", max),
-        (25, "setup: zeroing", max)] + [ (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]
+        (25, "setup: zeroing", max)] + [(35, "epi seg loop", max), (38, "epi W[O] staged", max), (37, "contrib release", max), (36, "fin spin done", max), (7, "1st tmem_full", max), (8, "epi done", max), (9, "end", max)]
 print("us from layer q's prep start (min or max over CTAs); CTAs per layer:", [int((g[:, 0] > 0).sum()) for g in G])
 print(f"{'':18s}" + "".join(f"{n:>8s}" for n in names))
 med = lambda v: v.median()
@@ -85,7 +85,9 @@ for name, g in zip(names, G):
         if end[c] <= 0:
             continue
         rows.append(f"cta {c:3d} end {(end[c] - t0) / 1e3:6.2f} 1st-tmem {(g[c, 7] - t0) / 1e3:6.2f} "
-                    f"ents {[int(g[c, 26 + k]) for k in range(3)]} roles {[int(g[c, 29 + k]) for k in range(3)]}")
+                    f"ents {[int(g[c, 26 + k]) for k in range(2)]} roles {[int(g[c, 29 + k]) for k in range(3)]} "
+                    f"seg-loop {(g[c, 35] - t0) / 1e3:6.2f} W[O] {(g[c, 38] - t0) / 1e3:6.2f} spin {(g[c, 36] - t0) / 1e3:6.2f} "
+                    f"MMA-issued {(g[c, 6] - t0) / 1e3:6.2f} 1stMMA {(g[c, 5] - t0) / 1e3:6.2f}")
     print(name, "latest:"); [print("   ", r) for r in rows]
     ents = g[:, 26:29].sum(1)
     print("    median end (no patched) {:.2f} / (patched) {:.2f}".format(
