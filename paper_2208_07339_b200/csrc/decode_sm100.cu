@@ -892,6 +892,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (L > 0 && static_cast<uint32_t>(u_begin) != t0 && cf0 / CL == clu) arrived = false;
         }
         if (arrived) cluster_arrive_release();
+        if (et == 0) DSTAMP(p.dbg, 35);
         int seg = 0;
         for (int u = u_begin; u < u_end; ++seg) {
             const int tile = u / num_kb;
@@ -935,6 +936,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 named_bar_sync(1, 128);
 #pragma unroll
                 for (int o = 0; o < WO_CAP; ++o) wr[o] = (o < n_o && n_ok) ? __half2float(sw[o * TILE_N + n_local]) : 0.0f;
+                if (et == 0 && seg == 0) DSTAMP(p.dbg, 38);
             } else {
 #pragma unroll
                 for (int o = 0; o < WO_CAP; ++o)
@@ -1063,6 +1065,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // thread 0's acquire + the barrier order every thread's loads after the
                 // contributors' release (no per-thread fence)
                 named_bar_sync(1, 128);
+                if (et == 0 && seg == 0) DSTAMP(p.dbg, 36);
                 for (uint32_t c = cl - fin_cross + 1; c <= cl; ++c) {
                     const int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
 #pragma unroll
@@ -1108,6 +1111,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // (cumulativity), as a per-thread fence would, at one GPU-scope op
                 named_bar_sync(1, 128);
                 if (et == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.tile_cnt + tile) : "memory");
+                if (et == 0) DSTAMP(p.dbg, 37);
                 continue;
             }
             if (kDevStamps && et == 0 && p.dbg != nullptr) p.dbg[blockIdx.x * 64 + 29 + min(seg, 2)] = full ? 2 : (cf != blockIdx.x ? 0 : 1);
