@@ -184,10 +184,10 @@ int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, in
  * launch; with the split entries, i8mm_linear_prologue only records alpha and
  * i8mm_linear_gemm runs the kernel. Outputs are bit-identical to the prefill
  * kernels. The workspace layout depends on the routing, so set max_m before
- * sizing a workspace. A decode-routed workspace carries per-tile arrival
- * counters that must be zero when it is first used: call
- * i8mm_linear_workspace_init once after allocating it (every decode call
- * leaves them zero; one workspace per stream). */
+ * sizing a workspace. A decode-routed workspace carries split-tile partial
+ * slots that must be empty (and per-tile counters zero) when it is first used:
+ * call i8mm_linear_workspace_init once after allocating it (every decode call
+ * leaves them so; one workspace per stream). */
 int i8mm_linear_workspace_init(void* workspace, size_t workspace_bytes, int64_t M, int64_t K, int64_t N,
                                void* stream);
 /* Patched-column list of the last decode-routed call on this workspace

@@ -323,8 +323,8 @@ Workspace carve(void* base, int64_t M, int64_t K, int64_t N, bool linear = false
             w.c32_words = grid * 16 * 128;
             w.c32 = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(w.c32_words)));
             w.n_tiles = (N + 127) / 128;
-            // per-tile arrival counters: zero when the workspace is first used
-            // (i8mm_linear_workspace_init), left zero by every decode call
+            // split-tile partial slots (above) start empty and per-tile counters
+            // zero (i8mm_linear_workspace_init); every decode call leaves them so
             w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (w.n_tiles + 2)));
             w.thr_word = reinterpret_cast<uint32_t*>(w.tile_cnt + w.n_tiles + 1);
             w.wq_p = reinterpret_cast<int8_t*>(take(static_cast<size_t>(128 * w.ldq)));  // patch tile rows
@@ -770,8 +770,12 @@ int i8mm_linear_workspace_init(void* workspace, size_t workspace_bytes, int64_t 
     Workspace ws;
     if (int s = linear_ws(workspace, workspace_bytes, M, K, N, &ws)) return s;
     if (!ws.decode) return I8MM_OK;  // the prefill routing zeroes its counters every call
-    return cuda_status(cudaMemsetAsync(ws.tile_cnt, 0, sizeof(int32_t) * (ws.n_tiles + 2),
-                                       static_cast<cudaStream_t>(stream)));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // split-tile partial slots start empty (byte 0x80: dec::kPartEmpty); every
+    // decode call leaves them empty and its counters zero
+    if (cudaMemsetAsync(ws.c32, 0x80, sizeof(int32_t) * static_cast<size_t>(ws.c32_words), st) != cudaSuccess)
+        return I8MM_ERR_CUDA;
+    return cuda_status(cudaMemsetAsync(ws.tile_cnt, 0, sizeof(int32_t) * (ws.n_tiles + 2), st));
 }
 
 int i8mm_linear_patch_stats(const void* w, int64_t ldw, const void* wbuf, int64_t M, int64_t K, int64_t N,

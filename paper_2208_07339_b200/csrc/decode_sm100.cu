@@ -173,6 +173,20 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 __device__ __forceinline__ uint64_t weight_policy(int mode) {
     return mode == 0 ? l2_policy_evict_first() : l2_policy_evict_normal();
 }
+// Cross-cluster split-tile partials are self-validating: a slot word holds
+// kPartEmpty until its contributor stores the sum (|sum| <= 127 * 127 * K <
+// 2^31 - kPartEmpty's magnitude for K <= 131072, so no sum equals it), and the
+// finisher puts kPartEmpty back after reading. No flag, fence or barrier: the
+// finisher polls the data words themselves (relaxed, single-copy atomic).
+constexpr int32_t kPartEmpty = static_cast<int32_t>(0x80808080u);  // byte-memset pattern 0x80
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1055,23 +1069,31 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) xpart[jj] = 0u;
             if (!full && cf == blockIdx.x && fin_cross > 0) {
-                if (et == 0) {
-                    // bounded: a workspace whose counters were never zeroed traps
-                    // instead of hanging the GPU
-                    for (uint32_t spin = 0; ld_acquire(a.tile_cnt + tile) < fin_cross; ++spin)
-                        if (spin > (1u << 22)) __trap();
-                    a.tile_cnt[tile] = 0;
-                }
-                // thread 0's acquire + the barrier order every thread's loads after the
-                // contributors' release (no per-thread fence)
-                named_bar_sync(1, 128);
-                if (et == 0 && seg == 0) DSTAMP(p.dbg, 36);
+                // each thread polls its own words of the contributors' slots until none
+                // is kPartEmpty (bounded: a workspace never initialised traps instead
+                // of hanging the GPU), then empties them for the next call
+                const uint32_t need = (1u << M) - 1u;
                 for (uint32_t c = cl - fin_cross + 1; c <= cl; ++c) {
-                    const int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
+                    int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
+                    uint32_t got = 0;
+                    for (uint32_t spin = 0; got != need; ++spin) {
+                        int32_t v[16];
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            v[jj] = (jj < M && !((got >> jj) & 1u)) ? ld_relaxed(src + jj * TILE_N) : kPartEmpty;
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            if (v[jj] != kPartEmpty) {
+                                xpart[jj] += static_cast<uint32_t>(v[jj]);
+                                got |= 1u << jj;
+                            }
+                        if (spin > (1u << 22)) __trap();
+                    }
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj)
-                        if (jj < M) xpart[jj] += static_cast<uint32_t>(__ldcg(src + jj * TILE_N));
+                        if (jj < M) st_relaxed(src + jj * TILE_N, kPartEmpty);
                 }
+                if (et == 0 && seg == 0) DSTAMP(p.dbg, 36);
             }
             mbar_wait(&bars->tmem_full[acc], (seg >> 1) & 1);
             tc_fence_after();
@@ -1103,14 +1125,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 continue;
             }
             if (!full && cf != blockIdx.x) {
+                // self-validating partial words (kPartEmpty): no flag, no barrier
                 int32_t* slotp = a.c32 + static_cast<int64_t>(blockIdx.x) * (MAX_M * TILE_N) + n_local;
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj)
-                    if (jj < M) __stcg(slotp + jj * TILE_N, static_cast<int32_t>(r[jj]));
-                // the barrier orders every thread's stores before thread 0's release
-                // (cumulativity), as a per-thread fence would, at one GPU-scope op
-                named_bar_sync(1, 128);
-                if (et == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.tile_cnt + tile) : "memory");
+                    if (jj < M) st_relaxed(slotp + jj * TILE_N, static_cast<int32_t>(r[jj]));
                 if (et == 0) DSTAMP(p.dbg, 37);
                 continue;
             }

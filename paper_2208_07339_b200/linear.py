@@ -138,8 +138,8 @@ class Int8Linear(torch.nn.Module):
     def workspace(self, m: int) -> torch.Tensor:
         """A workspace for an M-row call. Prefill routing: a fresh buffer.
         Decode routing: cached per (M, stream), initialised once
-        (``i8mm_linear_workspace_init``: its per-tile arrival counters must be
-        zero on first use; every decode call leaves them zero). A workspace
+        (``i8mm_linear_workspace_init``: its split-tile partial slots must be
+        empty on first use; every decode call leaves them so). A workspace
         first created while a CUDA graph is being captured puts that
         initialisation into the graph; ``GraphedCall`` captures on its warm-up
         stream so the graph holds only the layer kernels."""
