@@ -187,7 +187,8 @@ int i8mm_linear_forward(const void* x, int64_t ldx, int64_t M, const void* w, in
  * sizing a workspace. A decode-routed workspace carries split-tile partial
  * slots that must be empty (and per-tile counters zero) when it is first used:
  * call i8mm_linear_workspace_init once after allocating it (every decode call
- * leaves them so; one workspace per stream). */
+ * leaves them so; one workspace per stream and per (M, K, N): the slots' offset
+ * depends on the shape, so re-initialise a buffer before using it for another). */
 int i8mm_linear_workspace_init(void* workspace, size_t workspace_bytes, int64_t M, int64_t K, int64_t N,
                                void* stream);
 /* Patched-column list of the last decode-routed call on this workspace
