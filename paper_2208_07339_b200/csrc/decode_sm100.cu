@@ -1072,26 +1072,36 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // each thread polls its own words of the contributors' slots until none
                 // is kPartEmpty (bounded: a workspace never initialised traps instead
                 // of hanging the GPU), then empties them for the next call
-                const uint32_t need = (1u << M) - 1u;
-                for (uint32_t c = cl - fin_cross + 1; c <= cl; ++c) {
-                    int32_t* src = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
+                // two contributors' slots per polling round (their words in flight together)
+                const uint32_t need1 = (1u << M) - 1u;
+                for (uint32_t c = cl - fin_cross + 1; c <= cl; c += 2) {
+                    const bool two = c + 1 <= cl;
+                    int32_t* src0 = a.c32 + static_cast<int64_t>(c) * (MAX_M * TILE_N) + n_local;
+                    int32_t* src1 = src0 + MAX_M * TILE_N;
+                    const uint32_t need = need1 | (two ? need1 << 16 : 0u);
                     uint32_t got = 0;
                     for (uint32_t spin = 0; got != need; ++spin) {
-                        int32_t v[16];
+                        int32_t v[32];
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj)
-                            v[jj] = (jj < M && !((got >> jj) & 1u)) ? ld_relaxed(src + jj * TILE_N) : kPartEmpty;
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const int row = jj & 15;
+                            v[jj] = ((need >> jj) & 1u) && !((got >> jj) & 1u)
+                                        ? ld_relaxed((jj < 16 ? src0 : src1) + row * TILE_N) : kPartEmpty;
+                        }
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj)
+                        for (int jj = 0; jj < 32; ++jj)
                             if (v[jj] != kPartEmpty) {
-                                xpart[jj] += static_cast<uint32_t>(v[jj]);
+                                xpart[jj & 15] += static_cast<uint32_t>(v[jj]);
                                 got |= 1u << jj;
                             }
                         if (spin > (1u << 22)) __trap();
                     }
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj)
-                        if (jj < M) st_relaxed(src + jj * TILE_N, kPartEmpty);
+                        if (jj < M) {
+                            st_relaxed(src0 + jj * TILE_N, kPartEmpty);
+                            if (two) st_relaxed(src1 + jj * TILE_N, kPartEmpty);
+                        }
                 }
                 if (et == 0 && seg == 0) DSTAMP(p.dbg, 36);
             }
