@@ -937,7 +937,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             float wr[WO_CAP];
             const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
-            if (EPI != EPI_F32_EXACT && n_o > 0 && a.w_vec && n0 + TILE_N <= N) {
+            // a contributor segment (not full, tile started by another CTA) hands raw
+            // partials over: it needs no W[O, tile]
+            const bool contrib_seg = !full && ((static_cast<uint32_t>(tile * num_kb) + 1) * Gu - 1) / T != blockIdx.x;
+            if (contrib_seg) {
+#pragma unroll
+                for (int o = 0; o < WO_CAP; ++o) wr[o] = 0.0f;
+            } else if (EPI != EPI_F32_EXACT && n_o > 0 && a.w_vec && n0 + TILE_N <= N) {
                 // W[O, tile] staged through the (idle) pdot area with 16-byte loads: one
                 // load round trip instead of one per outlier row
                 __half* sw = reinterpret_cast<__half*>(pdot);  // [WO_CAP][TILE_N]
