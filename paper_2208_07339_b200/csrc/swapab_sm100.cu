@@ -262,9 +262,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                 aw = n_ok ? p.patch_amax[pi] : 127.0f;
             }
             const float colf = amax_or_127(aw) * (1.0f / 16129.0f);
+            // split tile: first-unit holder finishes, the others hand over partials
+            const uint32_t t0 = static_cast<uint32_t>(tile * num_kb), t1 = t0 + num_kb;
+            const uint32_t cf = ((t0 + 1) * G - 1) / T;
+            const uint32_t cl = (t1 * G - 1) / T;
+            const bool finisher = !full && cf == blockIdx.x;
             float wr[WO_CAP];
             const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
-            if (!patch && n_o > 0 && n_o <= p.wo_cap && n0 + TILE_N <= p.N && (p.ldwo % 8) == 0) {
+            if (!full && !finisher) {  // contributor: raw partials only, no outlier term
+#pragma unroll
+                for (int o = 0; o < WO_CAP; ++o) wr[o] = 0.0f;
+            } else if (!patch && n_o > 0 && n_o <= p.wo_cap && n0 + TILE_N <= p.N && (p.ldwo % 8) == 0) {
                 // W[O, tile] staged with 16-byte loads (two per thread), then read from
                 // shared memory: one load round trip instead of one per outlier row
                 named_bar_sync(1, 128);  // the previous segment's readers are done
@@ -288,11 +296,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                               : __half2float(p.w[static_cast<int64_t>(p.o_idx[o]) * p.ldw + n]))
                                               : 0.0f;
             }
-            // split tile: first-unit holder finishes, the others hand over partials
-            const uint32_t t0 = static_cast<uint32_t>(tile * num_kb), t1 = t0 + num_kb;
-            const uint32_t cf = ((t0 + 1) * G - 1) / T;
-            const uint32_t cl = (t1 * G - 1) / T;
-            const bool finisher = !full && cf == blockIdx.x;
             if (et == 0 && seg < 3) stamp(p, 5 + seg);  // epilogue reaches the segment
             if (finisher) {
                 if (et == 0) {
