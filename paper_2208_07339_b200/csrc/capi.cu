@@ -533,7 +533,6 @@ static DecodeArgs decode_args(const Workspace& ws, const WeightBuf& b, const __h
     d.cand_r = b.cand_r;
     d.q2 = b.q2;
     d.c32 = ws.c32;
-    d.tile_cnt = ws.tile_cnt;
     d.y = y;
     d.ldy = ldy;
     return d;

@@ -187,11 +187,6 @@ __device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
 __device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // Weight-stationary column fixup (weights.cu fixup_kernel semantics, quantize.py:
 // 182-187 on w[keep, :]) for a column whose cached maximiser row cr[0] is an

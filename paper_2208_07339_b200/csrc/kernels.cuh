@@ -221,8 +221,8 @@ struct DecodeArgs {
     const uint16_t* cand_v;
     const int32_t* cand_r;
     const int8_t* q2;     // N x ldq second-candidate codes (weight buffer)
-    int32_t* c32;         // [grid] x [16 x 128] split-tile partial slots
-    int32_t* tile_cnt;    // [n_tiles] arrival counters: zero on first use, reset by the finishers
+    int32_t* c32;         // [grid] x [16 x 128] split-tile partial slots: empty (0x80 bytes) on
+                          // first use, emptied again by the finishers
     void* y;
     int64_t ldy;
 };
