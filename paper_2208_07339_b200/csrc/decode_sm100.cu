@@ -834,62 +834,74 @@ __global__ void __launch_bounds__(THREADS, 1)
             __syncwarp();
         }
         if (lane == 0) DSTAMP(p.dbg, 6);
-    } else if (warp >= 4) {
-        // ---------------- epilogue: thread = weight row n of the tile
-        const int et = tid - 128;
-        // the sorted outlier list (only the epilogue reads it): off the token
-        // phase's critical path, while the producer and the MMA warp start
-        compact_mask(smask, nwords, bars, lead && crank == 0 ? a.o_idx : nullptr, et, 128, 1);
-        if (lead && crank == 0 && et == 0) {
+    } else if (warp == 2 || warp == 3) {
+        // ---------------- idle warps 2-3: the sorted outlier list (and the lead CTA's O
+        // outputs), L2 prefetches of W[O, tile], x[:, O] into shared memory; the
+        // epilogue waits for them (named barrier 4) only before its first finishing
+        // segment, so a leading contributor segment hands its partials over first
+        const int t = tid - 64;
+        compact_mask(smask, nwords, bars, lead && crank == 0 ? a.o_idx : nullptr, t, 64, 3);
+        if (lead && crank == 0 && t == 0) {
             *a.o_count = bars->n_out;
             uint32_t any = 0;  // every rank's NaN/Inf flag landed before barrier 1
             for (int q = 0; q < CL; ++q) any |= bars->nonfinite[q];
             if (a.nonfinite != nullptr) *a.nonfinite = any ? 1 : 0;
         }
         const int n_out = bars->n_out;
-        const int n_o = n_out <= WO_CAP ? n_out : 0;  // x[:, O] factors staged in smem
-    // the epilogue's global data, pulled into L2 while the first MMAs run:
-    // W[O, tile] (256 B per outlier row and segment) and, for each patched
-    // column, the cached q2 codes over the segment's k-range
-    const int n_o0 = min(bars->n_out, WO_PRE_L2);
-    int u = u_begin;
-#pragma unroll
-    for (int sg = 0; sg < NSEG_PRE; ++sg) {
-        const int tile = u / num_kb;
-        const int seg_end = min(u_end, (tile + 1) * num_kb);
-        if (u < u_end) {
-            if (et < n_o0) {
+        const int n_o = n_out <= WO_CAP ? n_out : 0;
+        const int n_o0 = min(n_out, WO_PRE_L2);
+        int u = u_begin;
+        for (int sg = 0; sg < NSEG_PRE && u < u_end; ++sg) {
+            const int tile = u / num_kb;
+            if (t < n_o0) {
                 const int64_t n0 = static_cast<int64_t>(tile) * TILE_N;
                 const int64_t cols = min(static_cast<int64_t>(TILE_N), N - n0);
                 const uint32_t bytes = static_cast<uint32_t>(cols * 2) & ~15u;
                 if (bytes && a.w_vec)
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                                     a.w + static_cast<int64_t>(bars->o_s[et]) * a.ldw + n0),
+                                     a.w + static_cast<int64_t>(bars->o_s[t]) * a.ldw + n0),
                                  "r"(bytes)
                                  : "memory");
             }
-            const int64_t n = static_cast<int64_t>(tile) * TILE_N + et;
-            if (n < N && pre_cr[sg][0] >= 0 && bit_of(smask, pre_cr[sg][0])) {
-                int src;
-                const float an = fixup_amax(pre_cr[sg], pre_cv[sg], smask, src);
-                if (src == 1 && an != pre_aw[sg]) {
-                    const int k_lo = (u % num_kb) * BK, k_hi = min((seg_end - 1) % num_kb + 1, num_kb) * BK;
-                    if (k_hi > k_lo)
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.q2 + n * a.ldq + k_lo),
-                                     "r"(static_cast<uint32_t>(k_hi - k_lo))
-                                     : "memory");
-                }
-            }
+            u = min(u_end, (tile + 1) * num_kb);
         }
-        u = seg_end;
-    }
-
-        const int n_local = et;
-        const int quad = warp & 3;
-        for (int i = et; i < static_cast<int>(M) * n_o; i += 128) {
+        for (int i = t; i < static_cast<int>(M) * n_o; i += 64) {
             const int m = i / n_o, o = i - m * n_o;
             sxo[m * WO_CAP + o] = __half2float(a.x[m * a.ldx + bars->o_s[o]]);
         }
+        asm volatile("bar.arrive 4, 192;" ::: "memory");
+    } else if (warp >= 4) {
+        // ---------------- epilogue: thread = weight row n of the tile
+        const int et = tid - 128;
+        // the patched columns' cached q2 rows -> L2 while the first MMAs run
+        // (the outlier list, W[O, tile] prefetches and x[:, O] are warps 2-3's)
+        {
+            int u = u_begin;
+#pragma unroll
+            for (int sg = 0; sg < NSEG_PRE; ++sg) {
+                const int tile = u / num_kb;
+                const int seg_end = min(u_end, (tile + 1) * num_kb);
+                if (u < u_end) {
+                    const int64_t n = static_cast<int64_t>(tile) * TILE_N + et;
+                    if (n < N && pre_cr[sg][0] >= 0 && bit_of(smask, pre_cr[sg][0])) {
+                        int src;
+                        const float an = fixup_amax(pre_cr[sg], pre_cv[sg], smask, src);
+                        if (src == 1 && an != pre_aw[sg]) {
+                            const int k_lo = (u % num_kb) * BK, k_hi = min((seg_end - 1) % num_kb + 1, num_kb) * BK;
+                            if (k_hi > k_lo)
+                                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.q2 + n * a.ldq + k_lo),
+                                             "r"(static_cast<uint32_t>(k_hi - k_lo))
+                                             : "memory");
+                        }
+                    }
+                }
+                u = seg_end;
+            }
+        }
+        int n_out = 0, n_o = 0;
+        bool o_ready = false;  // warps 2-3's outlier list (named barrier 4)
+        const int n_local = et;
+        const int quad = warp & 3;
         // closing barrier, split: a CTA adds into a peer's shared memory only in its
         // first segment, and only when that segment continues a tile an earlier CTA of
         // this cluster started; every other epilogue thread arrives right away (the
@@ -935,6 +947,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             // a contributor segment (not full, tile started by another CTA) hands raw
             // partials over: it needs no W[O, tile]
             const bool contrib_seg = !full && ((static_cast<uint32_t>(tile * num_kb) + 1) * Gu - 1) / T != blockIdx.x;
+            if (!contrib_seg && !o_ready) {
+                named_bar_sync(4, 192);
+                o_ready = true;
+                n_out = bars->n_out;
+                n_o = n_out <= WO_CAP ? n_out : 0;
+            }
             if (contrib_seg) {
 #pragma unroll
                 for (int o = 0; o < WO_CAP; ++o) wr[o] = 0.0f;
@@ -1164,6 +1182,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
         }
+        if (!o_ready) named_bar_sync(4, 192);  // pairs warps 2-3's arrive
         if (!arrived) cluster_arrive_release();
         if (et == 0) DSTAMP(p.dbg, 8);
     }
